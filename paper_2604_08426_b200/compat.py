@@ -1,0 +1,382 @@
+"""Drop-in mirror of the reference's decode-path Python API (kvlab).
+
+Same names, argument meanings, return types and ValueError conditions as
+kvlab's ``build_store`` (kvstore.py:354-385), ``select_by_landmarks``
+(selection.py:72-87), ``approx_topk_residual`` (selection.py:132-171),
+``residual_scores`` (:114-129), ``oracle_select`` (:90-111), ``recall``
+(:174-180), ``sparse_attention`` / ``full_attention_heads``
+(attention.py:48-90) and the result types -- but every score, top-k, gather
+and attention runs in libkvb's sm_100a kernels (through ``store.DeviceStore``,
+batch 1). numpy in / numpy out, exactly like the reference, so
+``harness.run_grid_point`` can be pointed at this module.
+
+Extensions: ``build_store(..., dtype=torch.bfloat16)`` keeps K/V/landmarks
+in bf16 on the device; ``svd_concat=True`` applies an SVD slow tier to the
+head-concatenated [n, Hkv*D] keys (ShadowKV).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from .schemes import (HIGGS, NONE, SVD, SchemeDescriptor, bits_per_key as _bits_per_key,
+                      scheme_none)
+from .store import DeviceStore
+
+
+def as_f32(x, name: str = "tensor") -> np.ndarray:
+    """numerics.py:25-29."""
+    arr = np.asarray(x, dtype=np.float32)
+    if not np.all(np.isfinite(arr)):
+        raise ValueError(f"{name} contains non-finite values")
+    return np.ascontiguousarray(arr)
+
+
+@dataclass(frozen=True)
+class BudgetConfig:
+    """kvstore.py:32-44."""
+
+    sparse_fraction: float = 0.0156
+    outlier_tokens: int = 384
+    local_window: int = 32
+
+    def __post_init__(self):
+        if not 0 < self.sparse_fraction <= 1:
+            raise ValueError(f"sparse_fraction {self.sparse_fraction} not in (0, 1]")
+        if self.outlier_tokens < 0 or self.local_window < 0:
+            raise ValueError("outlier_tokens and local_window must be >= 0")
+
+
+@dataclass(frozen=True)
+class SelectionResult:
+    """selection.py:18-30."""
+
+    chunk_ids: tuple
+    token_ids: np.ndarray
+    scores: np.ndarray
+    loaded_fraction: float
+
+
+@dataclass(frozen=True)
+class AttentionOutput:
+    """attention.py:19-23."""
+
+    output: np.ndarray
+    tokens_used: int
+    rel_error_vs_full: float | None
+
+
+@dataclass
+class TierTraffic:
+    """kvstore.py:47-50."""
+
+    tokens_loaded_from_slow_tier: int
+    fast_tier_resident_bits: Fraction
+
+
+def _heads3(arr, name):
+    a = as_f32(arr, name)
+    if a.ndim == 2:
+        a = a[None]
+    if a.ndim != 3:
+        raise ValueError(f"{name} must be [n, D] or [heads, n, D], got shape {a.shape}")
+    return a
+
+
+def normalize_queries(queries, n_heads: int) -> np.ndarray:
+    """selection.py:33-43."""
+    q = as_f32(queries, "queries")
+    if q.ndim == 1:
+        q = q[None, None, :]
+    elif q.ndim == 2:
+        q = q[None, :, :]
+    if q.ndim != 3:
+        raise ValueError(f"queries must be [D], [G, D] or [heads, G, D], got {q.shape}")
+    if q.shape[0] != n_heads:
+        raise ValueError(f"queries carry {q.shape[0]} head groups, store has {n_heads}")
+    return q
+
+
+def _to_dev_tokens(a: np.ndarray, dtype) -> torch.Tensor:
+    # [H, n, D] -> [1, n, H, D] on the device
+    return torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2))[None]).to(
+        device="cuda", dtype=dtype).contiguous()
+
+
+def _dev_q(q: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(q)[None]).to("cuda").contiguous()
+
+
+class ChunkedKVStore:
+    """kvstore.py:75-306, backed by a device store (batch 1)."""
+
+    def __init__(self, keys, values, chunk_size, landmark_scheme, residual_scheme, budget,
+                 slow_tier_scheme, dtype=torch.float32, svd_concat=False, offload="hbm"):
+        self.keys = keys
+        self.values = values
+        self.chunk_size = chunk_size
+        self.landmark_scheme = landmark_scheme
+        self.residual_scheme = residual_scheme
+        self.budget = budget
+        self.slow_tier_scheme = slow_tier_scheme
+        self.dtype = dtype
+        self.svd_concat = svd_concat
+        self.offload = offload
+        self._build()
+
+    def _build(self):
+        h, n, d = self.keys.shape
+        slow = self.slow_tier_scheme
+        groups = 1
+        if slow.kind == SVD:
+            groups = 1 if self.svd_concat else h
+        self.dev = DeviceStore(batch=1, n_tokens=n, kv_heads=h, head_dim=d,
+                               chunk_size=self.chunk_size, dtype=self.dtype,
+                               landmark=self.landmark_scheme, residual=self.residual_scheme,
+                               slow=slow, svd_groups=groups,
+                               outlier_tokens=self.budget.outlier_tokens,
+                               local_window=self.budget.local_window, offload=self.offload)
+        self._k_dev = _to_dev_tokens(self.keys, self.dtype)
+        v_dev = _to_dev_tokens(self.values, self.dtype)
+        self.dev.build(self._k_dev, v_dev)
+        torch.cuda.synchronize()
+
+    # -- geometry (kvstore.py:98-123)
+    @property
+    def n_heads(self) -> int:
+        return self.keys.shape[0]
+
+    @property
+    def n_tokens(self) -> int:
+        return self.keys.shape[1]
+
+    @property
+    def head_dim(self) -> int:
+        return self.keys.shape[2]
+
+    @property
+    def n_chunks(self) -> int:
+        return -(-self.n_tokens // self.chunk_size)
+
+    def chunk_of(self, token_id: int) -> int:
+        return token_id // self.chunk_size
+
+    def chunk_token_ids(self, chunk_id: int) -> np.ndarray:
+        if not 0 <= chunk_id < self.n_chunks:
+            raise ValueError(f"chunk id {chunk_id} out of range [0, {self.n_chunks})")
+        start = chunk_id * self.chunk_size
+        return np.arange(start, min(start + self.chunk_size, self.n_tokens))
+
+    # -- derived state
+    @property
+    def outlier_chunks(self) -> tuple:
+        return self.dev.residency.outlier_chunks[0]
+
+    def landmarks_dequantized(self) -> np.ndarray:
+        """[heads, n_chunks, D] float32 (kvstore.py:204-206)."""
+        lm = self.dev.landmarks_dequantized()[0].permute(1, 0, 2).contiguous()
+        return lm.cpu().numpy()
+
+    def residuals_dequantized(self) -> np.ndarray:
+        if self.residual_scheme is None:
+            raise ValueError("store was built without residuals")
+        return self.dev.residuals_dequantized()[0].permute(1, 0, 2).contiguous().cpu().numpy()
+
+    def landmark_of(self, chunk_id: int, head: int = 0) -> np.ndarray:
+        if not 0 <= chunk_id < self.n_chunks:
+            raise ValueError(f"chunk id {chunk_id} out of range [0, {self.n_chunks})")
+        return self.landmarks_dequantized()[head, chunk_id]
+
+    def approx_key(self, token_id: int, head: int = 0) -> np.ndarray:
+        if self.residual_scheme is None:
+            raise ValueError("store was built without residuals")
+        if not 0 <= token_id < self.n_tokens:
+            raise ValueError(f"token id {token_id} out of range [0, {self.n_tokens})")
+        return (self.landmarks_dequantized()[head, self.chunk_of(token_id)]
+                + self.residuals_dequantized()[head, token_id])
+
+    @property
+    def local_token_ids(self) -> np.ndarray:
+        w = min(self.budget.local_window, self.n_tokens)
+        return np.arange(self.n_tokens - w, self.n_tokens)
+
+    @property
+    def resident_token_ids(self) -> np.ndarray:
+        return self.dev.residency.resident[0]
+
+    def fast_tier_resident_bits(self) -> Fraction:
+        """kvstore.py:242-252 (modelled footprint, exact rational)."""
+        d = self.head_dim
+        lm = self.landmark_scheme.code_bits * self.n_chunks * d * self.n_heads
+        res = Fraction(0)
+        if self.residual_scheme is not None:
+            res = self.residual_scheme.code_bits * self.n_tokens * d * self.n_heads
+        kv = Fraction(2 * 16 * d * len(self.resident_token_ids) * self.n_heads)
+        return lm + res + kv
+
+    def bits_per_key(self) -> Fraction:
+        return _bits_per_key(self.landmark_scheme, self.chunk_size, self.residual_scheme)
+
+    def load_chunks(self, chunk_ids):
+        """Traffic accounting of kvstore.py:257-279 (token counts only; the
+        K/V themselves are consumed on the device by sparse_attention)."""
+        ids = sorted(set(int(c) for c in chunk_ids))
+        for c in ids:
+            if not 0 <= c < self.n_chunks:
+                raise ValueError(f"chunk id {c} out of range [0, {self.n_chunks})")
+        toks = (np.concatenate([self.chunk_token_ids(c) for c in ids]) if ids
+                else np.empty(0, dtype=np.int64))
+        loaded = int(np.count_nonzero(~np.isin(toks, self.resident_token_ids)))
+        return TierTraffic(loaded, self.fast_tier_resident_bits())
+
+    def append(self, new_keys, new_values) -> None:
+        """kvstore.py:295-305: one token per head joins the tail chunk; the
+        derived state is rebuilt on the device."""
+        nk = as_f32(new_keys, "new_keys").reshape(self.n_heads, 1, self.head_dim)
+        nv = as_f32(new_values, "new_values").reshape(self.n_heads, 1, self.head_dim)
+        self.keys = np.concatenate([self.keys, nk], axis=1)
+        self.values = np.concatenate([self.values, nv], axis=1)
+        self.dev.close()
+        self._build()
+
+
+def build_store(keys, values, chunk_size: int, landmark_scheme: SchemeDescriptor,
+                residual_scheme: SchemeDescriptor | None = None,
+                budget: BudgetConfig = BudgetConfig(),
+                slow_tier_scheme: SchemeDescriptor | None = None, *,
+                dtype=torch.float32, svd_concat: bool = False,
+                offload: str = "hbm") -> ChunkedKVStore:
+    """kvstore.py:354-385."""
+    keys = _heads3(keys, "keys")
+    values = _heads3(values, "values")
+    if keys.shape != values.shape:
+        raise ValueError(f"keys {keys.shape} and values {values.shape} differ")
+    if keys.shape[1] < 1:
+        raise ValueError("store requires at least one token")
+    if chunk_size < 1:
+        raise ValueError("chunk_size must be >= 1")
+    return ChunkedKVStore(keys, values, chunk_size, landmark_scheme, residual_scheme, budget,
+                          slow_tier_scheme if slow_tier_scheme is not None else scheme_none(),
+                          dtype=dtype, svd_concat=svd_concat, offload=offload)
+
+
+def _n_sel(store: ChunkedKVStore, frac: float) -> int:
+    return min(store.n_chunks, math.ceil(frac * store.n_tokens / store.chunk_size))
+
+
+def _tokens(tok, ntok) -> np.ndarray:
+    n = int(ntok[0].item())
+    return tok[0, :n].cpu().numpy().astype(np.int64)
+
+
+def select_by_landmarks(store: ChunkedKVStore, queries, budget: BudgetConfig,
+                        aggregation: str = "sum") -> SelectionResult:
+    """selection.py:72-87 on the GPU (K1 scoring + K2 top-k + K2b union)."""
+    q = normalize_queries(queries, store.n_heads)
+    if aggregation not in ("sum", "max"):
+        raise ValueError(f"unknown aggregation {aggregation!r}")
+    k = _n_sel(store, budget.sparse_fraction)
+    cid, sc, tok, ntok = store.dev.select(_dev_q(q), k, aggregation=aggregation, rank_order=True)
+    tokens = _tokens(tok, ntok)
+    return SelectionResult(chunk_ids=tuple(int(c) for c in cid[0].cpu().tolist()),
+                           token_ids=tokens, scores=sc[0].cpu().numpy(),
+                           loaded_fraction=len(tokens) / store.n_tokens)
+
+
+def approx_topk_residual(store: ChunkedKVStore, queries, k: int,
+                         candidate_multiplier: int = 4) -> SelectionResult:
+    """selection.py:132-171 on the GPU."""
+    if candidate_multiplier < 1:
+        raise ValueError("candidate_multiplier must be >= 1")
+    if store.residual_scheme is None:
+        raise ValueError("store was built without residuals")
+    q = normalize_queries(queries, store.n_heads)
+    if not 1 <= k <= store.n_tokens:
+        raise ValueError(f"k {k} out of range [1, {store.n_tokens}]")
+    cand, sc, tok, ntok = store.dev.select_residual(_dev_q(q), k, candidate_multiplier)
+    tokens = _tokens(tok, ntok)
+    return SelectionResult(chunk_ids=tuple(int(c) for c in cand[0].cpu().tolist()),
+                           token_ids=tokens, scores=sc[0].cpu().numpy(),
+                           loaded_fraction=len(tokens) / store.n_tokens)
+
+
+def residual_scores(store: ChunkedKVStore, queries) -> np.ndarray:
+    """selection.py:114-129: every chunk is a candidate, so the refined
+    scores cover all tokens."""
+    if store.residual_scheme is None:
+        raise ValueError("store was built without residuals")
+    q = normalize_queries(queries, store.n_heads)
+    mult = store.n_chunks
+    _, sc, _, _ = store.dev.select_residual(_dev_q(q), 1, max(1, math.ceil(mult)))
+    return sc[0].cpu().numpy()
+
+
+def sparse_attention(queries, store: ChunkedKVStore, sel: SelectionResult,
+                     full_baseline: np.ndarray | None = None) -> AttentionOutput:
+    """attention.py:62-90 on the GPU (fused tier gather + split-K decode)."""
+    q = normalize_queries(queries, store.n_heads)
+    ids = np.asarray(sel.token_ids, dtype=np.int64)
+    if len(ids) == 0:
+        raise ValueError("selection is empty")
+    if ids.min() < 0 or ids.max() >= store.n_tokens:
+        raise ValueError("token id out of range")
+    tok = torch.from_numpy(ids.astype(np.int32)[None]).cuda()
+    ntok = torch.tensor([len(ids)], dtype=torch.int32, device="cuda")
+    out, _ = store.dev.attend(_dev_q(q), tok, ntok)
+    o = out[0].cpu().numpy()
+    rel = None
+    if full_baseline is not None:
+        denom = float(np.linalg.norm(full_baseline))
+        rel = float(np.linalg.norm(o - full_baseline) / max(denom, 1e-30))
+    return AttentionOutput(output=o, tokens_used=len(ids), rel_error_vs_full=rel)
+
+
+def oracle_select(keys, queries, k: int) -> SelectionResult:
+    """selection.py:90-111: exact top-k tokens -- a chunk-1 lossless store
+    with no residents through the same GPU scoring / top-k kernels."""
+    keys = _heads3(keys, "keys")
+    q = normalize_queries(queries, keys.shape[0])
+    n = keys.shape[1]
+    if not 1 <= k <= n:
+        raise ValueError(f"k {k} out of range [1, {n}]")
+    dev = DeviceStore(batch=1, n_tokens=n, kv_heads=keys.shape[0], head_dim=keys.shape[2],
+                      chunk_size=1, landmark=scheme_none(), outlier_tokens=0, local_window=0)
+    kd = _to_dev_tokens(keys, torch.float32)
+    dev.build(kd, kd)
+    cid, sc, tok, ntok = dev.select(_dev_q(q), k, rank_order=True)
+    top = cid[0].cpu().numpy().astype(np.int64)
+    dev.close()
+    return SelectionResult(chunk_ids=tuple(int(t) for t in top), token_ids=np.sort(top),
+                           scores=sc[0].cpu().numpy(), loaded_fraction=k / n)
+
+
+def full_attention_heads(queries, keys, values) -> np.ndarray:
+    """attention.py:48-59: attention over every token, on the GPU."""
+    keys = _heads3(keys, "keys")
+    values = _heads3(values, "values")
+    q = normalize_queries(queries, keys.shape[0])
+    if keys.shape[1] == 0:
+        raise ValueError("attention over zero keys is undefined")
+    h, n, d = keys.shape
+    dev = DeviceStore(batch=1, n_tokens=n, kv_heads=h, head_dim=d, chunk_size=1,
+                      landmark=scheme_none(), outlier_tokens=0, local_window=0)
+    dev.build(_to_dev_tokens(keys, torch.float32), _to_dev_tokens(values, torch.float32))
+    tok = torch.arange(n, dtype=torch.int32, device="cuda")[None].contiguous()
+    ntok = torch.tensor([n], dtype=torch.int32, device="cuda")
+    out, _ = dev.attend(_dev_q(q), tok, ntok)
+    o = out[0].cpu().numpy()
+    dev.close()
+    return o
+
+
+def recall(selected: SelectionResult, oracle: SelectionResult) -> float:
+    """selection.py:174-180."""
+    oracle_ids = set(oracle.token_ids.tolist())
+    if not oracle_ids:
+        raise ValueError("oracle selection is empty")
+    return len(oracle_ids & set(selected.token_ids.tolist())) / len(oracle_ids)

@@ -1,0 +1,686 @@
+// libkvb C-ABI: store lifecycle, validation (reference ValueError conditions),
+// workspace carving and kernel orchestration. See include/kvb.h.
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <unordered_map>
+#include <string>
+#include <vector>
+
+#include "kvb_common.cuh"
+#include "kvb_internal.h"
+
+namespace kvb {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+void count_launch(int n) { g_launches += n; }
+
+cudaError_t ensure_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(func);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[func] = bytes;
+  return e;
+}
+
+kvb_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return KVB_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? KVB_ENOMEM : KVB_ECUDA;
+}
+
+}  // namespace kvb
+
+using namespace kvb;
+
+#define KVB_FAIL(code, msg)  \
+  do {                       \
+    kvb::set_error(msg);     \
+    return code;             \
+  } while (0)
+#define KVB_CUDA(expr, what)                                  \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return kvb::cuda_status(_e, what); \
+  } while (0)
+
+namespace {
+
+bool pow2(int x) { return x >= 1 && (x & (x - 1)) == 0; }
+
+template <typename T>
+kvb_status dalloc(T** p, size_t count, const char* what) {
+  *p = nullptr;
+  if (count == 0) return KVB_OK;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return cuda_status(e, what);
+  }
+  return KVB_OK;
+}
+
+kvb_status setup_higgs(kvb_store* s, const kvb_higgs_desc& hd, int rows, kvb_higgs_dev* out,
+                       const char* which) {
+  const int D = s->d.head_dim;
+  if (hd.d != 1 && hd.d != 2 && hd.d != 4)
+    KVB_FAIL(KVB_EINVAL, std::string(which) + ": sub-vector dimension must be 1, 2 or 4");
+  if (!pow2(hd.n) || hd.n < 2)
+    KVB_FAIL(KVB_EINVAL, std::string(which) + ": HIGGS codeword count must be a power of two");
+  if (!pow2(hd.group))
+    KVB_FAIL(KVB_EINVAL, std::string(which) + ": HIGGS group size must be a power of two");
+  const int bits = 31 - __builtin_clz((unsigned)hd.n);
+  if (bits > 8 || 8 % bits)
+    KVB_FAIL(KVB_EUNSUPPORTED, std::string(which) + ": code width must divide 8 (n <= 256)");
+  if (hd.group % D || D % 32 || hd.group < 32 || hd.group > 4096)
+    KVB_FAIL(KVB_EUNSUPPORTED,
+             std::string(which) + ": GPU HIGGS path needs head_dim % 32 == 0 and group % head_dim == 0");
+  if (((hd.group / hd.d) * bits) % 8)
+    KVB_FAIL(KVB_EUNSUPPORTED, std::string(which) + ": group codes must fill whole bytes");
+  if (!hd.codebook || !hd.signs) KVB_FAIL(KVB_EINVAL, std::string(which) + ": codebook/signs missing");
+  out->d = hd.d;
+  out->n = hd.n;
+  out->group = hd.group;
+  out->seed = hd.seed;
+  out->bits = bits;
+  out->rows = hd.group / D;
+  out->groups = (int)(((int64_t)rows * D + hd.group - 1) / hd.group);
+  out->group_bytes = (hd.group / hd.d) * bits / 8;
+  const size_t G = (size_t)s->d.batch * s->d.kv_heads * out->groups;
+  kvb_status st;
+  if ((st = dalloc(&out->codebook, (size_t)hd.n * hd.d, "codebook")) != KVB_OK) return st;
+  if ((st = dalloc(&out->signs, (size_t)hd.group, "signs")) != KVB_OK) return st;
+  if ((st = dalloc(&out->codes, G * out->group_bytes, "higgs codes")) != KVB_OK) return st;
+  if ((st = dalloc(&out->scales, G, "higgs scales")) != KVB_OK) return st;
+  if ((st = dalloc(&out->factor, G, "higgs factors")) != KVB_OK) return st;
+  KVB_CUDA(cudaMemcpy(out->codebook, hd.codebook, sizeof(float) * hd.n * hd.d, cudaMemcpyHostToDevice),
+           "codebook upload");
+  KVB_CUDA(cudaMemcpy(out->signs, hd.signs, sizeof(float) * hd.group, cudaMemcpyHostToDevice),
+           "signs upload");
+  return KVB_OK;
+}
+
+void free_higgs(kvb_higgs_dev& h) {
+  cudaFree(h.codebook);
+  cudaFree(h.signs);
+  cudaFree(h.codes);
+  cudaFree(h.scales);
+  cudaFree(h.factor);
+  h = kvb_higgs_dev{};
+}
+
+void free_store(kvb_store* s) {
+  cudaFree(s->lm_dense);
+  free_higgs(s->lm_h);
+  free_higgs(s->res_h);
+  cudaFree(s->res_ids);
+  cudaFree(s->res_count);
+  cudaFree(s->res_bitmap);
+  cudaFree(s->res_prefix);
+  cudaFree(s->res_k);
+  cudaFree(s->res_v);
+  cudaFree(s->svd_left);
+  cudaFree(s->svd_right);
+  if (s->off_host) {
+    cudaFreeHost(s->off_k);
+    cudaFreeHost(s->off_v);
+  } else {
+    cudaFree(s->off_k);
+    cudaFree(s->off_v);
+  }
+  delete s;
+}
+
+cudaStream_t as_stream(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+// Carves a caller workspace into aligned sub-buffers.
+struct Carve {
+  char* base;
+  size_t off = 0, cap;
+  Carve(void* b, size_t c) : base((char*)b), cap(c) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return off <= cap; }
+};
+
+size_t aligned(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+
+kvb_status check_queries(const kvb_store* s, int G) {
+  if (G < 1 || G > kMaxG)
+    KVB_FAIL(KVB_EUNSUPPORTED, "queries_per_head must be in [1, 8]");
+  (void)s;
+  return KVB_OK;
+}
+
+kvb_status check_ready_landmarks(const kvb_store* s) {
+  (void)s;
+  return KVB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kvb_last_error(void) { return g_err.c_str(); }
+int32_t kvb_abi_version(void) { return KVB_ABI_VERSION; }
+int64_t kvb_launch_count(void) { return g_launches.load(); }
+
+kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
+  if (!desc || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  *out = nullptr;
+  const kvb_store_desc& d = *desc;
+  // kvstore.py:369-376
+  if (d.n_tokens < 1) KVB_FAIL(KVB_EINVAL, "store requires at least one token");
+  if (d.chunk_size < 1) KVB_FAIL(KVB_EINVAL, "chunk_size must be >= 1");
+  if (d.batch < 1 || d.kv_heads < 1 || d.head_dim < 1)
+    KVB_FAIL(KVB_EINVAL, "batch, kv_heads and head_dim must be >= 1");
+  if (d.kv_dtype != KVB_F32 && d.kv_dtype != KVB_BF16) KVB_FAIL(KVB_EINVAL, "unknown kv_dtype");
+  if (d.max_resident < 1) KVB_FAIL(KVB_EINVAL, "max_resident must be >= 1");
+  if (d.slow_kind == KVB_SLOW_SVD) {
+    if (d.svd_rank < 1) KVB_FAIL(KVB_EINVAL, "svd rank must be >= 1");
+    if (d.svd_groups < 1 || d.kv_heads % d.svd_groups)
+      KVB_FAIL(KVB_EINVAL, "svd_groups must divide kv_heads");
+  } else if (d.slow_kind != KVB_SLOW_NONE) {
+    KVB_FAIL(KVB_EUNSUPPORTED, "slow tier must be none or svd");
+  }
+  if ((int64_t)d.n_tokens > (1ll << 26)) KVB_FAIL(KVB_EUNSUPPORTED, "n_tokens too large");
+  auto* s = new kvb_store();
+  s->d = d;
+  s->C = (d.n_tokens + d.chunk_size - 1) / d.chunk_size;
+  s->E = d.kv_heads * d.head_dim;
+  s->W = (d.n_tokens + 31) / 32;
+  s->esz = d.kv_dtype == KVB_BF16 ? 2 : 4;
+  const size_t B = d.batch, E = s->E, n = d.n_tokens;
+  kvb_status st = KVB_OK;
+  auto bail = [&](kvb_status code) {
+    free_store(s);
+    return code;
+  };
+  if (d.landmark_kind == KVB_LM_DENSE) {
+    if ((st = dalloc((char**)&s->lm_dense, B * s->C * E * s->esz, "landmarks")) != KVB_OK) return bail(st);
+  } else if (d.landmark_kind == KVB_LM_HIGGS) {
+    if ((st = setup_higgs(s, d.landmark_higgs, s->C, &s->lm_h, "landmark")) != KVB_OK) return bail(st);
+  } else {
+    return bail((set_error("unknown landmark kind"), KVB_EINVAL));
+  }
+  if (d.has_residual) {
+    if ((st = setup_higgs(s, d.residual_higgs, d.n_tokens, &s->res_h, "residual")) != KVB_OK)
+      return bail(st);
+  }
+  const size_t R = d.max_resident;
+  if ((st = dalloc(&s->res_ids, B * R, "resident ids")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->res_count, B, "resident counts")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->res_bitmap, B * s->W, "resident bitmap")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->res_prefix, B * s->W, "resident prefix")) != KVB_OK) return bail(st);
+  if ((st = dalloc((char**)&s->res_k, B * R * E * s->esz, "resident K")) != KVB_OK) return bail(st);
+  if ((st = dalloc((char**)&s->res_v, B * R * E * s->esz, "resident V")) != KVB_OK) return bail(st);
+  cudaMemset(s->res_count, 0, B * sizeof(int32_t));
+  cudaMemset(s->res_bitmap, 0, B * s->W * sizeof(uint32_t));
+  cudaMemset(s->res_prefix, 0, B * s->W * sizeof(int32_t));
+  const size_t off_bytes = B * n * E * s->esz;
+  const bool need_k = d.slow_kind == KVB_SLOW_NONE;
+  if (d.offload_tier == KVB_TIER_HOST_MAPPED) {
+    s->off_host = true;
+    cudaError_t e = cudaHostAlloc(&s->off_v, off_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return bail(cuda_status(e, "pinned V"));
+    cudaHostGetDevicePointer(&s->off_v_dev, s->off_v, 0);
+    if (need_k) {
+      e = cudaHostAlloc(&s->off_k, off_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e != cudaSuccess) return bail(cuda_status(e, "pinned K"));
+      cudaHostGetDevicePointer(&s->off_k_dev, s->off_k, 0);
+    }
+  } else if (d.offload_tier == KVB_TIER_HBM) {
+    if ((st = dalloc((char**)&s->off_v, off_bytes, "offload V")) != KVB_OK) return bail(st);
+    s->off_v_dev = s->off_v;
+    if (need_k) {
+      if ((st = dalloc((char**)&s->off_k, off_bytes, "offload K")) != KVB_OK) return bail(st);
+      s->off_k_dev = s->off_k;
+    }
+  } else {
+    return bail((set_error("unknown offload tier"), KVB_EINVAL));
+  }
+  if (d.slow_kind == KVB_SLOW_SVD) {
+    const size_t r = d.svd_rank, g = d.svd_groups, Dg = E / g;
+    if ((st = dalloc(&s->svd_left, B * n * g * r, "svd left")) != KVB_OK) return bail(st);
+    if ((st = dalloc(&s->svd_right, B * g * r * Dg, "svd right")) != KVB_OK) return bail(st);
+  }
+  *out = s;
+  return KVB_OK;
+}
+
+kvb_status kvb_store_destroy(kvb_store* store) {
+  if (store) free_store(store);
+  return KVB_OK;
+}
+
+kvb_status kvb_store_get_info(const kvb_store* s, kvb_store_info* info) {
+  if (!s || !info) KVB_FAIL(KVB_EINVAL, "null argument");
+  const size_t B = s->d.batch, E = s->E, n = s->d.n_tokens;
+  info->n_chunks = s->C;
+  info->n_groups_landmark = s->lm_h.groups;
+  info->n_groups_residual = s->res_h.groups;
+  int64_t fast = 0;
+  if (s->lm_dense) fast += (int64_t)B * s->C * E * s->esz;
+  if (s->lm_h.codes) fast += (int64_t)B * s->d.kv_heads * s->lm_h.groups * (s->lm_h.group_bytes + 2);
+  if (s->res_h.codes) fast += (int64_t)B * s->d.kv_heads * s->res_h.groups * (s->res_h.group_bytes + 2);
+  fast += (int64_t)B * s->d.max_resident * E * s->esz * 2;
+  if (s->svd_left)
+    fast += (int64_t)B * (n * s->d.svd_groups * s->d.svd_rank + (size_t)s->d.svd_rank * E) * 2;
+  info->bytes_fast_tier = fast;
+  info->bytes_offload_tier = (int64_t)B * n * E * s->esz * (s->off_k ? 2 : 1);
+  return KVB_OK;
+}
+
+kvb_status kvb_store_landmark_ptr(const kvb_store* s, void** ptr) {
+  if (!s || !ptr) KVB_FAIL(KVB_EINVAL, "null argument");
+  *ptr = s->lm_dense ? s->lm_dense : (void*)s->lm_h.codes;
+  return KVB_OK;
+}
+
+// ---- build -----------------------------------------------------------------
+
+kvb_status kvb_build_landmarks(kvb_store* s, const void* keys, void* stream) {
+  if (!s || !keys) KVB_FAIL(KVB_EINVAL, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (s->d.landmark_kind == KVB_LM_DENSE) {
+    KVB_CUDA(launch_chunk_means(s, keys, s->lm_dense, nullptr, st), "chunk means");
+    return KVB_OK;
+  }
+  float* tmp = nullptr;
+  const size_t cnt = (size_t)s->d.batch * s->C * s->E;
+  KVB_CUDA(cudaMallocAsync((void**)&tmp, cnt * sizeof(float), st), "landmark scratch");
+  cudaError_t e = launch_chunk_means(s, keys, nullptr, tmp, st);
+  if (e == cudaSuccess) e = launch_higgs_quantize(s, s->lm_h, tmp, s->C, st);
+  cudaFreeAsync(tmp, st);
+  KVB_CUDA(e, "landmark quantize");
+  return KVB_OK;
+}
+
+kvb_status kvb_landmarks_dequantized(kvb_store* s, float* out, void* stream) {
+  if (!s || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (s->d.landmark_kind == KVB_LM_DENSE)
+    KVB_CUDA(launch_dense_to_f32(s, out, st), "landmark widen");
+  else
+    KVB_CUDA(launch_higgs_dequant(s, s->lm_h, s->C, out, st), "landmark dequant");
+  return KVB_OK;
+}
+
+kvb_status kvb_residuals_dequantized(kvb_store* s, float* out, void* stream) {
+  if (!s || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (!s->d.has_residual) KVB_FAIL(KVB_EINVAL, "store was built without residuals");
+  KVB_CUDA(launch_higgs_dequant(s, s->res_h, s->d.n_tokens, out, as_stream(stream)),
+           "residual dequant");
+  return KVB_OK;
+}
+
+kvb_status kvb_build_residuals(kvb_store* s, const void* keys, void* stream) {
+  if (!s || !keys) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (!s->d.has_residual) KVB_FAIL(KVB_EINVAL, "store was built without residuals");
+  cudaStream_t st = as_stream(stream);
+  float *lm = nullptr, *src = nullptr;
+  const size_t lcnt = (size_t)s->d.batch * s->C * s->E;
+  const size_t rcnt = (size_t)s->d.batch * s->d.n_tokens * s->E;
+  KVB_CUDA(cudaMallocAsync((void**)&lm, lcnt * sizeof(float), st), "residual scratch");
+  cudaError_t e = cudaMallocAsync((void**)&src, rcnt * sizeof(float), st);
+  if (e == cudaSuccess) {
+    kvb_status ks = kvb_landmarks_dequantized(s, lm, stream);
+    if (ks != KVB_OK) e = cudaErrorUnknown;
+    if (e == cudaSuccess) e = launch_residual_source(s, keys, lm, src, st);
+    if (e == cudaSuccess) e = launch_higgs_quantize(s, s->res_h, src, s->d.n_tokens, st);
+    cudaFreeAsync(src, st);
+  }
+  cudaFreeAsync(lm, st);
+  KVB_CUDA(e, "residual quantize");
+  return KVB_OK;
+}
+
+kvb_status kvb_build_chunk_cosine(kvb_store* s, const void* keys, double* out, void* stream) {
+  if (!s || !keys || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (s->d.chunk_size > 64) KVB_FAIL(KVB_EUNSUPPORTED, "outlier scoring needs chunk_size <= 64");
+  cudaStream_t st = as_stream(stream);
+  float* lm = nullptr;
+  const size_t lcnt = (size_t)s->d.batch * s->C * s->E;
+  KVB_CUDA(cudaMallocAsync((void**)&lm, lcnt * sizeof(float), st), "cosine scratch");
+  kvb_status ks = kvb_landmarks_dequantized(s, lm, stream);
+  cudaError_t e = ks == KVB_OK ? launch_chunk_cosine(s, keys, lm, out, st) : cudaErrorUnknown;
+  cudaFreeAsync(lm, st);
+  if (ks != KVB_OK) return ks;
+  KVB_CUDA(e, "chunk cosine");
+  return KVB_OK;
+}
+
+kvb_status kvb_choose_outliers(const double* per_chunk, int32_t C, int32_t n, int32_t cs,
+                               int32_t budget, int32_t* out_chunks, int32_t* out_count) {
+  if (!out_count) KVB_FAIL(KVB_EINVAL, "null argument");
+  *out_count = 0;
+  if (budget <= 0) return KVB_OK;  // kvstore.py:164-165
+  if (!per_chunk || !out_chunks || C < 1 || cs < 1) KVB_FAIL(KVB_EINVAL, "bad outlier arguments");
+  std::vector<int32_t> order(C);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return per_chunk[a] < per_chunk[b]; });
+  std::vector<int32_t> seq;
+  seq.reserve(C);
+  seq.push_back(0);
+  for (int32_t c : order)
+    if (c != 0) seq.push_back(c);
+  std::vector<int32_t> chosen;
+  int64_t used = 0;
+  for (int32_t c : seq) {
+    const int64_t size = std::min<int64_t>(cs, (int64_t)n - (int64_t)c * cs);
+    if (used + size > budget) continue;  // skip, not stop (kvstore.py:186-187)
+    chosen.push_back(c);
+    used += size;
+  }
+  std::sort(chosen.begin(), chosen.end());
+  for (size_t i = 0; i < chosen.size(); ++i) out_chunks[i] = chosen[i];
+  *out_count = (int32_t)chosen.size();
+  return KVB_OK;
+}
+
+kvb_status kvb_store_set_residency(kvb_store* s, const int32_t* ids, const int32_t* counts,
+                                   const void* keys, const void* values, void* stream) {
+  if (!s || !ids || !counts || !keys || !values) KVB_FAIL(KVB_EINVAL, "null argument");
+  const int B = s->d.batch, R = s->d.max_resident, n = s->d.n_tokens;
+  for (int b = 0; b < B; ++b) {
+    if (counts[b] < 0 || counts[b] > R) KVB_FAIL(KVB_EINVAL, "resident count exceeds max_resident");
+    for (int i = 0; i < counts[b]; ++i) {
+      const int t = ids[(size_t)b * R + i];
+      if (t < 0 || t >= n) KVB_FAIL(KVB_EINVAL, "resident token id out of range");
+      if (i && t <= ids[(size_t)b * R + i - 1]) KVB_FAIL(KVB_EINVAL, "resident ids must be sorted unique");
+    }
+  }
+  cudaStream_t st = as_stream(stream);
+  KVB_CUDA(cudaMemcpyAsync(s->res_ids, ids, sizeof(int32_t) * B * R, cudaMemcpyHostToDevice, st),
+           "resident ids");
+  KVB_CUDA(cudaMemcpyAsync(s->res_count, counts, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st),
+           "resident counts");
+  KVB_CUDA(launch_residency(s, keys, values, st), "residency");
+  // the host arrays may be reused by the caller right after return
+  KVB_CUDA(cudaStreamSynchronize(st), "residency sync");
+  return KVB_OK;
+}
+
+kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* values, void* stream) {
+  if (!s || !values) KVB_FAIL(KVB_EINVAL, "null argument");
+  const size_t bytes = (size_t)s->d.batch * s->d.n_tokens * s->E * s->esz;
+  cudaStream_t st = as_stream(stream);
+  KVB_CUDA(cudaMemcpyAsync(s->off_v_dev, values, bytes, cudaMemcpyDefault, st), "offload V");
+  if (s->off_k) {
+    if (!keys) KVB_FAIL(KVB_EINVAL, "slow tier 'none' needs keys");
+    KVB_CUDA(cudaMemcpyAsync(s->off_k_dev, keys, bytes, cudaMemcpyDefault, st), "offload K");
+  }
+  return KVB_OK;
+}
+
+kvb_status kvb_store_set_svd(kvb_store* s, const void* left16, const void* right16, void* stream) {
+  if (!s || !left16 || !right16) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (s->d.slow_kind != KVB_SLOW_SVD) KVB_FAIL(KVB_EINVAL, "store slow tier is not svd");
+  const size_t B = s->d.batch, n = s->d.n_tokens, r = s->d.svd_rank, g = s->d.svd_groups;
+  const size_t Dg = s->E / g;
+  cudaStream_t st = as_stream(stream);
+  KVB_CUDA(cudaMemcpyAsync(s->svd_left, left16, B * n * g * r * 2, cudaMemcpyDefault, st), "svd left");
+  KVB_CUDA(cudaMemcpyAsync(s->svd_right, right16, B * g * r * Dg * 2, cudaMemcpyDefault, st), "svd right");
+  return KVB_OK;
+}
+
+kvb_status kvb_store_set_landmarks_dense(kvb_store* s, const void* lm, void* stream) {
+  if (!s || !lm) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (!s->lm_dense) KVB_FAIL(KVB_EINVAL, "store landmarks are not dense");
+  KVB_CUDA(cudaMemcpyAsync(s->lm_dense, lm, (size_t)s->d.batch * s->C * s->E * s->esz,
+                           cudaMemcpyDefault, as_stream(stream)),
+           "landmark import");
+  return KVB_OK;
+}
+
+static kvb_status import_higgs(kvb_store* s, kvb_higgs_dev& h, const uint8_t* codes,
+                               const float* scales, cudaStream_t st) {
+  const size_t G = (size_t)s->d.batch * s->d.kv_heads * h.groups;
+  KVB_CUDA(cudaMemcpyAsync(h.codes, codes, G * h.group_bytes, cudaMemcpyDefault, st), "codes import");
+  KVB_CUDA(cudaMemcpyAsync(h.scales, scales, G * sizeof(float), cudaMemcpyDefault, st), "scales import");
+  KVB_CUDA(launch_higgs_factor(s, h, st), "group factors");
+  return KVB_OK;
+}
+
+kvb_status kvb_store_set_landmarks_higgs(kvb_store* s, const uint8_t* codes, const float* scales,
+                                         void* stream) {
+  if (!s || !codes || !scales) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (s->d.landmark_kind != KVB_LM_HIGGS) KVB_FAIL(KVB_EINVAL, "store landmarks are not HIGGS");
+  return import_higgs(s, s->lm_h, codes, scales, as_stream(stream));
+}
+
+kvb_status kvb_store_set_residuals_higgs(kvb_store* s, const uint8_t* codes, const float* scales,
+                                         void* stream) {
+  if (!s || !codes || !scales) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (!s->d.has_residual) KVB_FAIL(KVB_EINVAL, "store was built without residuals");
+  return import_higgs(s, s->res_h, codes, scales, as_stream(stream));
+}
+
+// ---- decode ----------------------------------------------------------------
+
+static kvb_status score_landmarks(kvb_store* s, const float* q, int G, int agg, float* scores,
+                                  cudaStream_t st) {
+  if (s->d.landmark_kind == KVB_LM_DENSE)
+    KVB_CUDA(launch_score_dense(s, q, G, agg, scores, st), "landmark scoring");
+  else
+    KVB_CUDA(launch_score_higgs(s, q, G, agg, scores, st), "HIGGS landmark scoring");
+  return KVB_OK;
+}
+
+int64_t kvb_select_workspace_bytes(const kvb_store* s, const kvb_select_args* a) {
+  if (!s || !a) return -1;
+  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned(4) + 256);
+}
+
+static kvb_status check_select(const kvb_store* s, const kvb_select_args* a) {
+  if (!s || !a) KVB_FAIL(KVB_EINVAL, "null argument");
+  kvb_status st = check_queries(s, a->queries_per_head);
+  if (st != KVB_OK) return st;
+  if (a->n_select < 1 || a->n_select > s->C) KVB_FAIL(KVB_EINVAL, "n_select out of range [1, C]");
+  if (a->aggregation != KVB_AGG_SUM && a->aggregation != KVB_AGG_MAX)
+    KVB_FAIL(KVB_EINVAL, "unknown aggregation");
+  const int64_t need = (int64_t)a->n_select * s->d.chunk_size + s->d.max_resident;
+  if (a->token_capacity < std::min<int64_t>(need, s->d.n_tokens))
+    KVB_FAIL(KVB_EINVAL, "token_capacity too small for K*cs + residents");
+  size_t smem = (a->rank_order ? (size_t)8 : (size_t)4) * a->n_select * 2 + (size_t)s->W * 4;
+  if (smem > 220 * 1024) KVB_FAIL(KVB_EUNSUPPORTED, "selection exceeds shared-memory capacity");
+  return KVB_OK;
+}
+
+kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, int32_t* chunk_ids,
+                      float* scores, int32_t* token_ids, int32_t* n_tokens, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  kvb_status ks = check_select(s, a);
+  if (ks != KVB_OK) return ks;
+  if (!q || !chunk_ids || !token_ids || !n_tokens) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (ws_bytes < kvb_select_workspace_bytes(s, a) || !ws) KVB_FAIL(KVB_EINVAL, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  Carve cv(ws, ws_bytes);
+  float* sc = scores ? scores : cv.take<float>((size_t)s->d.batch * s->C);
+  int32_t* err = cv.take<int32_t>(1);
+  if ((ks = score_landmarks(s, q, a->queries_per_head, a->aggregation, sc, st)) != KVB_OK) return ks;
+  SelectLaunch L{};
+  L.scores = sc;
+  L.M_stride = s->C;
+  L.m_count = nullptr;
+  L.K = a->n_select;
+  L.rank_order = a->rank_order;
+  L.mode = 0;
+  L.sel_ids = chunk_ids;
+  L.token_ids = token_ids;
+  L.n_tokens = n_tokens;
+  L.cap = a->token_capacity;
+  L.with_residents = 1;
+  L.err_flag = nullptr;
+  (void)err;
+  KVB_CUDA(launch_select(s, L, st), "top-k selection");
+  return KVB_OK;
+}
+
+int64_t kvb_select_residual_workspace_bytes(const kvb_store* s, const kvb_residual_args* a) {
+  if (!s || !a) return -1;
+  const size_t B = s->d.batch, nc = a->n_candidates, cs = s->d.chunk_size;
+  return (int64_t)(aligned(B * s->C * 4) + aligned(B * nc * 4) + aligned(B * nc * 4) +
+                   aligned(B * nc * cs * 4) * 2 + aligned(B * 4) + aligned(B * a->k_tokens * 4) +
+                   aligned(B * 4) + 2048);
+}
+
+kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_args* a,
+                               int32_t* chunk_ids, float* scores, int32_t* token_ids,
+                               int32_t* n_tokens, void* ws, int64_t ws_bytes, void* stream) {
+  if (!s || !a || !q || !chunk_ids || !token_ids || !n_tokens) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (!s->d.has_residual) KVB_FAIL(KVB_EINVAL, "store was built without residuals");
+  kvb_status ks = check_queries(s, a->queries_per_head);
+  if (ks != KVB_OK) return ks;
+  const int n = s->d.n_tokens, cs = s->d.chunk_size;
+  if (a->k_tokens < 1 || a->k_tokens > n) KVB_FAIL(KVB_EINVAL, "k out of range [1, n]");
+  if (a->n_candidates < 1 || a->n_candidates > s->C) KVB_FAIL(KVB_EINVAL, "n_candidates out of range");
+  if (a->token_capacity < std::min<int64_t>((int64_t)a->k_tokens + s->d.max_resident, n))
+    KVB_FAIL(KVB_EINVAL, "token_capacity too small");
+  if (ws_bytes < kvb_select_residual_workspace_bytes(s, a) || !ws)
+    KVB_FAIL(KVB_EINVAL, "workspace too small");
+  const size_t B = s->d.batch, nc = a->n_candidates;
+  cudaStream_t st = as_stream(stream);
+  Carve cv(ws, ws_bytes);
+  float* chunk_s = cv.take<float>(B * s->C);
+  int32_t* cand_sorted = cv.take<int32_t>(B * nc);
+  int32_t* spare = cv.take<int32_t>(B * nc);
+  (void)spare;
+  int32_t* cand_tok = cv.take<int32_t>(B * nc * cs);
+  float* tok_s = cv.take<float>(B * nc * cs);
+  int32_t* cand_count = cv.take<int32_t>(B);
+  int32_t* sel_pos = cv.take<int32_t>(B * a->k_tokens);
+  // stage 1: chunk scores (selection.py:150) and candidate shortlist (:151-152)
+  if ((ks = score_landmarks(s, q, a->queries_per_head, KVB_AGG_SUM, chunk_s, st)) != KVB_OK) return ks;
+  SelectLaunch L{};
+  L.scores = chunk_s;
+  L.M_stride = s->C;
+  L.K = (int)nc;
+  L.rank_order = 1;
+  L.mode = 0;
+  L.sel_ids = chunk_ids;
+  L.token_ids = nullptr;
+  L.n_tokens = nullptr;
+  KVB_CUDA(launch_select(s, L, st), "candidate chunks");
+  // stage 2: candidate tokens (:153), residual-refined scores (:155-158)
+  KVB_CUDA(launch_candidate_tokens(s, chunk_ids, (int)nc, cand_tok, cand_count, cand_sorted, st),
+           "candidate tokens");
+  KVB_CUDA(launch_residual_scores(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc, tok_s, st),
+           "residual scores");
+  // token top-k inside the candidates (:160-161) and union with residents (:162)
+  SelectLaunch T{};
+  T.scores = tok_s;
+  T.M_stride = (int)(nc * cs);
+  T.m_count = cand_count;
+  T.K = a->k_tokens;
+  T.rank_order = 0;
+  T.mode = 1;
+  T.cand_tok = cand_tok;
+  T.sel_ids = sel_pos;
+  T.token_ids = token_ids;
+  T.n_tokens = n_tokens;
+  T.cap = a->token_capacity;
+  T.with_residents = 1;
+  KVB_CUDA(launch_select(s, T, st), "token top-k");
+  if (scores)
+    KVB_CUDA(launch_residual_full_scores(s, chunk_s, cand_tok, cand_count, (int)(nc * cs), tok_s,
+                                         scores, st),
+             "full scores");
+  return KVB_OK;
+}
+
+int64_t kvb_attend_workspace_bytes(const kvb_store* s, const kvb_attend_args* a) {
+  if (!s || !a) return -1;
+  return (int64_t)attend_ws_bytes(s, a->queries_per_head, a->token_capacity);
+}
+
+kvb_status kvb_attend(kvb_store* s, const float* q, const kvb_attend_args* a,
+                      const int32_t* token_ids, const int32_t* n_tokens, float* out, float* lse,
+                      void* ws, int64_t ws_bytes, void* stream) {
+  if (!s || !a || !q || !token_ids || !n_tokens || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  kvb_status ks = check_queries(s, a->queries_per_head);
+  if (ks != KVB_OK) return ks;
+  if (a->token_capacity < 1) KVB_FAIL(KVB_EINVAL, "token_capacity must be >= 1");
+  if (s->d.slow_kind == KVB_SLOW_SVD && a->k_path == 2)
+    KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
+  if (!ws || ws_bytes < kvb_attend_workspace_bytes(s, a)) KVB_FAIL(KVB_EINVAL, "workspace too small");
+  AttendLaunch L{};
+  L.q = q;
+  L.G = a->queries_per_head;
+  L.token_ids = token_ids;
+  L.n_tokens = n_tokens;
+  L.cap = a->token_capacity;
+  L.out = out;
+  L.lse = lse;
+  L.k_path = a->k_path;
+  L.ws = ws;
+  KVB_CUDA(launch_attend(s, L, as_stream(stream)), "sparse attention");
+  return KVB_OK;
+}
+
+int64_t kvb_decode_workspace_bytes(const kvb_store* s, const kvb_select_args* sel,
+                                   const kvb_attend_args* att) {
+  if (!s || !sel || !att) return -1;
+  return (int64_t)(aligned(kvb_select_workspace_bytes(s, sel)) +
+                   aligned((size_t)s->d.batch * sel->n_select * 4) +
+                   aligned(kvb_attend_workspace_bytes(s, att)) + 512);
+}
+
+kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* sel,
+                           const kvb_attend_args* att, int32_t* chunk_ids, int32_t* token_ids,
+                           int32_t* n_tokens, float* out, float* lse, void* ws, int64_t ws_bytes,
+                           void* stream) {
+  kvb_status ks = check_select(s, sel);
+  if (ks != KVB_OK) return ks;
+  if (!att || !q || !token_ids || !n_tokens || !out) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (att->token_capacity != sel->token_capacity) KVB_FAIL(KVB_EINVAL, "token capacities differ");
+  if (!ws || ws_bytes < kvb_decode_workspace_bytes(s, sel, att)) KVB_FAIL(KVB_EINVAL, "workspace too small");
+  Carve cv(ws, ws_bytes);
+  const int64_t sb = kvb_select_workspace_bytes(s, sel);
+  void* sws = cv.take<char>((size_t)sb);
+  int32_t* cid = chunk_ids ? chunk_ids : cv.take<int32_t>((size_t)s->d.batch * sel->n_select);
+  const int64_t ab = kvb_attend_workspace_bytes(s, att);
+  void* aws = cv.take<char>((size_t)ab);
+  kvb_select_args a2 = *sel;
+  a2.rank_order = 0;
+  if ((ks = kvb_select(s, q, &a2, cid, nullptr, token_ids, n_tokens, sws, sb, stream)) != KVB_OK)
+    return ks;
+  return kvb_attend(s, q, att, token_ids, n_tokens, out, lse, aws, ab, stream);
+}
+
+kvb_status kvb_merge_attention(const float* out_parts, const float* lse_parts, int32_t parts,
+                               int32_t rows, int32_t D, float* out, float* lse, void* stream) {
+  if (!out_parts || !lse_parts || !out || parts < 1 || rows < 1 || D < 1)
+    KVB_FAIL(KVB_EINVAL, "bad merge arguments");
+  KVB_CUDA(launch_merge_attention(out_parts, lse_parts, parts, rows, D, out, lse, as_stream(stream)),
+           "attention merge");
+  return KVB_OK;
+}
+
+kvb_status kvb_merge_topk(const float* sc, const int32_t* ids, int32_t parts, int32_t batch,
+                          int32_t k, int32_t* chunk_ids, void* stream) {
+  if (!sc || !ids || !chunk_ids || parts < 1 || batch < 1 || k < 1)
+    KVB_FAIL(KVB_EINVAL, "bad merge arguments");
+  KVB_CUDA(launch_merge_topk(sc, ids, parts, batch, k, chunk_ids, as_stream(stream)), "top-k merge");
+  return KVB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// Shared device helpers for libkvb (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/kvb.h"
+
+namespace kvb {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kMaxG = 8;  // queries per KV head supported by the decode kernels
+
+// ---- element access ---------------------------------------------------------
+
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// 16-byte vector -> floats. bf16 widening is exact (bits << 16).
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* o) {
+    o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y);
+    o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+  }
+};
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* o) {
+    o[0] = __uint_as_float(v.x << 16); o[1] = __uint_as_float(v.x & 0xffff0000u);
+    o[2] = __uint_as_float(v.y << 16); o[3] = __uint_as_float(v.y & 0xffff0000u);
+    o[4] = __uint_as_float(v.z << 16); o[5] = __uint_as_float(v.z & 0xffff0000u);
+    o[6] = __uint_as_float(v.w << 16); o[7] = __uint_as_float(v.w & 0xffff0000u);
+  }
+};
+
+// Streaming 16-byte load that does not allocate in L1 (landmark scan).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---- ranking keys -----------------------------------------------------------
+// Order-preserving map float -> uint32 (larger score -> larger key), with
+// -0.0 canonicalised to +0.0 so that the two compare equal, as in the
+// reference's np.argsort(-scores, kind="stable") (selection.py:55-57).
+__device__ __forceinline__ uint32_t score_key(float s) {
+  uint32_t b = __float_as_uint(s);
+  if ((b << 1) == 0u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float key_score(uint32_t u) {
+  uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(b);
+#else
+  float f; memcpy(&f, &b, 4); return f;
+#endif
+}
+
+// Butterfly all-reduce: every lane ends with the same bits (fp add commutes).
+__device__ __forceinline__ float warp_sum_butterfly(float v) {
+  v = v + __shfl_xor_sync(FULL, v, 16);
+  v = v + __shfl_xor_sync(FULL, v, 8);
+  v = v + __shfl_xor_sync(FULL, v, 4);
+  v = v + __shfl_xor_sync(FULL, v, 2);
+  v = v + __shfl_xor_sync(FULL, v, 1);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v = max(v, __shfl_xor_sync(FULL, v, m));
+  return v;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim multiple of 32,
+// <= 1024). `red` needs 33 ints of shared memory. Returns the exclusive
+// prefix; *total receives the block sum.
+__device__ __forceinline__ int block_excl_scan(int v, int* red, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  int inc = warp_incl_scan(v, lane);
+  if (lane == 31) red[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? red[lane] : 0;
+    int wi = warp_incl_scan(w, lane);
+    if (lane < nw) red[lane] = wi - w;
+    if (lane == 31) red[32] = wi;
+  }
+  __syncthreads();
+  int ex = red[warp] + inc - v;
+  *total = red[32];
+  __syncthreads();
+  return ex;
+}
+
+}  // namespace kvb

@@ -1,0 +1,128 @@
+// Internal store representation and kernel launchers of libkvb.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/kvb.h"
+
+struct kvb_higgs_dev {
+  int d = 0, n = 0, group = 0, seed = 0, bits = 0;
+  int groups = 0;       // groups per (sequence, head)
+  int group_bytes = 0;  // packed code bytes per group
+  int rows = 0;         // rows (chunks or tokens) per group = group / head_dim
+  float* codebook = nullptr;  // device [n][d]
+  float* signs = nullptr;     // device [group]
+  uint8_t* codes = nullptr;   // device [B][Hkv][groups][group_bytes]
+  float* scales = nullptr;    // device [B][Hkv][groups]  fp16-exact RMS
+  float* factor = nullptr;    // device [B][Hkv][groups]  fp32(scale / RMS(vq))
+};
+
+struct kvb_store {
+  kvb_store_desc d{};
+  int C = 0;          // chunks per sequence
+  int E = 0;          // kv_heads * head_dim
+  int W = 0;          // resident bitmap words per sequence
+  size_t esz = 4;     // bytes per K/V element
+  // fast tier -------------------------------------------------------------
+  void* lm_dense = nullptr;      // [B][C][E] kv dtype
+  kvb_higgs_dev lm_h;            // HIGGS landmarks over per-head [C, D]
+  kvb_higgs_dev res_h;           // HIGGS residuals over per-head [n, D]
+  int32_t* res_ids = nullptr;    // [B][max_resident] sorted resident tokens
+  int32_t* res_count = nullptr;  // [B]
+  uint32_t* res_bitmap = nullptr;  // [B][W]
+  int32_t* res_prefix = nullptr;   // [B][W] residents before word w
+  void* res_k = nullptr;         // [B][max_resident][E]
+  void* res_v = nullptr;
+  uint16_t* svd_left = nullptr;  // fp16 [B][n][groups][r]
+  uint16_t* svd_right = nullptr; // fp16 [B][groups][r][Dg]
+  // offload tier ------------------------------------------------------------
+  void* off_k = nullptr;         // [B][n][E]  (slow_kind == NONE)
+  void* off_v = nullptr;         // [B][n][E]
+  void* off_k_dev = nullptr;     // device alias when host-mapped
+  void* off_v_dev = nullptr;
+  bool off_host = false;
+};
+
+namespace kvb {
+
+void set_error(const std::string& msg);
+kvb_status cuda_status(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
+cudaError_t ensure_smem(const void* func, size_t bytes);
+
+// ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
+cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
+                               float* scores, cudaStream_t st);
+cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
+                               float* scores, cudaStream_t st);
+// Top-K + token union. mode 0: items are chunks (M = C); mode 1: items are
+// positions in cand_tok (M = per-sequence count m_count[b]).
+struct SelectLaunch {
+  const float* scores;    // [B][M_stride]
+  int M_stride;
+  const int32_t* m_count; // may be null: every sequence has M_stride items
+  int K;                  // per sequence (clamped to M for mode 1)
+  int rank_order;
+  int mode;
+  const int32_t* cand_tok;  // mode 1 [B][M_stride]
+  int32_t* sel_ids;         // [B][K] item ids (rank order if requested)
+  int32_t* token_ids;       // [B][cap] (may be null: skip union)
+  int32_t* n_tokens;        // [B]
+  int cap;
+  int with_residents;
+  int32_t* err_flag;        // device int, set on capacity overflow
+};
+cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_t st);
+size_t select_smem_bytes(const kvb_store* s, int K, int mode);
+
+// Ascending list of the tokens of the selected chunks (Appendix-E stage 2).
+cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,
+                                    int32_t* cand_tok, int32_t* cand_count,
+                                    int32_t* cand_chunks_sorted, cudaStream_t st);
+cudaError_t launch_residual_scores(const kvb_store* s, const float* q, int G,
+                                   const float* chunk_scores, const int32_t* cand_chunks_sorted,
+                                   int n_cand, float* tok_scores, cudaStream_t st);
+cudaError_t launch_residual_full_scores(const kvb_store* s, const float* chunk_scores,
+                                        const int32_t* cand_tok, const int32_t* cand_count,
+                                        int cand_stride, const float* tok_scores,
+                                        float* full, cudaStream_t st);
+
+struct AttendLaunch {
+  const float* q;
+  int G;
+  const int32_t* token_ids;
+  const int32_t* n_tokens;
+  int cap;
+  float* out;
+  float* lse;
+  int k_path;
+  void* ws;
+};
+size_t attend_ws_bytes(const kvb_store* s, int G, int cap);
+cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
+cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
+                                   int D, float* out, float* lse, cudaStream_t st);
+cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
+                              int32_t* out, cudaStream_t st);
+
+// ---- build ---------------------------------------------------------------
+cudaError_t launch_chunk_means(const kvb_store* s, const void* keys, void* out_dense,
+                               float* out_f32_headmajor, cudaStream_t st);
+cudaError_t launch_higgs_quantize(const kvb_store* s, const kvb_higgs_dev& h, const float* src,
+                                  int rows_per_head, cudaStream_t st);
+cudaError_t launch_higgs_factor(const kvb_store* s, const kvb_higgs_dev& h, cudaStream_t st);
+cudaError_t launch_higgs_dequant(const kvb_store* s, const kvb_higgs_dev& h, int rows_per_head,
+                                 float* out_rowmajor, cudaStream_t st);
+cudaError_t launch_residual_source(const kvb_store* s, const void* keys, const float* lm_dq,
+                                   float* out_headmajor, cudaStream_t st);
+cudaError_t launch_chunk_cosine(const kvb_store* s, const void* keys, const float* lm_dq,
+                                double* out, cudaStream_t st);
+cudaError_t launch_residency(const kvb_store* s, const void* keys, const void* values,
+                             cudaStream_t st);
+cudaError_t launch_dense_to_f32(const kvb_store* s, float* out, cudaStream_t st);
+
+}  // namespace kvb

@@ -1,0 +1,366 @@
+// K2 -- deterministic top-K (selection.py:55-57) and K2b -- sorted token union
+// with the always-resident tokens (selection.py:60-69, kvstore.py:230-240).
+//
+// One 1024-thread CTA per sequence:
+//  1. radix select, MSB first, 8-bit digits over the order-preserving 32-bit
+//     key of each score (-0 canonicalised to +0). Histograms are built with
+//     warp-aggregated shared atomics (__match_any_sync). After four passes the
+//     K-th key T and the number of ties to take are known exactly;
+//  2. collect keys > T, plus the lowest-id ties (ordered block scans), which
+//     reproduces np.argsort(-s, kind="stable")[:K] as a set;
+//  3. optional rank order: bitonic sort of the K winners on the 64-bit key
+//     (key << 32 | ~id), i.e. score descending, id ascending;
+//  4. token union: the selected chunks' tokens are OR-ed into the sequence's
+//     resident bitmap (n bits, shared memory) and compacted in ascending order
+//     by a block scan -- the sorted np.unique of the reference, with no sort.
+
+#include "kvb_common.cuh"
+#include "kvb_internal.h"
+
+namespace kvb {
+
+namespace {
+
+constexpr int kSelThreads = 1024;
+
+struct SelParams {
+  const float* scores;
+  int M_stride;
+  const int32_t* m_count;
+  int K;
+  int rank_order;
+  int mode;
+  const int32_t* cand_tok;
+  int32_t* sel_ids;
+  int32_t* token_ids;
+  int32_t* n_tokens;
+  int cap;
+  int with_residents;
+  int32_t* err_flag;
+  const uint32_t* res_bitmap;
+  int n, cs, W, P;
+};
+
+__global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int hist[256];
+  __shared__ int red[33];
+  __shared__ int s_digit, s_krem, s_eq, s_cnt;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x;
+  const int b = blockIdx.x;
+  const float* sc = p.scores + (size_t)b * p.M_stride;
+  const int M = p.m_count ? p.m_count[b] : p.M_stride;
+  const int K = p.K < M ? p.K : M;
+
+  uint64_t* keys64 = reinterpret_cast<uint64_t*>(smem_raw);          // [P] (rank order)
+  int32_t* ids = reinterpret_cast<int32_t*>(smem_raw);               // [K] (set only)
+  const size_t sel_bytes = p.rank_order ? (size_t)p.P * 8 : (size_t)((p.K + 3) & ~3) * 4;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sel_bytes);  // [W]
+
+  // ---- 1. radix select ----------------------------------------------------
+  uint32_t prefix = 0u, pmask = 0u;
+  int krem = K, eqcnt = 0;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = tid; i < 256; i += nthr) hist[i] = 0;
+    __syncthreads();
+    for (int base = warp * 32; base < M; base += nthr) {
+      const int i = base + lane;
+      const bool valid = i < M;
+      const uint32_t u = valid ? score_key(sc[i]) : 0u;
+      const bool pred = valid && ((u & pmask) == prefix);
+      const uint32_t dg = (u >> shift) & 255u;
+      const unsigned peers = __match_any_sync(FULL, pred ? dg : (256u + lane));
+      if (pred && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], __popc(peers));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int c[8], loc = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[lane * 8 + j];
+        loc += c[j];
+      }
+      int suf = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_down_sync(FULL, suf, o);
+        if (lane + o < 32) suf += t;
+      }
+      const int above = suf - loc;
+      const bool hit = (above < krem) && (krem <= suf);
+      if (hit) {
+        int acc = above;
+        for (int j = 7; j >= 0; --j) {
+          if (acc + c[j] >= krem) {
+            s_digit = lane * 8 + j;
+            s_krem = krem - acc;
+            s_eq = c[j];
+            break;
+          }
+          acc += c[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)s_digit << shift;
+    pmask |= 0xffu << shift;
+    krem = s_krem;
+    eqcnt = s_eq;
+    __syncthreads();
+  }
+  const uint32_t T = prefix;
+
+  // ---- 2. collect ----------------------------------------------------------
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  const bool all_ties = (krem == eqcnt);
+  auto put = [&](int pos, uint32_t u, int i) {
+    if (p.rank_order)
+      keys64[pos] = ((uint64_t)u << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
+    else
+      ids[pos] = i;
+  };
+  for (int base = warp * 32; base < M; base += nthr) {
+    const int i = base + lane;
+    const bool valid = i < M;
+    const uint32_t u = valid ? score_key(sc[i]) : 0u;
+    const bool take = valid && (u > T || (all_ties && u == T));
+    const unsigned m = __ballot_sync(FULL, take);
+    int wb = 0;
+    if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+    wb = __shfl_sync(FULL, wb, 0);
+    if (take) put(wb + __popc(m & ((1u << lane) - 1u)), u, i);
+  }
+  __syncthreads();
+  if (!all_ties) {
+    // lowest ids among the ties: rounds in ascending id order
+    const int start = s_cnt;
+    int taken = 0;
+    for (int base = 0; base < M && taken < krem; base += nthr) {
+      const int i = base + tid;
+      const bool eq = (i < M) && score_key(sc[i]) == T;
+      int tot;
+      const int ex = block_excl_scan(eq ? 1 : 0, red, &tot);
+      if (eq && taken + ex < krem) put(start + taken + ex, T, i);
+      taken += tot;
+    }
+    __syncthreads();
+  }
+
+  // ---- 3. rank order ---------------------------------------------------------
+  int32_t* out_ids = p.sel_ids + (size_t)b * p.K;
+  if (p.rank_order) {
+    for (int i = K + tid; i < p.P; i += nthr) keys64[i] = 0ull;
+    __syncthreads();
+    for (int k = 2; k <= p.P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = tid; t < p.P / 2; t += nthr) {
+          const int i = (t / j) * 2 * j + (t % j);
+          const int l = i + j;
+          const bool desc = (i & k) == 0;
+          const uint64_t a = keys64[i], c = keys64[l];
+          if ((a < c) == desc) {
+            keys64[i] = c;
+            keys64[l] = a;
+          }
+        }
+        __syncthreads();
+      }
+    for (int r = tid; r < p.K; r += nthr)
+      out_ids[r] = r < K ? (int32_t)(0xffffffffu - (uint32_t)keys64[r]) : -1;
+  } else {
+    for (int r = tid; r < p.K; r += nthr) out_ids[r] = r < K ? ids[r] : -1;
+  }
+  if (!p.token_ids) return;
+  __syncthreads();
+
+  // ---- 4. token union ----------------------------------------------------------
+  const uint32_t* rb = p.res_bitmap + (size_t)b * p.W;
+  for (int w = tid; w < p.W; w += nthr) bm[w] = p.with_residents ? rb[w] : 0u;
+  __syncthreads();
+  for (int r = tid; r < K; r += nthr) {
+    const int item = p.rank_order ? (int)(0xffffffffu - (uint32_t)keys64[r]) : ids[r];
+    if (p.mode == 0) {
+      const int t0 = item * p.cs;
+      const int t1 = min(t0 + p.cs, p.n);
+      for (int t = t0; t < t1; ++t) atomicOr(&bm[t >> 5], 1u << (t & 31));
+    } else {
+      const int t = p.cand_tok[(size_t)b * p.M_stride + item];
+      atomicOr(&bm[t >> 5], 1u << (t & 31));
+    }
+  }
+  __syncthreads();
+  const int wpt = (p.W + nthr - 1) / nthr;
+  const int w0 = tid * wpt;
+  int cnt = 0;
+  for (int w = w0; w < w0 + wpt && w < p.W; ++w) cnt += __popc(bm[w]);
+  int total;
+  int pos = block_excl_scan(cnt, red, &total);
+  int32_t* dst = p.token_ids + (size_t)b * p.cap;
+  for (int w = w0; w < w0 + wpt && w < p.W; ++w) {
+    uint32_t bits = bm[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos < p.cap) dst[pos] = w * 32 + bit;
+      ++pos;
+    }
+  }
+  if (tid == 0) {
+    p.n_tokens[b] = total < p.cap ? total : p.cap;
+    if (total > p.cap && p.err_flag) atomicOr(p.err_flag, 1);
+  }
+}
+
+int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+size_t select_smem_bytes(const kvb_store* s, int K, int mode) {
+  (void)mode;
+  const size_t sel = (size_t)next_pow2(K < 1 ? 1 : K) * 8;
+  return sel + (size_t)s->W * 4;
+}
+
+cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_t st) {
+  SelParams p;
+  p.scores = a.scores;
+  p.M_stride = a.M_stride;
+  p.m_count = a.m_count;
+  p.K = a.K;
+  p.rank_order = a.rank_order;
+  p.mode = a.mode;
+  p.cand_tok = a.cand_tok;
+  p.sel_ids = a.sel_ids;
+  p.token_ids = a.token_ids;
+  p.n_tokens = a.n_tokens;
+  p.cap = a.cap;
+  p.with_residents = a.with_residents;
+  p.err_flag = a.err_flag;
+  p.res_bitmap = s->res_bitmap;
+  p.n = s->d.n_tokens;
+  p.cs = s->d.chunk_size;
+  p.W = s->W;
+  p.P = next_pow2(a.K < 1 ? 1 : a.K);
+  const size_t sel = a.rank_order ? (size_t)p.P * 8 : (size_t)((a.K + 3) & ~3) * 4;
+  const size_t smem = sel + (a.token_ids ? (size_t)s->W * 4 : 0);
+  ensure_smem((const void*)k2_select, smem);
+  count_launch();
+  k2_select<<<s->d.batch, kSelThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Appendix-E candidate token list (selection.py:152-153): candidate chunks in
+// ascending id order and their tokens, ascending.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+k_candidate_tokens(const int32_t* __restrict__ cand, int n_cand, int C, int n, int cs,
+                   int32_t* __restrict__ cand_tok, int32_t* __restrict__ cand_count,
+                   int32_t* __restrict__ cand_sorted) {
+  extern __shared__ uint32_t cbm[];
+  __shared__ int red[33];
+  const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  const int Wc = (C + 31) / 32;
+  for (int w = tid; w < Wc; w += nthr) cbm[w] = 0u;
+  __syncthreads();
+  for (int r = tid; r < n_cand; r += nthr) {
+    const int c = cand[(size_t)b * n_cand + r];
+    atomicOr(&cbm[c >> 5], 1u << (c & 31));
+  }
+  __syncthreads();
+  const int wpt = (Wc + nthr - 1) / nthr;
+  const int w0 = tid * wpt;
+  int cnt = 0;
+  for (int w = w0; w < w0 + wpt && w < Wc; ++w) cnt += __popc(cbm[w]);
+  int total;
+  int pos = block_excl_scan(cnt, red, &total);
+  for (int w = w0; w < w0 + wpt && w < Wc; ++w) {
+    uint32_t bits = cbm[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int c = w * 32 + bit;
+      cand_sorted[(size_t)b * n_cand + pos] = c;
+      const int t0 = c * cs, t1 = min(t0 + cs, n);
+      for (int t = t0; t < t1; ++t) cand_tok[(size_t)b * n_cand * cs + (size_t)pos * cs + (t - t0)] = t;
+      ++pos;
+    }
+  }
+  if (tid == 0) {
+    // only the last chunk can be short, and it sorts last
+    const bool tail = (cbm[(C - 1) >> 5] >> ((C - 1) & 31)) & 1u;
+    cand_count[b] = total * cs - (tail ? (C * cs - n) : 0);
+  }
+}
+
+cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,
+                                    int32_t* cand_tok, int32_t* cand_count,
+                                    int32_t* cand_chunks_sorted, cudaStream_t st) {
+  const size_t smem = (size_t)((s->C + 31) / 32) * 4;
+  ensure_smem((const void*)k_candidate_tokens, smem);
+  count_launch();
+  k_candidate_tokens<<<s->d.batch, 1024, smem, st>>>(cand_chunks, n_cand, s->C, s->d.n_tokens,
+                                                      s->d.chunk_size, cand_tok, cand_count,
+                                                      cand_chunks_sorted);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Cross-shard top-K merge: P*K candidates (global ids) per
+// sequence -> global top-K in rank order by bitonic sort on (key, ~gid).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int parts, int batch,
+             int k, int P, int32_t* __restrict__ out) {
+  extern __shared__ uint64_t mk[];
+  const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  const int tot = parts * k;
+  for (int i = tid; i < P; i += nthr) {
+    uint64_t v = 0ull;
+    if (i < tot) {
+      const int pp = i / k, j = i - pp * k;
+      const size_t off = ((size_t)pp * batch + b) * k + j;
+      const int id = gid[off];
+      if (id >= 0) v = ((uint64_t)score_key(sc[off]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)id);
+    }
+    mk[i] = v;
+  }
+  __syncthreads();
+  for (int kk = 2; kk <= P; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < P / 2; t += nthr) {
+        const int i = (t / j) * 2 * j + (t % j);
+        const int l = i + j;
+        const bool desc = (i & kk) == 0;
+        const uint64_t a = mk[i], c = mk[l];
+        if ((a < c) == desc) {
+          mk[i] = c;
+          mk[l] = a;
+        }
+      }
+      __syncthreads();
+    }
+  for (int r = tid; r < k; r += nthr)
+    out[(size_t)b * k + r] = mk[r] ? (int32_t)(0xffffffffu - (uint32_t)mk[r]) : -1;
+}
+
+cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
+                              int32_t* out, cudaStream_t st) {
+  const int P = next_pow2(parts * k);
+  const size_t smem = (size_t)P * 8;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  ensure_smem((const void*)k_merge_topk, smem);
+  count_launch();
+  k_merge_topk<<<batch, 1024, smem, st>>>(sc, ids, parts, batch, k, P, out);
+  return cudaGetLastError();
+}
+
+}  // namespace kvb
