@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Decode-step benchmark of the kvb sparse-attention hot path.
+
+Workload (BASELINE.json configs[1], "C2"): Llama-3.1-8B shape -- 32 layers,
+Hkv 8, G 4 (32 query heads), D 128 -- 128K context, batch 8, bf16 K/V,
+synthetic data. Default variant: the ShadowKV baseline (chunk-8 bf16
+landmarks, rank-160 SVD keys over [n, 1024], V in the HBM offload tier,
+budget 2048 tokens + 384 outlier + 32 local). One step = select + gather +
+attend for all 32 layers x 8 sequences, i.e. 8 decode tokens.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--variant ...]
+
+Multi-GPU (torchrun, one rank per GPU): every rank serves its own batch of 8
+sequences (replicas, weak scaling, no collective on this path); timing is the
+max over ranks. The sequence-sharded 1M-context config is ``--variant c4``.
+
+The JSON line carries the roofline of the dominant kernel (K1 landmark scan,
+CUDA events on its launching stream), the whole-step roofline, the end-to-end
+rate through the public API with host buffers, the CPU oracle baseline, and
+the SM clocks sampled (NVML) during the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-attn decode tok/s, 128K ctx Llama-3-8B shape; % of HBM/PCIe roofline"
+HBM_FALLBACK = 6650.0
+
+VARIANTS = {
+    # name: (description, landmark, chunk, slow, budget tokens, outliers, local)
+    "shadowkv": "ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
+    "higgs2c1": "paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kvb", choices=["kvb", "reference"])
+    ap.add_argument("--variant", default="shadowkv", choices=sorted(VARIANTS))
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--budget", type=int, default=2048)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="run N eager steps after setup (for ncu) and exit")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------
+# model state: one DeviceStore (batch B) per layer
+# ---------------------------------------------------------------------------
+def build_layers(a, rank):
+    import torch
+
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    H, G, D = 8, 4, 128
+    stores = []
+    gen = torch.Generator(device="cuda")
+    for layer in range(a.layers):
+        gen.manual_seed(1000 * rank + layer)
+        shape = (a.batch, a.ctx, H, D)
+        k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
+        v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
+        if a.variant == "shadowkv":
+            st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
+                             dtype=torch.bfloat16, landmark=S.scheme_none(),
+                             slow=S.scheme_svd(160, H * D), svd_groups=1,
+                             outlier_tokens=384, local_window=32)
+        else:
+            st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=1,
+                             dtype=torch.bfloat16, landmark=S.scheme_higgs(2),
+                             outlier_tokens=384, local_window=32)
+        st.build(k, v)
+        del k, v
+        stores.append(st)
+    torch.cuda.synchronize()
+    return stores, (H, G, D)
+
+
+def algorithmic_bytes(a, st, G):
+    """Per (layer, sequence) bytes the step must move, bf16."""
+    H, D, n = st.heads, st.dim, st.n
+    E = H * D
+    K = st.n_select(a.budget / n)
+    S_tok = K * st.cs
+    R = st.max_resident
+    q = H * G * D * 4 + H * G * D * 4  # queries in, output out
+    if a.variant == "shadowkv":
+        lm = st.C * E * 2
+        r = st.slow.rank
+        return {"landmarks": lm, "left_rows": S_tok * r * 2, "right": r * E * 2,
+                "values": S_tok * E * 2, "resident_kv": R * E * 2 * 2, "q_out": q}
+    lm = st.info.n_groups_landmark * H * (st.landmark.group_size // st.landmark.d *
+                                          (st.landmark.n.bit_length() - 1) // 8 + 4)
+    return {"landmark_codes": lm, "kv": S_tok * E * 2 * 2, "resident_kv": R * E * 2 * 2, "q_out": q}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample (one layer x one sequence)
+# ---------------------------------------------------------------------------
+def oracle_slice(a, seed=0):
+    import numpy as np
+
+    from oracle import kvlab_port as P
+
+    H, G, D, n = 8, 4, 128, a.ctx
+    rng = np.random.default_rng(seed)
+    k = rng.standard_normal((H, n, D), dtype=np.float32)
+    v = rng.standard_normal((H, n, D), dtype=np.float32)
+    if a.variant == "shadowkv":
+        cs = 8
+        lm = np.stack([P.chunk_means(k[h], cs) for h in range(H)])
+        outl = P.outlier_chunks(k, lm, cs, 384)
+        # decode cost does not depend on factor values: synthetic fp16 factors
+        l16 = (rng.standard_normal((n, 160), dtype=np.float32) * 0.5).astype(np.float16)
+        r16 = (rng.standard_normal((160, H * D), dtype=np.float32) * 0.08).astype(np.float16)
+        slow_k = P.svd16_reconstruct(l16, r16).reshape(n, H, D).transpose(1, 0, 2)
+        budget = P.Budget(a.budget / n, 384, 32)
+        st = P.store_from_parts(k, v, cs, budget, lm, outl, slow_k=np.ascontiguousarray(slow_k))
+    else:
+        cs = 1
+        st = P.build(k[:, :4096], v[:, :4096], 1, P.Scheme.none())  # geometry only
+        lm = k.copy()  # dequantised landmarks at chunk 1 have the keys' shape
+        budget = P.Budget(a.budget / n, 384, 32)
+        st = P.store_from_parts(k, v, cs, budget, lm, (0,))
+    qs = [rng.standard_normal((H, G, D), dtype=np.float32) for _ in range(4)]
+    return st, budget, qs
+
+
+def time_oracle_slice(st, budget, q):
+    from oracle import kvlab_port as P
+
+    t0 = time.perf_counter()
+    sel = P.select_by_landmarks(st, q, budget)
+    P.sparse_attention(q, st, sel.token_ids)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(a):
+    st, budget, qs = oracle_slice(a)
+    times = [time_oracle_slice(st, budget, q) for q in qs]
+    t = sorted(times)[len(times) // 2]
+    cores = os.cpu_count()
+    return {"value": round(1.0 / (a.layers * t), 4), "unit": "tok/s", "cores": cores,
+            "kind": "port",
+            "sample": (f"oracle/kvlab_port.py (numpy, kvlab's arithmetic) select_by_landmarks + "
+                       f"sparse_attention on one (layer, sequence) slice, n={a.ctx}, Hkv 8, G 4, "
+                       f"D 128, fp32, {a.variant}; median of {len(times)} = {t * 1e3:.1f} ms; "
+                       f"tok/s = 1/(layers x t_slice) (kvlab has no batching); "
+                       f"numpy BLAS may use up to {cores} threads")}
+
+
+def run_reference(a):
+    """--impl reference: the reference's CPU path (the oracle port of kvlab,
+    SURVEY 8c) on every host core: one forked worker per core, each timing
+    slices of the same workload; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    st, budget, qs = oracle_slice(a)
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 64))
+    global _REF_STATE
+    _REF_STATE = (st, budget, qs)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_ref_init) as pool:
+        for _ in range(max(1, a.warmup)):
+            pool.map(_ref_slice, range(workers))
+        walls = []
+        for _ in range(a.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_slice, range(workers))
+            walls.append(time.perf_counter() - t0)
+    t_round = sorted(walls)[len(walls) // 2]
+    slices_per_s = workers / t_round
+    tok_s = slices_per_s / a.layers
+    ms_full_step = a.layers * a.batch / slices_per_s * 1e3
+    line = {"metric": METRIC, "value": round(tok_s, 4), "unit": "tok/s", "impl": "reference",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(ms_full_step, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C2 {VARIANTS[a.variant]}", "layers": a.layers,
+                       "batch": a.batch, "ctx": a.ctx, "budget_tokens": a.budget},
+            "cpu_baseline": {"value": round(tok_s, 4), "unit": "tok/s", "cores": workers,
+                             "kind": "port",
+                             "sample": (f"{workers} forked workers x 1 (layer, sequence) slice per "
+                                        f"step, each single-threaded BLAS; full-step time "
+                                        f"extrapolated to {a.layers} layers x {a.batch} seqs")},
+            "e2e": {"value": round(tok_s, 4), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+_REF_STATE = None
+
+
+def _ref_init():
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _ref_slice(i):
+    st, budget, qs = _REF_STATE
+    return time_oracle_slice(st, budget, qs[i % len(qs)])
+
+
+# ---------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_08426_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+
+    t_build = time.perf_counter()
+    stores, (H, G, D) = build_layers(a, rank)
+    t_build = time.perf_counter() - t_build
+    L_ = a.layers
+    B = a.batch
+    K = stores[0].n_select(a.budget / a.ctx)
+    plans = [st.decode_plan(G, K) for st in stores]
+    qgen = torch.Generator(device="cuda").manual_seed(7 + rank)
+    q_dev = torch.randn((L_, B, H, G, D), generator=qgen, device="cuda")
+    out_dev = torch.empty_like(q_dev)
+    q_host = q_dev.cpu().pin_memory()
+    out_host = torch.empty_like(q_host).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for l in range(L_):
+            plans[l].run(q_dev[l], out_dev[l])
+
+    if a.profile_steps:
+        for _ in range(a.profile_steps):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    # launches per step (counted on one eager step)
+    c0 = lib.kvb_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = lib.kvb_launch_count() - c0
+
+    graph = None
+    if not a.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+
+    for _ in range(a.warmup):
+        run()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            run()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B / (ms_max / 1e3)
+
+    # ---- end to end through the public API with host buffers ---------------
+    def e2e_step():
+        q_dev.copy_(q_host, non_blocking=True)
+        for l in range(L_):
+            plans[l].run(q_dev[l], out_dev[l])
+        out_host.copy_(out_dev, non_blocking=True)
+
+    for _ in range(max(2, a.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(a.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3 / a.steps
+    e2e_ms = max(e0.elapsed_time(e1) / a.steps, wall_ms)
+    te = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B / (float(te.item()) / 1e3)
+
+    # ---- per-kernel timing (CUDA events on the launching stream) -----------
+    st0 = stores[0]
+    reps = 3
+    scores = [torch.empty((B, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for _ in range(reps):
+            for l in range(L_):
+                fn(l)
+        evs[1].record(stream)
+        torch.cuda.synchronize()
+        return evs[0].elapsed_time(evs[1]) / (reps * L_)
+
+    k1_ms = timed(lambda l=0: stores[l].score(q_dev[l], out=scores[l]))
+    sel_outs = [None] * L_
+
+    def do_select(l=0):
+        sel_outs[l] = stores[l].select(q_dev[l], K, rank_order=False, want_scores=False)
+    sel_ms = timed(do_select)
+
+    def do_attend(l=0):
+        c, s_, tok, ntok = sel_outs[l]
+        stores[l].attend(q_dev[l], tok, ntok)
+    att_ms = timed(do_attend)
+
+    hbm, peak_kind = peaks()
+    ab = algorithmic_bytes(a, st0, G)
+    lm_key = "landmarks" if a.variant == "shadowkv" else "landmark_codes"
+    k1_bytes = B * (ab[lm_key] + H * G * D * 4)
+    k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
+    step_bytes = L_ * B * sum(ab.values())
+    step_gbs = step_bytes / (ms_max / 1e3) / 1e9
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not a.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(a)
+            except Exception as exc:  # never lose the GPU line over the baseline
+                cpu = {"value": None, "error": repr(exc)}
+        clk = sampler.summary()
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tok/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (torch.randn K/V per layer; random queries)",
+            "config": {"workload": f"C2 {VARIANTS[a.variant]}",
+                       "model": "Llama-3.1-8B shape (32 layers, 32 q / 8 kv heads, d 128)",
+                       "global_batch": world * B, "seq_len": a.ctx, "layers": L_,
+                       "chunk": st0.cs, "budget_tokens": a.budget, "selected_chunks": K,
+                       "parallelism": f"dp{world} (replicas)",
+                       "l2": f"inputs exceed L2: {step_bytes / 1e9:.1f} GB algorithmic bytes per step",
+                       "cuda_graph": graph is not None},
+            "roofline": {"bound": "hbm", "kernel": "k1 landmark scan (kvb_score_landmarks)",
+                         "achieved": round(k1_gbs, 1), "peak": hbm, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(k1_gbs / hbm, 4),
+                         "algorithmic_bytes_per_launch": k1_bytes,
+                         "avg_launch_ms": round(k1_ms, 5), "traffic": None},
+            "step_roofline": {"achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s",
+                              "frac": round(step_gbs / hbm, 4),
+                              "algorithmic_bytes_per_step": step_bytes,
+                              "per_layer_seq_bytes": ab},
+            "breakdown_ms_per_layer": {"k1_score": round(k1_ms, 5),
+                                       "select_total": round(sel_ms, 5),
+                                       "attend_total": round(att_ms, 5)},
+            "e2e": {"value": round(e2e_value, 2), "unit": "tok/s",
+                    "h2d_bytes_per_step": q_host.numel() * 4,
+                    "d2h_bytes_per_step": out_host.numel() * 4,
+                    "ms_per_step": round(float(te.item()), 4),
+                    "path": "pinned host q -> 32 x kvb_decode_step (C-ABI via ctypes) -> pinned host out"},
+            "gpu_launches": int(launches_per_step * a.steps),
+            "launches_per_step": int(launches_per_step),
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "build_s": round(t_build, 1),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,6 +190,12 @@ kvb_status kvb_select(kvb_store* store, const float* queries, const kvb_select_a
                       void* stream);
 int64_t kvb_select_workspace_bytes(const kvb_store* store, const kvb_select_args* args);
 
+/* Landmark scores only (selection.py:83-84: einsum + _aggregate), device
+ * float32 scores [batch][n_chunks]. The K1 kernel of kvb_select.            */
+kvb_status kvb_score_landmarks(kvb_store* store, const float* queries,
+                               int32_t queries_per_head, int32_t aggregation, float* scores,
+                               void* stream);
+
 /* approx_topk_residual (selection.py:132-171): k tokens, n_cand candidate
  * chunks. chunk_ids receives the candidate chunks (rank order); scores
  * (float32 [batch][n_tokens], may be NULL) = landmark estimate, refined on

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("kvb_landmarks_dequantized", _I32, [_P, _P, _P]),
     ("kvb_residuals_dequantized", _I32, [_P, _P, _P]),
     ("kvb_select", _I32, [_P, _P, C.POINTER(SelectArgs), _P, _P, _P, _P, _P, _I64, _P]),
+    ("kvb_score_landmarks", _I32, [_P, _P, _I32, _I32, _P, _P]),
     ("kvb_select_workspace_bytes", _I64, [_P, C.POINTER(SelectArgs)]),
     ("kvb_select_residual", _I32, [_P, _P, C.POINTER(ResidualArgs), _P, _P, _P, _P, _P, _I64, _P]),
     ("kvb_select_residual_workspace_bytes", _I64, [_P, C.POINTER(ResidualArgs)]),

@@ -22,7 +22,7 @@ SOURCES = ["kvb_api.cu", "kvb_score.cu", "kvb_select.cu", "kvb_attend.cu", "kvb_
            "kvb_recon.cu"]
 HEADERS = ["kvb_common.cuh", "kvb_internal.h", "kvb_tc.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-diag-suppress", "177"]
 
 

@@ -485,6 +485,15 @@ static kvb_status score_landmarks(kvb_store* s, const float* q, int G, int agg, 
   return KVB_OK;
 }
 
+kvb_status kvb_score_landmarks(kvb_store* s, const float* q, int32_t G, int32_t agg,
+                               float* scores, void* stream) {
+  if (!s || !q || !scores) KVB_FAIL(KVB_EINVAL, "null argument");
+  kvb_status ks = check_queries(s, G);
+  if (ks != KVB_OK) return ks;
+  if (agg != KVB_AGG_SUM && agg != KVB_AGG_MAX) KVB_FAIL(KVB_EINVAL, "unknown aggregation");
+  return score_landmarks(s, q, G, agg, scores, as_stream(stream));
+}
+
 int64_t kvb_select_workspace_bytes(const kvb_store* s, const kvb_select_args* a) {
   if (!s || !a) return -1;
   return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned(4) + 256);

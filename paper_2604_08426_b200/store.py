@@ -287,6 +287,18 @@ class DeviceStore:
         return out
 
     # ----------------------------------------------------------------- decode
+    def score(self, q: torch.Tensor, aggregation: str = "sum", out: torch.Tensor | None = None):
+        """Landmark scores [B, C] float32 (selection.py:83-84)."""
+        G = self._check_q(q)
+        if out is None:
+            out = torch.empty((self.batch, self.C), dtype=torch.float32, device="cuda")
+        agg = {"sum": L.KVB_AGG_SUM, "max": L.KVB_AGG_MAX}.get(aggregation)
+        if agg is None:
+            raise ValueError(f"unknown aggregation {aggregation!r}")
+        L.check(self.lib.kvb_score_landmarks(self.h, _ptr(q), G, agg, _ptr(out), _stream()),
+                "kvb_score_landmarks")
+        return out
+
     def select(self, q: torch.Tensor, n_select: int, aggregation: str = "sum",
                rank_order: bool = True, want_scores: bool = True):
         """select_by_landmarks (selection.py:72-87), batched. Returns
