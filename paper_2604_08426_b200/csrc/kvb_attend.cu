@@ -26,28 +26,30 @@ namespace kvb {
 
 namespace {
 
-constexpr int TT = 64;          // tokens per tile
 constexpr int kAttThreads = 256;
+constexpr int kMaxDpl = 4;   // head_dim <= 128
 
 struct AttParams {
   const float* q;        // [B][H][G][D]
   const int32_t* tok;    // [B][cap]
   const int32_t* ntok;   // [B]
-  int cap, G, H, D, n, W, Rcap, r, sgroups;
+  int cap, G, H, D, n, W, Rcap, r, sgroups, max_per;
   const uint32_t* res_bm;
   const int32_t* res_prefix;
   const void* res_k;
   const void* res_v;
   const void* off_k;     // slow NONE
   const void* off_v;
-  const uint16_t* left;  // slow SVD
+  const uint16_t* left;  // slow SVD, fp16 [B][n][sgroups][r]
   const float* qt;       // [B][H][G][r]
   float scale;
   int slow_svd;
-  float* pm;             // [B][tiles][H][G]
+  float* pm;             // [B][splits][H*G]
   float* pl;
-  float* po;             // [B][tiles][H][G][D]
-  int tiles;
+  float* po;             // [B][splits][H*G][D]
+  // shared-memory geometry (bytes)
+  int krow, kpad_head, lrow, vrow;   // row strides; kpad_head = padded head stride (bytes)
+  int off_qt, off_lg, off_alpha, off_tok, off_buf, buf_bytes, boff_l, boff_v;
 };
 
 __device__ __forceinline__ int resident_slot(const uint32_t* bm, const int32_t* pre, int t) {
@@ -57,199 +59,274 @@ __device__ __forceinline__ int resident_slot(const uint32_t* bm, const int32_t* 
   return pre[t >> 5] + __popc(w & (bit - 1u));
 }
 
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 template <typename T>
-__device__ __forceinline__ void load_span(const T* __restrict__ src, int cnt, bool vec, float* out) {
-  if (vec) {
-    constexpr int VW = 16 / sizeof(T);
-    for (int v = 0; v < cnt / VW; ++v) {
-      const uint4 x = *reinterpret_cast<const uint4*>(src + v * VW);
-      Vec<T>::unpack(x, out + v * VW);
+__device__ __forceinline__ float2 ld_pair(const T* p);
+template <>
+__device__ __forceinline__ float2 ld_pair<float>(const float* p) {
+  return *reinterpret_cast<const float2*>(p);
+}
+template <>
+__device__ __forceinline__ float2 ld_pair<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+
+// Issue the cp.async copies of sub-tile rows [i0, i0+ns) of this CTA's token
+// range into one buffer: exact K rows (head-padded), fp16 left rows (SVD
+// tokens), V rows. Row sizes are multiples of 16 B on the fast path, else 4 B.
+template <typename T>
+__device__ __forceinline__ void stage_rows(const AttParams& p, int b, const int* tok_s,
+                                           const int* slot_s, int i0, int ns,
+                                           unsigned char* buf) {
+  const int E = p.H * p.D;
+  const int esz = sizeof(T);
+  const bool v16 = (E * esz) % 16 == 0;
+  const bool k16 = v16 && ((p.D * esz) % 16 == 0);
+  const int gran_v = v16 ? 16 : 4;
+  const int gran_k = k16 ? 16 : 4;
+  const int kc = E * esz / gran_k;                  // K chunks per row
+  const int lbytes = p.slow_svd ? p.sgroups * p.r * 2 : 0;
+  const bool l16 = (lbytes % 16) == 0;
+  const int gran_l = l16 ? 16 : 4;
+  const int lc = lbytes / gran_l;
+  const int vc = E * esz / gran_v;
+  const int cpt = kc + lc + vc;
+  const int head_chunks = (p.D * esz) / gran_k;
+  unsigned char* kb = buf;
+  unsigned char* lb = buf + p.boff_l;
+  unsigned char* vb = buf + p.boff_v;
+  const unsigned char* rk = static_cast<const unsigned char*>(p.res_k) + (size_t)b * p.Rcap * E * esz;
+  const unsigned char* rv = static_cast<const unsigned char*>(p.res_v) + (size_t)b * p.Rcap * E * esz;
+  const unsigned char* ok = static_cast<const unsigned char*>(p.off_k);
+  const unsigned char* ov = static_cast<const unsigned char*>(p.off_v);
+  for (int idx = threadIdx.x; idx < ns * cpt; idx += blockDim.x) {
+    const int j = idx / cpt;
+    const int c = idx - j * cpt;
+    const int slot = slot_s[i0 + j];
+    const size_t tok = (size_t)tok_s[i0 + j];
+    const bool exact = slot >= 0 || !p.slow_svd;
+    if (c < kc) {
+      if (!exact) continue;
+      const unsigned char* src = slot >= 0 ? rk + (size_t)slot * E * esz
+                                           : ok + ((size_t)b * p.n + tok) * E * esz;
+      const int h = c / head_chunks, w = c - h * head_chunks;
+      unsigned char* dst = kb + (size_t)j * p.krow + (size_t)h * p.kpad_head + (size_t)w * gran_k;
+      const unsigned char* s = src + (size_t)c * gran_k;
+      if (k16) cp16(dst, s); else cp4(dst, s);
+    } else if (c < kc + lc) {
+      if (exact) continue;
+      const int w = c - kc;
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.left) +
+                                 ((size_t)b * p.n + tok) * lbytes + (size_t)w * gran_l;
+      unsigned char* dst = lb + (size_t)j * p.lrow + (size_t)w * gran_l;
+      if (l16) cp16(dst, src); else cp4(dst, src);
+    } else {
+      const int w = c - kc - lc;
+      const unsigned char* src = slot >= 0 ? rv + (size_t)slot * E * esz
+                                           : ov + ((size_t)b * p.n + tok) * E * esz;
+      unsigned char* dst = vb + (size_t)j * p.vrow + (size_t)w * gran_v;
+      if (v16) cp16(dst, src + (size_t)w * gran_v); else cp4(dst, src + (size_t)w * gran_v);
     }
-  } else {
-    for (int i = 0; i < cnt; ++i) out[i] = to_f32(src[i]);
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kAttThreads) k5_attend(AttParams p) {
-  extern __shared__ float sm[];
-  const int tile = blockIdx.x, b = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int count_all = p.ntok[b];
-  const int t_begin = tile * TT;
-  if (t_begin >= count_all) return;
-  const int cnt = min(TT, count_all - t_begin);
-  const int H = p.H, G = p.G, D = p.D, E = H * D;
-  const int HG = H * G;
+template <typename T, int TT>
+__global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.y, split = blockIdx.x, nsplit = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int H = p.H, G = p.G, D = p.D, HG = H * G;
+  const int Tb = p.ntok[b];
+  const int per = (Tb + nsplit - 1) / nsplit;
+  const int t0 = split * per;
+  const int cnt = max(0, min(Tb, t0 + per) - t0);
 
-  int* s_tok = reinterpret_cast<int*>(sm);        // TT
-  int* s_slot = s_tok + TT;                       // TT
-  float* qs = reinterpret_cast<float*>(s_slot + TT);  // HG*D
-  float* qts = qs + (size_t)HG * D;               // HG*r (svd)
-  float* lg = qts + (p.slow_svd ? (size_t)HG * p.r : 0);  // HG*TT
-  float* s_m = lg + (size_t)HG * TT;              // HG
-  float* s_l = s_m + HG;                          // HG
+  float* q_s = reinterpret_cast<float*>(sm);                 // [D/2][HG][2]
+  float* qt_s = reinterpret_cast<float*>(sm + p.off_qt);     // [r/2][HG][2]
+  float* lg = reinterpret_cast<float*>(sm + p.off_lg);       // [TT][HG]
+  float* alpha_s = reinterpret_cast<float*>(sm + p.off_alpha);
+  int* tok_s = reinterpret_cast<int*>(sm + p.off_tok);       // [max_per]
+  int* slot_s = tok_s + p.max_per;
+  unsigned char* bufs = sm + p.off_buf;
 
   const float* qb = p.q + (size_t)b * HG * D;
-  for (int i = tid; i < HG * D; i += blockDim.x) qs[i] = qb[i];
+  for (int i = tid; i < HG * D; i += blockDim.x) {
+    const int hg = i / D, d = i - hg * D;
+    q_s[((d >> 1) * HG + hg) * 2 + (d & 1)] = qb[i];
+  }
   if (p.slow_svd) {
     const float* qt = p.qt + (size_t)b * HG * p.r;
-    for (int i = tid; i < HG * p.r; i += blockDim.x) qts[i] = qt[i];
+    for (int i = tid; i < HG * p.r; i += blockDim.x) {
+      const int hg = i / p.r, rr = i - hg * p.r;
+      qt_s[((rr >> 1) * HG + hg) * 2 + (rr & 1)] = qt[i];
+    }
   }
   const uint32_t* bm = p.res_bm + (size_t)b * p.W;
   const int32_t* pre = p.res_prefix + (size_t)b * p.W;
-  for (int i = tid; i < TT; i += blockDim.x) {
-    int t = -1, slot = -1;
-    if (i < cnt) {
-      t = p.tok[(size_t)b * p.cap + t_begin + i];
-      slot = resident_slot(bm, pre, t);
-    }
-    s_tok[i] = t;
-    s_slot[i] = slot;
+  for (int i = tid; i < cnt; i += blockDim.x) {
+    const int t = p.tok[(size_t)b * p.cap + t0 + i];
+    tok_s[i] = t;
+    slot_s[i] = resident_slot(bm, pre, t);
   }
   __syncthreads();
 
-  // ---- phase 1: logits ------------------------------------------------------
-  // 8-lane groups; group gi handles items (token, head).
-  const int sub = lane >> 3, l8 = lane & 7;
-  const int gidx = warp * 4 + sub;
-  const int ngroups = (blockDim.x >> 5) * 4;
-  const T* res_k = static_cast<const T*>(p.res_k) + (size_t)b * p.Rcap * E;
-  const T* off_k = static_cast<const T*>(p.off_k);
-  const bool span_ok = (D % 8) == 0;
-  const int span = span_ok ? D / 8 : 0;
-  const bool vec = span_ok && ((span * (int)sizeof(T)) % 16 == 0);
-  const int items = TT * H;
-  for (int base = 0; base < items; base += ngroups) {
-    const int item = base + gidx;
-    const int t = item / H, h = item - t * H;
-    const bool valid = (item < items) && (t < cnt);
-    float acc[kMaxG];
+  const int nsub = (cnt + TT - 1) / TT;
+  if (nsub > 0) {
+    stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
+  }
+  cp_commit();
+
+  // online-softmax state: warp 0 owns (m, l) per hg; phase-3 threads own o
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+  // phase 3: warp w owns head w (blockDim = 32 * max(8, H))
+  float acc[kMaxG][kMaxDpl];
 #pragma unroll
-    for (int g = 0; g < kMaxG; ++g) acc[g] = 0.f;
-    if (valid) {
-      const int slot = s_slot[t];
-      const int tok = s_tok[t];
-      if (slot >= 0 || !p.slow_svd) {
-        const T* row = slot >= 0 ? res_k + (size_t)slot * E + h * D
-                                 : off_k + ((size_t)b * p.n + tok) * E + h * D;
-        if (span_ok) {
-          float kv[32];
-          for (int c0 = 0; c0 < span; c0 += 32) {
-            const int c = min(32, span - c0);
-            load_span(row + l8 * span + c0, c, vec, kv);
-            for (int g = 0; g < G; ++g) {
-              const float* qq = qs + (size_t)(h * G + g) * D + l8 * span + c0;
-              float a = acc[g];
-              for (int i = 0; i < c; ++i) a = fmaf(qq[i], kv[i], a);
-              acc[g] = a;
-            }
+  for (int g = 0; g < kMaxG; ++g)
+#pragma unroll
+    for (int i = 0; i < kMaxDpl; ++i) acc[g][i] = 0.f;
+  const int dpl = (D + 31) / 32;
+  const int esz = sizeof(T);
+
+  for (int st = 0; st < nsub; ++st) {
+    const int i0 = st * TT;
+    const int ns = min(TT, cnt - i0);
+    unsigned char* buf = bufs + (size_t)(st & 1) * p.buf_bytes;
+    if (st + 1 < nsub) {
+      stage_rows<T>(p, b, tok_s, slot_s, i0 + TT, min(TT, cnt - i0 - TT),
+                    bufs + (size_t)((st + 1) & 1) * p.buf_bytes);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+
+    // ---- phase 1: logits (lane = (h, g)) --------------------------------
+    const unsigned char* kb = buf;
+    const unsigned char* lb = buf + p.boff_l;
+    for (int j = warp; j < ns; j += nwarp) {
+      const int slot = slot_s[i0 + j];
+      const bool exact = slot >= 0 || !p.slow_svd;
+      for (int hg = lane; hg < HG; hg += 32) {
+        const int h = hg / G;
+        float a = 0.f;
+        if (exact) {
+          const T* kr = reinterpret_cast<const T*>(kb + (size_t)j * p.krow + (size_t)h * p.kpad_head);
+          const float2* q2 = reinterpret_cast<const float2*>(q_s) + hg;
+          for (int d = 0; d < D; d += 2) {
+            const float2 kv = ld_pair<T>(kr + d);
+            const float2 qv = q2[(d >> 1) * HG];
+            a = fmaf(qv.x, kv.x, a);
+            a = fmaf(qv.y, kv.y, a);
           }
         } else {
-          for (int d = l8; d < D; d += 8) {
-            const float kv = to_f32(row[d]);
-            for (int g = 0; g < G; ++g) acc[g] = fmaf(qs[(size_t)(h * G + g) * D + d], kv, acc[g]);
+          const int grp = h / (H / p.sgroups);
+          const __half2* lr = reinterpret_cast<const __half2*>(lb + (size_t)j * p.lrow) + grp * (p.r / 2);
+          const float2* t2 = reinterpret_cast<const float2*>(qt_s) + hg;
+          for (int rr = 0; rr < p.r; rr += 2) {
+            const float2 lv = __half22float2(lr[rr >> 1]);
+            const float2 qv = t2[(rr >> 1) * HG];
+            a = fmaf(lv.x, qv.x, a);
+            a = fmaf(lv.y, qv.y, a);
           }
         }
-      } else {
-        // SVD fold: left[t, grp(h), :] . q~[h, g, :]
-        const int hpg = H / p.sgroups;
-        const int grp = h / hpg;
-        const uint16_t* lrow = p.left + (((size_t)b * p.n + tok) * p.sgroups + grp) * p.r;
-        for (int rr = l8; rr < p.r; rr += 8) {
-          const float lv = __half2float(__ushort_as_half(lrow[rr]));
-          for (int g = 0; g < G; ++g) acc[g] = fmaf(lv, qts[(size_t)(h * G + g) * p.r + rr], acc[g]);
+        lg[j * HG + hg] = a * p.scale;
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 2: online softmax update (warp 0) --------------------------
+    if (warp == 0) {
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int hg = lane + 32 * s2;
+        if (hg < HG) {
+          float mx = m_run[s2];
+          for (int j = 0; j < ns; ++j) mx = fmaxf(mx, lg[j * HG + hg]);
+          const float alpha = expf(m_run[s2] - mx);
+          float sum = 0.f;
+          for (int j = 0; j < ns; ++j) {
+            const float e = expf(lg[j * HG + hg] - mx);
+            lg[j * HG + hg] = e;
+            sum += e;
+          }
+          l_run[s2] = l_run[s2] * alpha + sum;
+          m_run[s2] = mx;
+          alpha_s[hg] = alpha;
         }
       }
     }
-#pragma unroll
-    for (int g = 0; g < kMaxG; ++g) {
-      float a = acc[g];
-      a += __shfl_xor_sync(FULL, a, 4);
-      a += __shfl_xor_sync(FULL, a, 2);
-      a += __shfl_xor_sync(FULL, a, 1);
-      acc[g] = a;
-    }
-    if (valid && l8 == 0)
-      for (int g = 0; g < G; ++g) lg[(size_t)(h * G + g) * TT + t] = acc[g] * p.scale;
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // ---- phase 2: per-row max / exp / sum ------------------------------------
-  for (int row = warp; row < HG; row += blockDim.x >> 5) {
-    float* x = lg + (size_t)row * TT;
-    float mx = -INFINITY;
-    for (int t = lane; t < cnt; t += 32) mx = fmaxf(mx, x[t]);
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int t = lane; t < TT; t += 32) {
-      const float e = t < cnt ? expf(x[t] - mx) : 0.f;
-      x[t] = e;
-      sum += e;
-    }
-    sum = warp_sum_butterfly(sum);
-    if (lane == 0) {
-      s_m[row] = mx;
-      s_l[row] = sum;
-    }
-  }
-  __syncthreads();
-
-  // ---- phase 3: o = sum_t p V ----------------------------------------------
-  const T* res_v = static_cast<const T*>(p.res_v) + (size_t)b * p.Rcap * E;
-  const T* off_v = static_cast<const T*>(p.off_v);
-  const bool dspan = (D % 32) == 0;
-  const int per = dspan ? D / 32 : 0;
-  const bool vvec = dspan && ((per * (int)sizeof(T)) % 16 == 0);
-  const size_t pbase = ((size_t)b * p.tiles + tile) * HG;
-  for (int h = warp; h < H; h += blockDim.x >> 5) {
-    if (dspan && per <= 8) {
-      float acc[kMaxG][8];
+    // ---- phase 3: o = alpha*o + sum_j p_j V_j -----------------------------
+    const T* vb = reinterpret_cast<const T*>(buf + p.boff_v);
+    if (warp < H) {
+      const int h = warp;
 #pragma unroll
-      for (int g = 0; g < kMaxG; ++g)
+      for (int g = 0; g < kMaxG; ++g) {
+        if (g < G) {
+          const float al = alpha_s[h * G + g];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
-      for (int t = 0; t < cnt; ++t) {
-        const int slot = s_slot[t];
-        const T* row = slot >= 0 ? res_v + (size_t)slot * E + h * D
-                                 : off_v + ((size_t)b * p.n + s_tok[t]) * E + h * D;
-        float v[8];
-        if (vvec) {
-          load_span(row + lane * per, per, true, v);
-        } else {
-          for (int j = 0; j < per; ++j) v[j] = to_f32(row[lane * per + j]);
+          for (int i = 0; i < kMaxDpl; ++i) acc[g][i] *= al;
         }
+      }
+      for (int j = 0; j < ns; ++j) {
+        const T* vr = vb + (size_t)j * (p.vrow / esz) + h * D;
+        float v[kMaxDpl];
+#pragma unroll
+        for (int i = 0; i < kMaxDpl; ++i) {
+          const int d = lane + 32 * i;
+          v[i] = (i < dpl && d < D) ? to_f32(vr[d]) : 0.f;
+        }
+        const float* pj = lg + j * HG + h * G;
 #pragma unroll
         for (int g = 0; g < kMaxG; ++g) {
           if (g < G) {
-            const float pw = lg[(size_t)(h * G + g) * TT + t];
+            const float pw = pj[g];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < per) acc[g][j] = fmaf(pw, v[j], acc[g][j]);
+            for (int i = 0; i < kMaxDpl; ++i) acc[g][i] = fmaf(pw, v[i], acc[g][i]);
           }
         }
       }
-      for (int g = 0; g < G; ++g)
-        for (int j = 0; j < per; ++j)
-          p.po[(pbase + h * G + g) * D + lane * per + j] = acc[g][j];
-    } else {
-      for (int d = lane; d < D; d += 32) {
-        float acc[kMaxG];
-        for (int g = 0; g < kMaxG; ++g) acc[g] = 0.f;
-        for (int t = 0; t < cnt; ++t) {
-          const int slot = s_slot[t];
-          const T* row = slot >= 0 ? res_v + (size_t)slot * E + h * D
-                                   : off_v + ((size_t)b * p.n + s_tok[t]) * E + h * D;
-          const float v = to_f32(row[d]);
-          for (int g = 0; g < G; ++g) acc[g] = fmaf(lg[(size_t)(h * G + g) * TT + t], v, acc[g]);
-        }
-        for (int g = 0; g < G; ++g) p.po[(pbase + h * G + g) * D + d] = acc[g];
+    }
+    __syncthreads();
+  }
+
+  // ---- partials ----------------------------------------------------------------
+  const size_t pb = ((size_t)b * nsplit + split) * HG;
+  if (warp == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int hg = lane + 32 * s2;
+      if (hg < HG) {
+        p.pm[pb + hg] = m_run[s2];
+        p.pl[pb + hg] = l_run[s2];
       }
     }
   }
-  for (int row = tid; row < HG; row += blockDim.x) {
-    p.pm[pbase + row] = s_m[row];
-    p.pl[pbase + row] = s_l[row];
+  if (warp < H) {
+    const int h = warp;
+#pragma unroll
+    for (int g = 0; g < kMaxG; ++g) {
+      if (g >= G) continue;
+#pragma unroll
+      for (int i = 0; i < kMaxDpl; ++i) {
+        const int d = lane + 32 * i;
+        if (i < dpl && d < D) p.po[(pb + h * G + g) * D + d] = acc[g][i];
+      }
+    }
   }
 }
 
@@ -276,28 +353,26 @@ __global__ void k5_fold_queries(const float* __restrict__ q, const uint16_t* __r
   }
 }
 
-// Exact LSE merge of the tile partials of each (sequence, head, query).
+// Exact LSE merge of the split partials of each (sequence, head, query).
 __global__ void k5_combine(const float* __restrict__ pm, const float* __restrict__ pl,
-                           const float* __restrict__ po, const int32_t* __restrict__ ntok,
-                           int tiles, int H, int G, int D, float* __restrict__ out,
-                           float* __restrict__ lse) {
+                           const float* __restrict__ po, int splits, int H, int G, int D,
+                           float* __restrict__ out, float* __restrict__ lse) {
   const int b = blockIdx.y, h = blockIdx.x;
   const int HG = H * G;
-  const int nt = (ntok[b] + TT - 1) / TT;
   for (int g = 0; g < G; ++g) {
     const int row = h * G + g;
     float M = -INFINITY;
-    for (int i = 0; i < nt; ++i) M = fmaxf(M, pm[((size_t)b * tiles + i) * HG + row]);
+    for (int i = 0; i < splits; ++i) M = fmaxf(M, pm[((size_t)b * splits + i) * HG + row]);
     float L = 0.f;
-    for (int i = 0; i < nt; ++i) {
-      const size_t o = ((size_t)b * tiles + i) * HG + row;
-      L += pl[o] * expf(pm[o] - M);
+    for (int i = 0; i < splits; ++i) {
+      const size_t o = ((size_t)b * splits + i) * HG + row;
+      if (pl[o] > 0.f) L += pl[o] * expf(pm[o] - M);
     }
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       float acc = 0.f;
-      for (int i = 0; i < nt; ++i) {
-        const size_t o = ((size_t)b * tiles + i) * HG + row;
-        acc = fmaf(po[o * D + d], expf(pm[o] - M), acc);
+      for (int i = 0; i < splits; ++i) {
+        const size_t o = ((size_t)b * splits + i) * HG + row;
+        if (pl[o] > 0.f) acc = fmaf(po[o * D + d], expf(pm[o] - M), acc);
       }
       out[(((size_t)b * H + h) * G + g) * D + d] = acc / L;
     }
@@ -305,32 +380,78 @@ __global__ void k5_combine(const float* __restrict__ pm, const float* __restrict
   }
 }
 
+struct AttGeom {
+  AttParams p;
+  int tt, splits;
+  size_t smem;
+};
+
+AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
+  AttGeom a{};
+  AttParams& p = a.p;
+  const int H = s->d.kv_heads, D = s->d.head_dim, E = H * D;
+  const int esz = (int)s->esz;
+  const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
+  const int r = svd ? s->d.svd_rank : 0;
+  const int HG = H * G;
+  a.tt = esz == 2 ? 16 : 8;
+  const bool k16 = ((E * esz) % 16 == 0) && ((D * esz) % 16 == 0);
+  p.kpad_head = D * esz + (k16 ? 16 : 0);
+  p.krow = H * p.kpad_head;
+  const int lbytes = svd ? s->d.svd_groups * r * 2 : 0;
+  p.lrow = (lbytes + 15) & ~15;
+  p.vrow = (E * esz + 15) & ~15;
+  p.boff_l = a.tt * p.krow;
+  p.boff_v = p.boff_l + a.tt * p.lrow;
+  p.buf_bytes = (p.boff_v + a.tt * p.vrow + 127) & ~127;
+  // splits: ~1 wave of resident CTAs across 148 SMs
+  const int B = s->d.batch;
+  const int tiles = (cap + a.tt - 1) / a.tt;
+  size_t fixed = (size_t)HG * ((D + 1) & ~1) * 4 + (size_t)HG * ((r + 1) & ~1) * 4 +
+                 (size_t)a.tt * HG * 4 + (size_t)HG * 4;
+  const int ctas_per_sm = (fixed + 2 * (size_t)p.buf_bytes) * 2 + 8192 <= 220 * 1024 ? 2 : 1;
+  int splits = (148 * ctas_per_sm + B - 1) / B;
+  if (splits > tiles) splits = tiles;
+  if (splits < 1) splits = 1;
+  a.splits = splits;
+  p.max_per = (cap + splits - 1) / splits;
+  p.off_qt = HG * ((D + 1) & ~1) * 4;
+  p.off_lg = p.off_qt + HG * ((r + 1) & ~1) * 4;
+  p.off_alpha = p.off_lg + a.tt * HG * 4;
+  p.off_tok = p.off_alpha + ((HG * 4 + 15) & ~15);
+  p.off_buf = (p.off_tok + 2 * p.max_per * 4 + 127) & ~127;
+  a.smem = (size_t)p.off_buf + 2 * (size_t)p.buf_bytes;
+  return a;
+}
+
 }  // namespace
 
 size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
+  const AttGeom g = attend_geometry(s, G, cap);
   const size_t B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim;
-  const size_t tiles = (cap + TT - 1) / TT;
-  size_t bytes = B * tiles * H * G * (2 + D) * sizeof(float);
+  size_t bytes = B * g.splits * H * G * (2 + D) * sizeof(float) + 1024;
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
-  return bytes + 256;
+  return bytes;
 }
 
 cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
   const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
-  const int tiles = (a.cap + TT - 1) / TT;
+  AttGeom geo = attend_geometry(s, G, a.cap);
+  if (geo.smem > 227 * 1024) return cudaErrorInvalidValue;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
+  const int splits = geo.splits;
   float* ws = static_cast<float*>(a.ws);
   float* pm = ws;
-  float* pl = pm + (size_t)B * tiles * H * G;
-  float* po = pl + (size_t)B * tiles * H * G;
-  float* qt = po + (size_t)B * tiles * H * G * D;
+  float* pl = pm + (size_t)B * splits * H * G;
+  float* po = pl + (size_t)B * splits * H * G;
+  float* qt = po + (size_t)B * splits * H * G * D;
   if (svd) {
     count_launch();
-    k5_fold_queries<<<dim3(H, B), 256, 0, st>>>(a.q, s->svd_right, qt, H,
-                                                 G, D, r, s->d.svd_groups);
+    k5_fold_queries<<<dim3(H, B), 256, 0, st>>>(a.q, s->svd_right, qt, H, G, D, r,
+                                                 s->d.svd_groups);
   }
-  AttParams p;
+  AttParams& p = geo.p;
   p.q = a.q;
   p.tok = a.token_ids;
   p.ntok = a.n_tokens;
@@ -356,19 +477,16 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   p.pm = pm;
   p.pl = pl;
   p.po = po;
-  p.tiles = tiles;
-  const size_t smem = sizeof(int) * 2 * TT +
-                      sizeof(float) * ((size_t)H * G * D + (svd ? (size_t)H * G * r : 0) +
-                                       (size_t)H * G * TT + 2 * (size_t)H * G);
+  const int nthr = kAttThreads;  // 8 warps: warp h owns head h in phase 3 (H <= 8)
   count_launch(2);
   if (s->d.kv_dtype == KVB_BF16) {
-    ensure_smem((const void*)k5_attend<__nv_bfloat16>, smem);
-    k5_attend<__nv_bfloat16><<<dim3(tiles, B), kAttThreads, smem, st>>>(p);
+    ensure_smem((const void*)k5_attend<__nv_bfloat16, 16>, geo.smem);
+    k5_attend<__nv_bfloat16, 16><<<dim3(splits, B), nthr, geo.smem, st>>>(p);
   } else {
-    ensure_smem((const void*)k5_attend<float>, smem);
-    k5_attend<float><<<dim3(tiles, B), kAttThreads, smem, st>>>(p);
+    ensure_smem((const void*)k5_attend<float, 8>, geo.smem);
+    k5_attend<float, 8><<<dim3(splits, B), nthr, geo.smem, st>>>(p);
   }
-  k5_combine<<<dim3(H, B), 128, 0, st>>>(pm, pl, po, a.n_tokens, tiles, H, G, D, a.out, a.lse);
+  k5_combine<<<dim3(H, B), 128, 0, st>>>(pm, pl, po, splits, H, G, D, a.out, a.lse);
   return cudaGetLastError();
 }
 

@@ -39,6 +39,7 @@ struct SelParams {
   int32_t* err_flag;
   const uint32_t* res_bitmap;
   int n, cs, W, P;
+  int stage;  // keys staged in shared memory
 };
 
 __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
@@ -54,10 +55,30 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   const int M = p.m_count ? p.m_count[b] : p.M_stride;
   const int K = p.K < M ? p.K : M;
 
+  // dynamic smem: [sel keys/ids][bitmap W][staged keys M_stride (if p.stage)]
   uint64_t* keys64 = reinterpret_cast<uint64_t*>(smem_raw);          // [P] (rank order)
   int32_t* ids = reinterpret_cast<int32_t*>(smem_raw);               // [K] (set only)
   const size_t sel_bytes = p.rank_order ? (size_t)p.P * 8 : (size_t)((p.K + 3) & ~3) * 4;
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sel_bytes);  // [W]
+  uint32_t* ukeys = bm + (p.token_ids ? ((p.W + 3) & ~3) : 0);     // [M] staged keys
+  if (p.stage) {
+    const float4* s4 = reinterpret_cast<const float4*>(sc);
+    const bool al = ((reinterpret_cast<uintptr_t>(sc) & 15) == 0);
+    if (al) {
+      for (int i = tid; i < M / 4; i += nthr) {
+        const float4 v = s4[i];
+        ukeys[4 * i] = score_key(v.x);
+        ukeys[4 * i + 1] = score_key(v.y);
+        ukeys[4 * i + 2] = score_key(v.z);
+        ukeys[4 * i + 3] = score_key(v.w);
+      }
+      for (int i = (M / 4) * 4 + tid; i < M; i += nthr) ukeys[i] = score_key(sc[i]);
+    } else {
+      for (int i = tid; i < M; i += nthr) ukeys[i] = score_key(sc[i]);
+    }
+    __syncthreads();
+  }
+  auto key_at = [&](int i) -> uint32_t { return p.stage ? ukeys[i] : score_key(__ldg(sc + i)); };
 
   // ---- 1. radix select ----------------------------------------------------
   uint32_t prefix = 0u, pmask = 0u;
@@ -66,14 +87,22 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     const int shift = 24 - 8 * pass;
     for (int i = tid; i < 256; i += nthr) hist[i] = 0;
     __syncthreads();
-    for (int base = warp * 32; base < M; base += nthr) {
-      const int i = base + lane;
-      const bool valid = i < M;
-      const uint32_t u = valid ? score_key(sc[i]) : 0u;
-      const bool pred = valid && ((u & pmask) == prefix);
-      const uint32_t dg = (u >> shift) & 255u;
-      const unsigned peers = __match_any_sync(FULL, pred ? dg : (256u + lane));
-      if (pred && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], __popc(peers));
+    for (int base = warp * 32 * 4; base < M; base += nthr * 4) {
+      uint32_t u4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = base + k * 32 + lane;
+        u4[k] = i < M ? key_at(i) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = base + k * 32 + lane;
+        const uint32_t u = u4[k];
+        const bool pred = i < M && ((u & pmask) == prefix);
+        const uint32_t dg = (u >> shift) & 255u;
+        const unsigned peers = __match_any_sync(FULL, pred ? dg : (256u + lane));
+        if (pred && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], __popc(peers));
+      }
     }
     __syncthreads();
     if (warp == 0) {
@@ -126,7 +155,7 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   for (int base = warp * 32; base < M; base += nthr) {
     const int i = base + lane;
     const bool valid = i < M;
-    const uint32_t u = valid ? score_key(sc[i]) : 0u;
+    const uint32_t u = valid ? key_at(i) : 0u;
     const bool take = valid && (u > T || (all_ties && u == T));
     const unsigned m = __ballot_sync(FULL, take);
     int wb = 0;
@@ -141,7 +170,7 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     int taken = 0;
     for (int base = 0; base < M && taken < krem; base += nthr) {
       const int i = base + tid;
-      const bool eq = (i < M) && score_key(sc[i]) == T;
+      const bool eq = (i < M) && key_at(i) == T;
       int tot;
       const int ex = block_excl_scan(eq ? 1 : 0, red, &tot);
       if (eq && taken + ex < krem) put(start + taken + ex, T, i);
@@ -250,7 +279,9 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
   p.W = s->W;
   p.P = next_pow2(a.K < 1 ? 1 : a.K);
   const size_t sel = a.rank_order ? (size_t)p.P * 8 : (size_t)((a.K + 3) & ~3) * 4;
-  const size_t smem = sel + (a.token_ids ? (size_t)s->W * 4 : 0);
+  size_t smem = sel + (a.token_ids ? (size_t)((s->W + 3) & ~3) * 4 : 0);
+  p.stage = (smem + (size_t)a.M_stride * 4 <= 200 * 1024) ? 1 : 0;
+  if (p.stage) smem += (size_t)a.M_stride * 4;
   ensure_smem((const void*)k2_select, smem);
   count_launch();
   k2_select<<<s->d.batch, kSelThreads, smem, st>>>(p);
