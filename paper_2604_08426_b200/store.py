@@ -382,6 +382,23 @@ class DecodePlan:
         self.out = torch.empty((B, store.heads, sa.queries_per_head, store.dim), dtype=torch.float32,
                                device="cuda")
         self.lse = torch.empty((B, store.heads, sa.queries_per_head), dtype=torch.float32, device="cuda")
+        self.cid = torch.empty((B, sa.n_select), dtype=torch.int32, device="cuda")
+
+    def select_only(self, q: torch.Tensor):
+        """kvb_select into the plan's token buffers (no rank order, no scores)."""
+        s = self.store
+        L.check(s.lib.kvb_select(s.h, _ptr(q), C.byref(self.sa), _ptr(self.cid), None,
+                                 _ptr(self.tok), _ptr(self.ntok), _ptr(self.ws), self.ws.numel(),
+                                 _stream()), "kvb_select")
+
+    def attend_only(self, q: torch.Tensor, out: torch.Tensor | None = None):
+        """kvb_attend over the plan's current token buffers."""
+        s = self.store
+        dst = self.out if out is None else out
+        L.check(s.lib.kvb_attend(s.h, _ptr(q), C.byref(self.aa), _ptr(self.tok), _ptr(self.ntok),
+                                 _ptr(dst), _ptr(self.lse), _ptr(self.ws), self.ws.numel(),
+                                 _stream()), "kvb_attend")
+        return dst
 
     def run(self, q: torch.Tensor, out: torch.Tensor | None = None):
         s = self.store
