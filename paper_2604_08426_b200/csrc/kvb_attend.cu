@@ -331,53 +331,93 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
 }
 
 // q~[b,h,g,r] = sum_d right[b, grp(h), r, (h%hpg)*D + d] * q[b,h,g,d]
-__global__ void k5_fold_queries(const float* __restrict__ q, const uint16_t* __restrict__ right,
-                                float* __restrict__ qt, int H, int G, int D, int r, int sgroups) {
+// One CTA per (head, sequence): the head's [r, D] slice of `right` and its
+// queries are staged in shared memory with one round of loads, then every
+// thread produces (r, g) outputs from shared memory.
+__global__ void __launch_bounds__(256) k5_fold_queries(const float* __restrict__ q,
+                                                       const uint16_t* __restrict__ right,
+                                                       float* __restrict__ qt, int H, int G, int D,
+                                                       int r, int sgroups) {
+  extern __shared__ float fsm[];
+  float* qs = fsm;                       // [G][D]
+  float* rs = fsm + G * D;               // [r][D+1]
   const int b = blockIdx.y, h = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
   const int Dg = hpg * D;
-  const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg;
+  const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
   const float* qb = q + ((size_t)b * H + h) * G * D;
-  for (int rr = warp; rr < r; rr += nw) {
-    float acc[kMaxG];
-    for (int g = 0; g < kMaxG; ++g) acc[g] = 0.f;
-    for (int d = lane; d < D; d += 32) {
-      const float w = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + col0 + d]));
-      for (int g = 0; g < G; ++g) acc[g] = fmaf(w, qb[(size_t)g * D + d], acc[g]);
-    }
-    for (int g = 0; g < G; ++g) {
-      const float v = warp_sum_butterfly(acc[g]);
-      if (lane == 0) qt[(((size_t)b * H + h) * G + g) * r + rr] = v;
-    }
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) qs[i] = qb[i];
+  for (int i = threadIdx.x; i < r * D; i += blockDim.x) {
+    const int rr = i / D, d = i - rr * D;
+    rs[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < r * G; o += blockDim.x) {
+    const int g = o / r, rr = o - g * r;
+    const float* rw = rs + rr * (D + 1);
+    const float* qq = qs + g * D;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int d = 0; d < D; ++d) acc = fmaf(rw[d], qq[d], acc);
+    qt[(((size_t)b * H + h) * G + g) * r + rr] = acc;
   }
 }
 
-// Exact LSE merge of the split partials of each (sequence, head, query).
-__global__ void k5_combine(const float* __restrict__ pm, const float* __restrict__ pl,
-                           const float* __restrict__ po, int splits, int H, int G, int D,
-                           float* __restrict__ out, float* __restrict__ lse) {
-  const int b = blockIdx.y, h = blockIdx.x;
+// Exact LSE merge of the split partials; one CTA per (sequence, head, query).
+__global__ void __launch_bounds__(128) k5_combine(const float* __restrict__ pm,
+                                                  const float* __restrict__ pl,
+                                                  const float* __restrict__ po, int splits, int H,
+                                                  int G, int D, float* __restrict__ out,
+                                                  float* __restrict__ lse) {
+  __shared__ float w_s[1024];
+  __shared__ float red[2];
+  const int row = blockIdx.x, b = blockIdx.y;  // row = h*G + g
   const int HG = H * G;
-  for (int g = 0; g < G; ++g) {
-    const int row = h * G + g;
-    float M = -INFINITY;
-    for (int i = 0; i < splits; ++i) M = fmaxf(M, pm[((size_t)b * splits + i) * HG + row]);
-    float L = 0.f;
-    for (int i = 0; i < splits; ++i) {
-      const size_t o = ((size_t)b * splits + i) * HG + row;
-      if (pl[o] > 0.f) L += pl[o] * expf(pm[o] - M);
-    }
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      float acc = 0.f;
-      for (int i = 0; i < splits; ++i) {
-        const size_t o = ((size_t)b * splits + i) * HG + row;
-        if (pl[o] > 0.f) acc = fmaf(po[o * D + d], expf(pm[o] - M), acc);
-      }
-      out[(((size_t)b * H + h) * G + g) * D + d] = acc / L;
-    }
-    if (lse && threadIdx.x == 0) lse[((size_t)b * H + h) * G + g] = M + logf(L);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float m = -INFINITY;
+  for (int i = threadIdx.x; i < splits; i += blockDim.x) {
+    const size_t o = ((size_t)b * splits + i) * HG + row;
+    const float mi = pl[o] > 0.f ? pm[o] : -INFINITY;
+    w_s[i] = mi;
+    m = fmaxf(m, mi);
   }
+  m = warp_max(m);
+  __shared__ float wm[4];
+  if (lane == 0) wm[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = wm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, wm[w]);
+    red[0] = M;
+  }
+  __syncthreads();
+  const float M = red[0];
+  float lsum = 0.f;
+  for (int i = threadIdx.x; i < splits; i += blockDim.x) {
+    const size_t o = ((size_t)b * splits + i) * HG + row;
+    const float wi = w_s[i] == -INFINITY ? 0.f : expf(w_s[i] - M);
+    w_s[i] = wi;
+    lsum += pl[o] * wi;
+  }
+  lsum = warp_sum_butterfly(lsum);
+  __shared__ float wl[4];
+  if (lane == 0) wl[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float L = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) L += wl[w];
+    red[1] = L;
+  }
+  __syncthreads();
+  const float L = red[1];
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int i = 0; i < splits; ++i)
+      acc = fmaf(po[(((size_t)b * splits + i) * HG + row) * D + d], w_s[i], acc);
+    out[((size_t)b * HG + row) * D + d] = acc / L;
+  }
+  if (lse && threadIdx.x == 0) lse[(size_t)b * HG + row] = M + logf(L);
 }
 
 struct AttGeom {
@@ -410,7 +450,7 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
   size_t fixed = (size_t)HG * ((D + 1) & ~1) * 4 + (size_t)HG * ((r + 1) & ~1) * 4 +
                  (size_t)a.tt * HG * 4 + (size_t)HG * 4;
   const int ctas_per_sm = (fixed + 2 * (size_t)p.buf_bytes) * 2 + 8192 <= 220 * 1024 ? 2 : 1;
-  int splits = (148 * ctas_per_sm + B - 1) / B;
+  int splits = (148 * ctas_per_sm) / B;  // one full wave, never a partial second
   if (splits > tiles) splits = tiles;
   if (splits < 1) splits = 1;
   a.splits = splits;
@@ -448,7 +488,9 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   float* qt = po + (size_t)B * splits * H * G * D;
   if (svd) {
     count_launch();
-    k5_fold_queries<<<dim3(H, B), 256, 0, st>>>(a.q, s->svd_right, qt, H, G, D, r,
+    const size_t fs = sizeof(float) * ((size_t)G * D + (size_t)r * (D + 1));
+    ensure_smem((const void*)k5_fold_queries, fs);
+    k5_fold_queries<<<dim3(H, B), 256, fs, st>>>(a.q, s->svd_right, qt, H, G, D, r,
                                                  s->d.svd_groups);
   }
   AttParams& p = geo.p;
@@ -486,7 +528,7 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
     ensure_smem((const void*)k5_attend<float, 8>, geo.smem);
     k5_attend<float, 8><<<dim3(splits, B), nthr, geo.smem, st>>>(p);
   }
-  k5_combine<<<dim3(H, B), 128, 0, st>>>(pm, pl, po, splits, H, G, D, a.out, a.lse);
+  k5_combine<<<dim3(H * G, B), 128, 0, st>>>(pm, pl, po, splits, H, G, D, a.out, a.lse);
   return cudaGetLastError();
 }
 
