@@ -30,7 +30,6 @@ constexpr int kAttThreads = 256;
 constexpr int kMaxDpl = 4;   // head_dim <= 128
 
 struct AttParams {
-  const float* q;        // [B][H][G][D]
   const int32_t* tok;    // [B][cap]
   const int32_t* ntok;   // [B]
   int cap, G, H, D, n, W, Rcap, r, sgroups, max_per;
@@ -41,14 +40,15 @@ struct AttParams {
   const void* off_k;     // slow NONE
   const void* off_v;
   const uint16_t* left;  // slow SVD, fp16 [B][n][sgroups][r]
-  const float* qt;       // [B][H][G][r]
+  const float* q2;       // [B][D/2][HG][2]  (prep kernel)
+  const float* qt2;      // [B][r/2][HG][2]  (prep kernel, SVD only)
   float scale;
   int slow_svd;
   float* pm;             // [B][splits][H*G]
   float* pl;
   float* po;             // [B][splits][H*G][D]
   // shared-memory geometry (bytes)
-  int krow, kpad_head, lrow, vrow;   // row strides; kpad_head = padded head stride (bytes)
+  int krow, kpad_head, lrow, vrow;
   int off_qt, off_lg, off_alpha, off_tok, off_buf, buf_bytes, boff_l, boff_v;
 };
 
@@ -83,67 +83,105 @@ __device__ __forceinline__ float2 ld_pair<__nv_bfloat16>(const __nv_bfloat16* p)
   return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
 }
 
-// Issue the cp.async copies of sub-tile rows [i0, i0+ns) of this CTA's token
-// range into one buffer: exact K rows (head-padded), fp16 left rows (SVD
-// tokens), V rows. Row sizes are multiples of 16 B on the fast path, else 4 B.
+// per-lane contiguous span of `per` elements -> floats
+template <typename T>
+__device__ __forceinline__ void ld_span(const T* p, int per, float* v);
+template <>
+__device__ __forceinline__ void ld_span<__nv_bfloat16>(const __nv_bfloat16* p, int per, float* v) {
+  if (per == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xffff0000u);
+    v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xffff0000u);
+  } else {
+    for (int i = 0; i < per; ++i) v[i] = __bfloat162float(p[i]);
+  }
+}
+template <>
+__device__ __forceinline__ void ld_span<float>(const float* p, int per, float* v) {
+  if (per == 4) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  } else {
+    for (int i = 0; i < per; ++i) v[i] = p[i];
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t* a, const void* smem_row) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_row);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(s));
+}
+
+// Stage sub-tile rows [i0, i0+ns) into one buffer with cp.async: warp per
+// token, lanes over 16-byte chunks (4-byte fallback for odd row sizes).
 template <typename T>
 __device__ __forceinline__ void stage_rows(const AttParams& p, int b, const int* tok_s,
                                            const int* slot_s, int i0, int ns,
                                            unsigned char* buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int E = p.H * p.D;
-  const int esz = sizeof(T);
-  const bool v16 = (E * esz) % 16 == 0;
+  constexpr int esz = sizeof(T);
+  const int rowb = E * esz;
+  const bool v16 = rowb % 16 == 0;
   const bool k16 = v16 && ((p.D * esz) % 16 == 0);
-  const int gran_v = v16 ? 16 : 4;
-  const int gran_k = k16 ? 16 : 4;
-  const int kc = E * esz / gran_k;                  // K chunks per row
+  const int hb = p.D * esz;                          // bytes per head segment
   const int lbytes = p.slow_svd ? p.sgroups * p.r * 2 : 0;
   const bool l16 = (lbytes % 16) == 0;
-  const int gran_l = l16 ? 16 : 4;
-  const int lc = lbytes / gran_l;
-  const int vc = E * esz / gran_v;
-  const int cpt = kc + lc + vc;
-  const int head_chunks = (p.D * esz) / gran_k;
-  unsigned char* kb = buf;
-  unsigned char* lb = buf + p.boff_l;
-  unsigned char* vb = buf + p.boff_v;
-  const unsigned char* rk = static_cast<const unsigned char*>(p.res_k) + (size_t)b * p.Rcap * E * esz;
-  const unsigned char* rv = static_cast<const unsigned char*>(p.res_v) + (size_t)b * p.Rcap * E * esz;
+  const unsigned char* rk = static_cast<const unsigned char*>(p.res_k) + (size_t)b * p.Rcap * rowb;
+  const unsigned char* rv = static_cast<const unsigned char*>(p.res_v) + (size_t)b * p.Rcap * rowb;
   const unsigned char* ok = static_cast<const unsigned char*>(p.off_k);
   const unsigned char* ov = static_cast<const unsigned char*>(p.off_v);
-  for (int idx = threadIdx.x; idx < ns * cpt; idx += blockDim.x) {
-    const int j = idx / cpt;
-    const int c = idx - j * cpt;
+  for (int j = warp; j < ns; j += nwarp) {
     const int slot = slot_s[i0 + j];
     const size_t tok = (size_t)tok_s[i0 + j];
     const bool exact = slot >= 0 || !p.slow_svd;
-    if (c < kc) {
-      if (!exact) continue;
-      const unsigned char* src = slot >= 0 ? rk + (size_t)slot * E * esz
-                                           : ok + ((size_t)b * p.n + tok) * E * esz;
-      const int h = c / head_chunks, w = c - h * head_chunks;
-      unsigned char* dst = kb + (size_t)j * p.krow + (size_t)h * p.kpad_head + (size_t)w * gran_k;
-      const unsigned char* s = src + (size_t)c * gran_k;
-      if (k16) cp16(dst, s); else cp4(dst, s);
-    } else if (c < kc + lc) {
-      if (exact) continue;
-      const int w = c - kc;
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.left) +
-                                 ((size_t)b * p.n + tok) * lbytes + (size_t)w * gran_l;
-      unsigned char* dst = lb + (size_t)j * p.lrow + (size_t)w * gran_l;
-      if (l16) cp16(dst, src); else cp4(dst, src);
+    const unsigned char* vsrc = slot >= 0 ? rv + (size_t)slot * rowb : ov + ((size_t)b * p.n + tok) * rowb;
+    unsigned char* vdst = buf + p.boff_v + (size_t)j * p.vrow;
+    if (exact) {
+      const unsigned char* ksrc = slot >= 0 ? rk + (size_t)slot * rowb : ok + ((size_t)b * p.n + tok) * rowb;
+      unsigned char* kdst = buf + (size_t)j * p.krow;
+      if (k16) {
+        const int cph = hb / 16;
+        for (int c = lane; c < rowb / 16; c += 32) {
+          const int h = c / cph;
+          cp16(kdst + h * p.kpad_head + (c - h * cph) * 16, ksrc + c * 16);
+        }
+      } else {
+        for (int c = lane; c < rowb / 4; c += 32) cp4(kdst + c * 4, ksrc + c * 4);
+      }
     } else {
-      const int w = c - kc - lc;
-      const unsigned char* src = slot >= 0 ? rv + (size_t)slot * E * esz
-                                           : ov + ((size_t)b * p.n + tok) * E * esz;
-      unsigned char* dst = vb + (size_t)j * p.vrow + (size_t)w * gran_v;
-      if (v16) cp16(dst, src + (size_t)w * gran_v); else cp4(dst, src + (size_t)w * gran_v);
+      const unsigned char* lsrc = reinterpret_cast<const unsigned char*>(p.left) + ((size_t)b * p.n + tok) * lbytes;
+      unsigned char* ldst = buf + p.boff_l + (size_t)j * p.lrow;
+      if (l16) {
+        for (int c = lane; c < lbytes / 16; c += 32) cp16(ldst + c * 16, lsrc + c * 16);
+      } else {
+        for (int c = lane; c < lbytes / 4; c += 32) cp4(ldst + c * 4, lsrc + c * 4);
+      }
+    }
+    if (v16) {
+      for (int c = lane; c < rowb / 16; c += 32) cp16(vdst + c * 16, vsrc + c * 16);
+    } else {
+      for (int c = lane; c < rowb / 4; c += 32) cp4(vdst + c * 4, vsrc + c * 4);
     }
   }
 }
 
 template <typename T, int TT>
-__global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
+__global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int b = blockIdx.y, split = blockIdx.x, nsplit = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
@@ -161,17 +199,17 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
   int* slot_s = tok_s + p.max_per;
   unsigned char* bufs = sm + p.off_buf;
 
-  const float* qb = p.q + (size_t)b * HG * D;
-  for (int i = tid; i < HG * D; i += blockDim.x) {
-    const int hg = i / D, d = i - hg * D;
-    q_s[((d >> 1) * HG + hg) * 2 + (d & 1)] = qb[i];
-  }
-  if (p.slow_svd) {
-    const float* qt = p.qt + (size_t)b * HG * p.r;
-    for (int i = tid; i < HG * p.r; i += blockDim.x) {
-      const int hg = i / p.r, rr = i - hg * p.r;
-      qt_s[((rr >> 1) * HG + hg) * 2 + (rr & 1)] = qt[i];
+  // prologue: pre-transposed q (and q~) are straight 16-byte copies
+  {
+    const int qn = HG * D;  // floats (D even)
+    const float* src = p.q2 + (size_t)b * qn;
+    for (int i = tid; i < qn / 4; i += blockDim.x) cp16(q_s + 4 * i, src + 4 * i);
+    if (p.slow_svd) {
+      const int tn = HG * p.r;
+      const float* s2 = p.qt2 + (size_t)b * tn;
+      for (int i = tid; i < tn / 4; i += blockDim.x) cp16(qt_s + 4 * i, s2 + 4 * i);
     }
+    cp_commit();
   }
   const uint32_t* bm = p.res_bm + (size_t)b * p.W;
   const int32_t* pre = p.res_prefix + (size_t)b * p.W;
@@ -180,24 +218,54 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
     tok_s[i] = t;
     slot_s[i] = resident_slot(bm, pre, t);
   }
+  cp_wait<0>();
   __syncthreads();
 
   const int nsub = (cnt + TT - 1) / TT;
-  if (nsub > 0) {
-    stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
-  }
+  if (nsub > 0) stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
   cp_commit();
 
-  // online-softmax state: warp 0 owns (m, l) per hg; phase-3 threads own o
-  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-  // phase 3: warp w owns head w (blockDim = 32 * max(8, H))
+  // SVD logits on tensor cores: warps 0..3 own n-tile (8 hg) w, B = q~ split
+  // into fp16 hi + lo held in registers for the whole CTA (k-steps of 16 r).
+  const bool mma_warp = p.slow_svd && warp < 4 && warp * 8 < HG;
+  constexpr int kMaxKs = 16;  // r <= 256
+  uint32_t bhi[kMaxKs][2], blo[kMaxKs][2];
+  const int nks = (p.r + 15) / 16;
+  if (mma_warp) {
+    const int g4 = lane >> 2, tig = lane & 3;
+    const int hg = warp * 8 + g4;
+#pragma unroll
+    for (int ks = 0; ks < kMaxKs; ++ks) {
+      if (ks < nks) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int rp = ks * 8 + tig + hh * 4;  // pair index: rows 2rp, 2rp+1
+          float2 v = make_float2(0.f, 0.f);
+          if (2 * rp < p.r && hg < HG) v = reinterpret_cast<const float2*>(qt_s)[rp * HG + hg];
+          const __half2 hi = __floats2half2_rn(v.x, v.y);
+          const float2 hf = __half22float2(hi);
+          bhi[ks][hh] = *reinterpret_cast<const uint32_t*>(&hi);
+          blo[ks][hh] = pack_half2(v.x - hf.x, v.y - hf.y);
+        }
+      }
+    }
+  }
+
+  // online-softmax state: lane 0.. of warp (hg % nwarp) owns rows hg
+  float m_run[8], l_run[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    m_run[k] = -INFINITY;
+    l_run[k] = 0.f;
+  }
   float acc[kMaxG][kMaxDpl];
 #pragma unroll
   for (int g = 0; g < kMaxG; ++g)
 #pragma unroll
     for (int i = 0; i < kMaxDpl; ++i) acc[g][i] = 0.f;
+  const bool dspan = (D % 32) == 0 && D / 32 <= kMaxDpl;
+  const int dper = dspan ? D / 32 : 0;
   const int dpl = (D + 31) / 32;
-  const int esz = sizeof(T);
 
   for (int st = 0; st < nsub; ++st) {
     const int i0 = st * TT;
@@ -213,64 +281,88 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
     }
     __syncthreads();
 
-    // ---- phase 1: logits (lane = (h, g)) --------------------------------
+    // ---- phase 1: logits -------------------------------------------------
     const unsigned char* kb = buf;
     const unsigned char* lb = buf + p.boff_l;
-    for (int j = warp; j < ns; j += nwarp) {
-      const int slot = slot_s[i0 + j];
-      const bool exact = slot >= 0 || !p.slow_svd;
-      for (int hg = lane; hg < HG; hg += 32) {
-        const int h = hg / G;
-        float a = 0.f;
-        if (exact) {
-          const T* kr = reinterpret_cast<const T*>(kb + (size_t)j * p.krow + (size_t)h * p.kpad_head);
-          const float2* q2 = reinterpret_cast<const float2*>(q_s) + hg;
-          for (int d = 0; d < D; d += 2) {
-            const float2 kv = ld_pair<T>(kr + d);
-            const float2 qv = q2[(d >> 1) * HG];
-            a = fmaf(qv.x, kv.x, a);
-            a = fmaf(qv.y, kv.y, a);
-          }
-        } else {
-          const int grp = h / (H / p.sgroups);
-          const __half2* lr = reinterpret_cast<const __half2*>(lb + (size_t)j * p.lrow) + grp * (p.r / 2);
-          const float2* t2 = reinterpret_cast<const float2*>(qt_s) + hg;
-          for (int rr = 0; rr < p.r; rr += 2) {
-            const float2 lv = __half22float2(lr[rr >> 1]);
-            const float2 qv = t2[(rr >> 1) * HG];
-            a = fmaf(lv.x, qv.x, a);
-            a = fmaf(lv.y, qv.y, a);
-          }
-        }
-        lg[j * HG + hg] = a * p.scale;
-      }
-    }
-    __syncthreads();
-
-    // ---- phase 2: online softmax update (warp 0) --------------------------
-    if (warp == 0) {
+    if (mma_warp) {
+      const int g4 = lane >> 2, tig = lane & 3;
+      // TT rows per m-tile of 16 (TT <= 16); rows >= ns hold stale data, ignored
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      const int arow = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int acol = (lane >> 4) * 8;
+      const unsigned char* abase = lb + (size_t)(arow < TT ? arow : 0) * p.lrow;
 #pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2) {
-        const int hg = lane + 32 * s2;
-        if (hg < HG) {
-          float mx = m_run[s2];
-          for (int j = 0; j < ns; ++j) mx = fmaxf(mx, lg[j * HG + hg]);
-          const float alpha = expf(m_run[s2] - mx);
-          float sum = 0.f;
-          for (int j = 0; j < ns; ++j) {
-            const float e = expf(lg[j * HG + hg] - mx);
-            lg[j * HG + hg] = e;
-            sum += e;
+      for (int ks = 0; ks < kMaxKs; ++ks) {
+        if (ks < nks) {
+          uint32_t afr[4];
+          ldmatrix_x4(afr, abase + (ks * 16 + acol) * 2);
+          mma16816(c, afr, bhi[ks][0], bhi[ks][1]);
+          mma16816(c, afr, blo[ks][0], blo[ks][1]);
+        }
+      }
+      const int hg0 = warp * 8 + tig * 2;
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int j = g4 + hr * 8;
+        if (j < ns && slot_s[i0 + j] < 0) {
+          if (hg0 < HG) lg[j * HG + hg0] = c[hr * 2] * p.scale;
+          if (hg0 + 1 < HG) lg[j * HG + hg0 + 1] = c[hr * 2 + 1] * p.scale;
+        }
+      }
+    }
+    {
+      // exact keys (residents; every token when the slow tier is "none"):
+      // lane = (h, g), 4 partial sums over d
+      const int w0 = p.slow_svd ? 4 : 0;
+      const int nw = nwarp - w0;
+      if (warp >= w0) {
+        for (int j = warp - w0; j < ns; j += nw) {
+          if (p.slow_svd && slot_s[i0 + j] < 0) continue;
+          for (int hg = lane; hg < HG; hg += 32) {
+            const int h = hg / G;
+            const T* kr = reinterpret_cast<const T*>(kb + (size_t)j * p.krow + (size_t)h * p.kpad_head);
+            const float2* q2 = reinterpret_cast<const float2*>(q_s) + hg;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int d = 0;
+            for (; d + 4 <= D; d += 4) {
+              const float2 k0 = ld_pair<T>(kr + d), k1 = ld_pair<T>(kr + d + 2);
+              const float2 x0 = q2[(d >> 1) * HG], x1 = q2[((d >> 1) + 1) * HG];
+              a0 = fmaf(x0.x, k0.x, a0);
+              a1 = fmaf(x0.y, k0.y, a1);
+              a2 = fmaf(x1.x, k1.x, a2);
+              a3 = fmaf(x1.y, k1.y, a3);
+            }
+            for (; d < D; d += 2) {
+              const float2 k0 = ld_pair<T>(kr + d);
+              const float2 x0 = q2[(d >> 1) * HG];
+              a0 = fmaf(x0.x, k0.x, a0);
+              a1 = fmaf(x0.y, k0.y, a1);
+            }
+            lg[j * HG + hg] = ((a0 + a1) + (a2 + a3)) * p.scale;
           }
-          l_run[s2] = l_run[s2] * alpha + sum;
-          m_run[s2] = mx;
-          alpha_s[hg] = alpha;
         }
       }
     }
     __syncthreads();
 
-    // ---- phase 3: o = alpha*o + sum_j p_j V_j -----------------------------
+    // ---- phase 2: online softmax (row hg owned by warp hg % nwarp) ---------
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int hg = warp + k * (kAttThreads / 32);
+      if (hg >= HG) break;
+      const float x = lane < ns ? lg[lane * HG + hg] : -INFINITY;
+      const float mx = fmaxf(m_run[k], warp_max(x));
+      const float e = lane < ns ? expf(x - mx) : 0.f;
+      const float sum = warp_sum_butterfly(e);
+      if (lane < ns) lg[lane * HG + hg] = e;
+      const float alpha = expf(m_run[k] - mx);
+      l_run[k] = l_run[k] * alpha + sum;
+      m_run[k] = mx;
+      if (lane == 0) alpha_s[hg] = alpha;
+    }
+    __syncthreads();
+
+    // ---- phase 3: o = alpha*o + sum_j p_j V_j  (warp = head) ---------------
     const T* vb = reinterpret_cast<const T*>(buf + p.boff_v);
     if (warp < H) {
       const int h = warp;
@@ -282,13 +374,22 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
           for (int i = 0; i < kMaxDpl; ++i) acc[g][i] *= al;
         }
       }
+      const int vstride = p.vrow / (int)sizeof(T);
+#pragma unroll 2
       for (int j = 0; j < ns; ++j) {
-        const T* vr = vb + (size_t)j * (p.vrow / esz) + h * D;
+        const T* vr = vb + (size_t)j * vstride + h * D;
         float v[kMaxDpl];
+        if (dspan) {
+          ld_span<T>(vr + lane * dper, dper, v);
 #pragma unroll
-        for (int i = 0; i < kMaxDpl; ++i) {
-          const int d = lane + 32 * i;
-          v[i] = (i < dpl && d < D) ? to_f32(vr[d]) : 0.f;
+          for (int i = 0; i < kMaxDpl; ++i)
+            if (i >= dper) v[i] = 0.f;
+        } else {
+#pragma unroll
+          for (int i = 0; i < kMaxDpl; ++i) {
+            const int d = lane + 32 * i;
+            v[i] = (i < dpl && d < D) ? to_f32(vr[d]) : 0.f;
+          }
         }
         const float* pj = lg + j * HG + h * G;
 #pragma unroll
@@ -306,14 +407,12 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
 
   // ---- partials ----------------------------------------------------------------
   const size_t pb = ((size_t)b * nsplit + split) * HG;
-  if (warp == 0) {
 #pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-      const int hg = lane + 32 * s2;
-      if (hg < HG) {
-        p.pm[pb + hg] = m_run[s2];
-        p.pl[pb + hg] = l_run[s2];
-      }
+  for (int k = 0; k < 8; ++k) {
+    const int hg = warp + k * (kAttThreads / 32);
+    if (hg < HG && lane == 0) {
+      p.pm[pb + hg] = m_run[k];
+      p.pl[pb + hg] = l_run[k];
     }
   }
   if (warp < H) {
@@ -323,33 +422,57 @@ __global__ void __launch_bounds__(256, 2) k5_attend(AttParams p) {
       if (g >= G) continue;
 #pragma unroll
       for (int i = 0; i < kMaxDpl; ++i) {
-        const int d = lane + 32 * i;
-        if (i < dpl && d < D) p.po[(pb + h * G + g) * D + d] = acc[g][i];
+        const int d = dspan ? lane * dper + i : lane + 32 * i;
+        const bool ok = dspan ? i < dper : (i < dpl && d < D);
+        if (ok) p.po[(pb + h * G + g) * D + d] = acc[g][i];
       }
     }
   }
 }
 
-// q~[b,h,g,r] = sum_d right[b, grp(h), r, (h%hpg)*D + d] * q[b,h,g,d]
-// One CTA per (head, sequence): the head's [r, D] slice of `right` and its
-// queries are staged in shared memory with one round of loads, then every
-// thread produces (r, g) outputs from shared memory.
-__global__ void __launch_bounds__(256) k5_fold_queries(const float* __restrict__ q,
-                                                       const uint16_t* __restrict__ right,
-                                                       float* __restrict__ qt, int H, int G, int D,
-                                                       int r, int sgroups) {
+// Per-sequence prep: q2 = q transposed to [D/2][HG][2]; for SVD stores also
+// q~[h,g,r] = sum_d right[grp(h), r, (h%hpg)*D + d] * q[h,g,d] -> qt2
+// [r/2][HG][2]. One CTA per (head, sequence); the head's [r, D] slice of
+// `right` is staged in shared memory with 16-byte loads.
+__global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
+                                               const uint16_t* __restrict__ right,
+                                               float* __restrict__ q2, float* __restrict__ qt2,
+                                               int H, int G, int D, int r, int sgroups) {
   extern __shared__ float fsm[];
-  float* qs = fsm;                       // [G][D]
-  float* rs = fsm + G * D;               // [r][D+1]
   const int b = blockIdx.y, h = blockIdx.x;
+  const int HG = H * G;
+  float* qs = fsm;                 // [G][D]
+  const float* qb = q + ((size_t)b * H + h) * G * D;
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const float v = qb[i];
+    qs[i] = v;
+    const int g = i / D, d = i - g * D;
+    q2[(size_t)b * HG * D + ((size_t)(d >> 1) * HG + h * G + g) * 2 + (d & 1)] = v;
+  }
+  if (!right) return;
+  float* rs = fsm + G * D;          // [r][D+1]
   const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
   const int Dg = hpg * D;
   const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
-  const float* qb = q + ((size_t)b * H + h) * G * D;
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x) qs[i] = qb[i];
-  for (int i = threadIdx.x; i < r * D; i += blockDim.x) {
-    const int rr = i / D, d = i - rr * D;
-    rs[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+  if ((D % 8) == 0 && (Dg % 8) == 0 && (col0 % 8) == 0) {
+    const int cpr = D / 8;  // 16-byte chunks per row
+    for (int i = threadIdx.x; i < r * cpr; i += blockDim.x) {
+      const int rr = i / cpr, c = i - rr * cpr;
+      const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
+      const __half2* hv = reinterpret_cast<const __half2*>(&u);
+      float* dst = rs + rr * (D + 1) + c * 8;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(hv[k]);
+        dst[2 * k] = f.x;
+        dst[2 * k + 1] = f.y;
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < r * D; i += blockDim.x) {
+      const int rr = i / D, d = i - rr * D;
+      rs[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+    }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < r * G; o += blockDim.x) {
@@ -359,7 +482,7 @@ __global__ void __launch_bounds__(256) k5_fold_queries(const float* __restrict__
     float acc = 0.f;
 #pragma unroll 8
     for (int d = 0; d < D; ++d) acc = fmaf(rw[d], qq[d], acc);
-    qt[(((size_t)b * H + h) * G + g) * r + rr] = acc;
+    qt2[(size_t)b * HG * r + ((size_t)(rr >> 1) * HG + h * G + g) * 2 + (rr & 1)] = acc;
   }
 }
 
@@ -371,6 +494,7 @@ __global__ void __launch_bounds__(128) k5_combine(const float* __restrict__ pm,
                                                   float* __restrict__ lse) {
   __shared__ float w_s[1024];
   __shared__ float red[2];
+  __shared__ float wm[4], wl[4];
   const int row = blockIdx.x, b = blockIdx.y;  // row = h*G + g
   const int HG = H * G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -382,7 +506,6 @@ __global__ void __launch_bounds__(128) k5_combine(const float* __restrict__ pm,
     m = fmaxf(m, mi);
   }
   m = warp_max(m);
-  __shared__ float wm[4];
   if (lane == 0) wm[warp] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -400,7 +523,6 @@ __global__ void __launch_bounds__(128) k5_combine(const float* __restrict__ pm,
     lsum += pl[o] * wi;
   }
   lsum = warp_sum_butterfly(lsum);
-  __shared__ float wl[4];
   if (lane == 0) wl[warp] = lsum;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -439,24 +561,22 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
   p.kpad_head = D * esz + (k16 ? 16 : 0);
   p.krow = H * p.kpad_head;
   const int lbytes = svd ? s->d.svd_groups * r * 2 : 0;
-  p.lrow = (lbytes + 15) & ~15;
+  int lrow = (lbytes + 15) & ~15;
+  if (lrow && ((lrow / 16) % 2 == 0)) lrow += 16;  // odd multiple of 16 B: ldmatrix conflict-free
+  p.lrow = lrow;
   p.vrow = (E * esz + 15) & ~15;
   p.boff_l = a.tt * p.krow;
-  p.boff_v = p.boff_l + a.tt * p.lrow;
+  p.boff_v = p.boff_l + (svd ? 16 : a.tt) * p.lrow;  // ldmatrix reads 16 rows
   p.buf_bytes = (p.boff_v + a.tt * p.vrow + 127) & ~127;
-  // splits: ~1 wave of resident CTAs across 148 SMs
   const int B = s->d.batch;
   const int tiles = (cap + a.tt - 1) / a.tt;
-  size_t fixed = (size_t)HG * ((D + 1) & ~1) * 4 + (size_t)HG * ((r + 1) & ~1) * 4 +
-                 (size_t)a.tt * HG * 4 + (size_t)HG * 4;
-  const int ctas_per_sm = (fixed + 2 * (size_t)p.buf_bytes) * 2 + 8192 <= 220 * 1024 ? 2 : 1;
-  int splits = (148 * ctas_per_sm) / B;  // one full wave, never a partial second
+  int splits = 148 / B;
   if (splits > tiles) splits = tiles;
   if (splits < 1) splits = 1;
   a.splits = splits;
   p.max_per = (cap + splits - 1) / splits;
-  p.off_qt = HG * ((D + 1) & ~1) * 4;
-  p.off_lg = p.off_qt + HG * ((r + 1) & ~1) * 4;
+  p.off_qt = HG * D * 4;
+  p.off_lg = p.off_qt + HG * r * 4;
   p.off_alpha = p.off_lg + a.tt * HG * 4;
   p.off_tok = p.off_alpha + ((HG * 4 + 15) & ~15);
   p.off_buf = (p.off_tok + 2 * p.max_per * 4 + 127) & ~127;
@@ -469,7 +589,8 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
 size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
   const AttGeom g = attend_geometry(s, G, cap);
   const size_t B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim;
-  size_t bytes = B * g.splits * H * G * (2 + D) * sizeof(float) + 1024;
+  size_t bytes = B * g.splits * H * G * (2 + D) * sizeof(float) + 4096;
+  bytes += B * H * G * D * sizeof(float);                       // q2
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
   return bytes;
 }
@@ -485,16 +606,17 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   float* pm = ws;
   float* pl = pm + (size_t)B * splits * H * G;
   float* po = pl + (size_t)B * splits * H * G;
-  float* qt = po + (size_t)B * splits * H * G * D;
-  if (svd) {
+  float* q2 = po + (size_t)B * splits * H * G * D;
+  q2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q2) + 15) & ~uintptr_t(15));
+  float* qt2 = q2 + (size_t)B * H * G * D;
+  {
+    const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
+    ensure_smem((const void*)k5_prep, fs);
     count_launch();
-    const size_t fs = sizeof(float) * ((size_t)G * D + (size_t)r * (D + 1));
-    ensure_smem((const void*)k5_fold_queries, fs);
-    k5_fold_queries<<<dim3(H, B), 256, fs, st>>>(a.q, s->svd_right, qt, H, G, D, r,
-                                                 s->d.svd_groups);
+    k5_prep<<<dim3(H, B), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, q2, qt2, H, G, D, r,
+                                         svd ? s->d.svd_groups : 1);
   }
   AttParams& p = geo.p;
-  p.q = a.q;
   p.tok = a.token_ids;
   p.ntok = a.n_tokens;
   p.cap = a.cap;
@@ -513,20 +635,20 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   p.off_k = s->off_k_dev;
   p.off_v = s->off_v_dev;
   p.left = s->svd_left;
-  p.qt = qt;
+  p.q2 = q2;
+  p.qt2 = qt2;
   p.scale = (float)(1.0 / sqrt((double)D));
   p.slow_svd = svd ? 1 : 0;
   p.pm = pm;
   p.pl = pl;
   p.po = po;
-  const int nthr = kAttThreads;  // 8 warps: warp h owns head h in phase 3 (H <= 8)
   count_launch(2);
   if (s->d.kv_dtype == KVB_BF16) {
     ensure_smem((const void*)k5_attend<__nv_bfloat16, 16>, geo.smem);
-    k5_attend<__nv_bfloat16, 16><<<dim3(splits, B), nthr, geo.smem, st>>>(p);
+    k5_attend<__nv_bfloat16, 16><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
   } else {
     ensure_smem((const void*)k5_attend<float, 8>, geo.smem);
-    k5_attend<float, 8><<<dim3(splits, B), nthr, geo.smem, st>>>(p);
+    k5_attend<float, 8><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
   }
   k5_combine<<<dim3(H * G, B), 128, 0, st>>>(pm, pl, po, splits, H, G, D, a.out, a.lse);
   return cudaGetLastError();

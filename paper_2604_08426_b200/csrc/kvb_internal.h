@@ -53,6 +53,9 @@ kvb_status cuda_status(cudaError_t e, const char* what);
 void count_launch(int n = 1);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
 cudaError_t ensure_smem(const void* func, size_t bytes);
+// Number of SMs of the current device and resident CTAs/SM for a kernel.
+int sm_count();
+int resident_ctas(const void* func, int threads, size_t smem);
 
 // ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,

@@ -45,7 +45,7 @@ __device__ __forceinline__ void load_qbar(const float* __restrict__ qb, int Hkv,
 // vector elements are FMA'd in order; then warp_sum_butterfly.
 // ---------------------------------------------------------------------------
 template <typename T, int VW, int NV>
-__global__ void __launch_bounds__(kScoreThreads)
+__global__ void __launch_bounds__(kScoreThreads, 4)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
              int C, int Hkv, int G, int D) {
   extern __shared__ float qbar[];
@@ -349,11 +349,14 @@ __global__ void k1_higgs(const uint8_t* __restrict__ codes, const float* __restr
   }
 }
 
-int score_grid_x(int C, int B) {
+// One full wave of resident CTAs split across the batch (no partial wave).
+int score_grid_x(int C, int B, const void* func, size_t smem) {
   const int rows_per_cta = (kScoreThreads / 32) * 2;
-  int want = (148 * 4 + B - 1) / B;
+  const int slots = sm_count() * resident_ctas(func, kScoreThreads, smem);
+  int want = slots / B;
+  if (want < 1) want = 1;
   int maxc = (C + rows_per_cta - 1) / rows_per_cta;
-  return want < maxc ? (want < 1 ? 1 : want) : maxc;
+  return want < maxc ? want : maxc;
 }
 
 template <typename T>
@@ -364,19 +367,22 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   const bool vec = (E % VWv) == 0;
   const int VW = vec ? VWv : 1;
   const int nvl = (E / VW + 31) / 32;
-  dim3 grid(score_grid_x(C, B), B);
   const size_t smem = (size_t)E * sizeof(float);
-  count_launch();
+  const void* fn;
   if (vec) {
-    if (nvl <= 1) k1_dense_sum<T, VWv, 1><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
-    else if (nvl <= 2) k1_dense_sum<T, VWv, 2><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
-    else if (nvl <= 4) k1_dense_sum<T, VWv, 4><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
-    else if (nvl <= 8) k1_dense_sum<T, VWv, 8><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
-    else k1_dense_sum_wide<T, VWv><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
+    if (nvl <= 1) fn = (const void*)k1_dense_sum<T, VWv, 1>;
+    else if (nvl <= 2) fn = (const void*)k1_dense_sum<T, VWv, 2>;
+    else if (nvl <= 4) fn = (const void*)k1_dense_sum<T, VWv, 4>;
+    else if (nvl <= 8) fn = (const void*)k1_dense_sum<T, VWv, 8>;
+    else fn = (const void*)k1_dense_sum_wide<T, VWv>;
   } else {
-    if (nvl <= 8) k1_dense_sum<T, 1, 8><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
-    else k1_dense_sum_wide<T, 1><<<grid, kScoreThreads, smem, st>>>(lm, q, scores, C, H, G, D);
+    fn = nvl <= 8 ? (const void*)k1_dense_sum<T, 1, 8> : (const void*)k1_dense_sum_wide<T, 1>;
   }
+  ensure_smem(fn, smem);
+  dim3 grid(score_grid_x(C, B, fn, smem), B);
+  count_launch();
+  void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D};
+  return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
 }
 
@@ -390,8 +396,11 @@ cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int ag
       return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, st);
     return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, st);
   }
-  dim3 grid(score_grid_x(C, B), B);
   const size_t smem = (size_t)H * G * D * sizeof(float);
+  const void* fmax_fn = s->d.kv_dtype == KVB_BF16 ? (const void*)k1_dense_max<__nv_bfloat16>
+                                                  : (const void*)k1_dense_max<float>;
+  ensure_smem(fmax_fn, smem);
+  dim3 grid(score_grid_x(C, B, fmax_fn, smem), B);
   count_launch();
   if (s->d.kv_dtype == KVB_BF16)
     k1_dense_max<__nv_bfloat16><<<grid, kScoreThreads, smem, st>>>(

@@ -4,7 +4,8 @@
 // One 1024-thread CTA per sequence:
 //  1. radix select, MSB first, 8-bit digits over the order-preserving 32-bit
 //     key of each score (-0 canonicalised to +0). Histograms are built with
-//     warp-aggregated shared atomics (__match_any_sync). After four passes the
+//     per-warp private shared-memory histograms (plain atomics, summed across
+//     warps; no __match_any_sync, which serialises on sm_100). After four passes the
 //     K-th key T and the number of ties to take are known exactly;
 //  2. collect keys > T, plus the lowest-id ties (ordered block scans), which
 //     reproduces np.argsort(-s, kind="stable")[:K] as a set;
@@ -45,6 +46,7 @@ struct SelParams {
 __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int hist[256];
+  __shared__ int whist[kSelThreads / 32][256];  // per-warp private histograms
   __shared__ int red[33];
   __shared__ int s_digit, s_krem, s_eq, s_cnt;
 
@@ -85,8 +87,8 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   int krem = K, eqcnt = 0;
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
-    for (int i = tid; i < 256; i += nthr) hist[i] = 0;
-    __syncthreads();
+    for (int i = lane; i < 256; i += 32) whist[warp][i] = 0;
+    __syncwarp();
     for (int base = warp * 32 * 4; base < M; base += nthr * 4) {
       uint32_t u4[4];
 #pragma unroll
@@ -97,12 +99,15 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int i = base + k * 32 + lane;
-        const uint32_t u = u4[k];
-        const bool pred = i < M && ((u & pmask) == prefix);
-        const uint32_t dg = (u >> shift) & 255u;
-        const unsigned peers = __match_any_sync(FULL, pred ? dg : (256u + lane));
-        if (pred && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], __popc(peers));
+        if (i < M && (u4[k] & pmask) == prefix) atomicAdd(&whist[warp][(u4[k] >> shift) & 255u], 1);
       }
+    }
+    __syncthreads();
+    for (int bin = tid; bin < 256; bin += nthr) {
+      int c = 0;
+#pragma unroll 8
+      for (int w = 0; w < kSelThreads / 32; ++w) c += whist[w][bin];
+      hist[bin] = c;
     }
     __syncthreads();
     if (warp == 0) {
