@@ -657,8 +657,9 @@ kvb_status kvb_attend(kvb_store* s, const float* q, const kvb_attend_args* a,
   if (a->token_capacity < 1) KVB_FAIL(KVB_EINVAL, "token_capacity must be >= 1");
   if (s->d.kv_heads > 8 || s->d.head_dim > 128 || (s->d.head_dim & 1))
     KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel supports kv_heads <= 8, even head_dim <= 128");
-  if (s->d.slow_kind == KVB_SLOW_SVD && (s->d.svd_rank & 1))
-    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel needs an even SVD rank");
+  if (s->d.slow_kind == KVB_SLOW_SVD &&
+      ((s->d.svd_rank & 1) || s->d.svd_rank * s->d.svd_groups > 256))
+    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel needs an even SVD rank, groups*rank <= 256");
   if (s->d.slow_kind == KVB_SLOW_SVD && a->k_path == 2)
     KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
   if (!ws || ws_bytes < kvb_attend_workspace_bytes(s, a)) KVB_FAIL(KVB_EINVAL, "workspace too small");

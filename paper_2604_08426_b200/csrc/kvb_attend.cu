@@ -225,23 +225,30 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
   if (nsub > 0) stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
   cp_commit();
 
-  // SVD logits on tensor cores: warps 0..3 own n-tile (8 hg) w, B = q~ split
-  // into fp16 hi + lo held in registers for the whole CTA (k-steps of 16 r).
+  // SVD logits on tensor cores: warps 0..3 own n-tile (8 hg) w. A = the
+  // token's fp16 factor row over all SVD groups [sgroups*r] (exact), B = q~
+  // placed block-diagonally by group (zero where grp(h) differs), split into
+  // fp16 hi + lo and held in registers for the whole CTA (k-steps of 16).
   const bool mma_warp = p.slow_svd && warp < 4 && warp * 8 < HG;
-  constexpr int kMaxKs = 16;  // r <= 256
+  constexpr int kMaxKs = 16;  // sgroups * r <= 256
   uint32_t bhi[kMaxKs][2], blo[kMaxKs][2];
-  const int nks = (p.r + 15) / 16;
+  const int kdim = p.sgroups * p.r;
+  const int nks = (kdim + 15) / 16;
   if (mma_warp) {
     const int g4 = lane >> 2, tig = lane & 3;
     const int hg = warp * 8 + g4;
+    const int hgrp = hg < HG ? (hg / G) / (H / p.sgroups) : -1;
 #pragma unroll
     for (int ks = 0; ks < kMaxKs; ++ks) {
       if (ks < nks) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          const int rp = ks * 8 + tig + hh * 4;  // pair index: rows 2rp, 2rp+1
+          const int kk = 2 * (ks * 8 + tig + hh * 4);  // even k index of the pair
           float2 v = make_float2(0.f, 0.f);
-          if (2 * rp < p.r && hg < HG) v = reinterpret_cast<const float2*>(qt_s)[rp * HG + hg];
+          if (kk < kdim && kk / p.r == hgrp) {
+            const int rr = kk - hgrp * p.r;
+            v = reinterpret_cast<const float2*>(qt_s)[(rr >> 1) * HG + hg];
+          }
           const __half2 hi = __floats2half2_rn(v.x, v.y);
           const float2 hf = __half22float2(hi);
           bhi[ks][hh] = *reinterpret_cast<const uint32_t*>(&hi);

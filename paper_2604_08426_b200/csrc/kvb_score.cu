@@ -45,7 +45,7 @@ __device__ __forceinline__ void load_qbar(const float* __restrict__ qb, int Hkv,
 // vector elements are FMA'd in order; then warp_sum_butterfly.
 // ---------------------------------------------------------------------------
 template <typename T, int VW, int NV>
-__global__ void __launch_bounds__(kScoreThreads, 4)
+__global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
              int C, int Hkv, int G, int D) {
   extern __shared__ float qbar[];
