@@ -240,6 +240,28 @@ kvb_status kvb_decode_step(kvb_store* store, const float* queries,
 int64_t kvb_decode_workspace_bytes(const kvb_store* store, const kvb_select_args* sel,
                                    const kvb_attend_args* att);
 
+/* ---- sequence sharding ----------------------------------------
+ * A shard store holds the chunk-aligned token range starting at global chunk
+ * `chunk_offset`. Step: kvb_select_candidates on every shard -> allgather ->
+ * kvb_merge_topk -> kvb_tokens_from_chunks -> kvb_attend (with lse) ->
+ * allgather -> kvb_merge_attention. Reproduces the single-store selection
+ * exactly and the attention up to fp32 reassociation.                       */
+
+/* Local landmark scores + top-k candidates: cand_scores float32 [batch][k],
+ * cand_ids int32 [batch][k] = local chunk id + chunk_offset (unordered; -1 and
+ * -inf pad when the shard has fewer than k chunks).                         */
+kvb_status kvb_select_candidates(kvb_store* store, const float* queries,
+                                 int32_t queries_per_head, int32_t k, int32_t aggregation,
+                                 int32_t chunk_offset, float* cand_scores, int32_t* cand_ids,
+                                 void* workspace, int64_t workspace_bytes, void* stream);
+int64_t kvb_select_candidates_workspace_bytes(const kvb_store* store, int32_t k);
+/* Sorted token union of the global chunk selection restricted to this shard
+ * (chunk ids outside [chunk_offset, chunk_offset + n_chunks) are ignored) with
+ * the shard's resident tokens; token ids are local (global - offset*cs).    */
+kvb_status kvb_tokens_from_chunks(kvb_store* store, const int32_t* chunk_ids, int32_t k,
+                                  int32_t chunk_offset, int32_t* token_ids, int32_t* n_tokens,
+                                  int32_t token_capacity, void* stream);
+
 /* Merge per-shard attention partials (sequence sharding):
  * out_p/lse_p: float32 [P][batch*kv_heads*G][D] and [P][batch*kv_heads*G];
  * writes out [rows][D] and lse [rows] (may be NULL). Exact LSE merge.      */

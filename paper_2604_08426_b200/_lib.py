@@ -88,6 +88,9 @@ SIGNATURES = [
     ("kvb_decode_step", _I32, [_P, _P, C.POINTER(SelectArgs), C.POINTER(AttendArgs), _P, _P, _P,
                                _P, _P, _P, _I64, _P]),
     ("kvb_decode_workspace_bytes", _I64, [_P, C.POINTER(SelectArgs), C.POINTER(AttendArgs)]),
+    ("kvb_select_candidates", _I32, [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _P]),
+    ("kvb_select_candidates_workspace_bytes", _I64, [_P, _I32]),
+    ("kvb_tokens_from_chunks", _I32, [_P, _P, _I32, _I32, _P, _P, _I32, _P]),
     ("kvb_merge_attention", _I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P]),
     ("kvb_merge_topk", _I32, [_P, _P, _I32, _I32, _I32, _P, _P]),
 ]

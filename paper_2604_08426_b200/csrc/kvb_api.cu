@@ -707,6 +707,50 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   return kvb_attend(s, q, att, token_ids, n_tokens, out, lse, aws, ab, stream);
 }
 
+int64_t kvb_select_candidates_workspace_bytes(const kvb_store* s, int32_t k) {
+  if (!s) return -1;
+  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned((size_t)s->d.batch * 4) + 256);
+}
+
+kvb_status kvb_select_candidates(kvb_store* s, const float* q, int32_t G, int32_t k, int32_t agg,
+                                 int32_t chunk_offset, float* cand_scores, int32_t* cand_ids,
+                                 void* ws, int64_t ws_bytes, void* stream) {
+  if (!s || !q || !cand_scores || !cand_ids) KVB_FAIL(KVB_EINVAL, "null argument");
+  kvb_status ks = check_queries(s, G);
+  if (ks != KVB_OK) return ks;
+  if (k < 1) KVB_FAIL(KVB_EINVAL, "k must be >= 1");
+  if (agg != KVB_AGG_SUM && agg != KVB_AGG_MAX) KVB_FAIL(KVB_EINVAL, "unknown aggregation");
+  if (!ws || ws_bytes < kvb_select_candidates_workspace_bytes(s, k))
+    KVB_FAIL(KVB_EINVAL, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  Carve cv(ws, ws_bytes);
+  float* sc = cv.take<float>((size_t)s->d.batch * s->C);
+  if ((ks = score_landmarks(s, q, G, agg, sc, st)) != KVB_OK) return ks;
+  SelectLaunch L{};
+  L.scores = sc;
+  L.M_stride = s->C;
+  L.K = k;            // clamped to C inside; rows padded with -1 / -inf
+  L.rank_order = 0;
+  L.mode = 0;
+  L.sel_ids = cand_ids;
+  L.sel_scores = cand_scores;
+  L.id_offset = chunk_offset;
+  KVB_CUDA(launch_select(s, L, st), "local top-k");
+  return KVB_OK;
+}
+
+kvb_status kvb_tokens_from_chunks(kvb_store* s, const int32_t* chunk_ids, int32_t k,
+                                  int32_t chunk_offset, int32_t* token_ids, int32_t* n_tokens,
+                                  int32_t cap, void* stream) {
+  if (!s || !chunk_ids || !token_ids || !n_tokens) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (k < 1 || cap < 1) KVB_FAIL(KVB_EINVAL, "k and token_capacity must be >= 1");
+  if ((size_t)s->W * 4 > 220 * 1024) KVB_FAIL(KVB_EUNSUPPORTED, "shard too long for the union kernel");
+  KVB_CUDA(launch_tokens_from_chunks(s, chunk_ids, k, chunk_offset, token_ids, n_tokens, cap,
+                                     as_stream(stream)),
+           "token union");
+  return KVB_OK;
+}
+
 kvb_status kvb_merge_attention(const float* out_parts, const float* lse_parts, int32_t parts,
                                int32_t rows, int32_t D, float* out, float* lse, void* stream) {
   if (!out_parts || !lse_parts || !out || parts < 1 || rows < 1 || D < 1)

@@ -19,6 +19,8 @@
 // q~[h,g] = right_h . q[h,g] precomputed once per (sequence, head) by
 // k5_fold_queries -- mathematically q.(left.right_h), 32x fewer MACs.
 
+#include <type_traits>
+
 #include "kvb_common.cuh"
 #include "kvb_internal.h"
 
@@ -117,6 +119,37 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
       "{%8,%9}, {%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void mma16816_bf16(float* c, uint32_t a0, uint32_t a2, uint32_t b0,
+                                              uint32_t b1) {
+  // rows 8..15 of A are zero (M = queries of one head, G <= 8)
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t* r, const void* smem_row) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_row);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(s));
+}
+
+// Exact 3-way bf16 split of an fp32 pair: x = hi + mid + lo.
+__device__ __forceinline__ void split3_bf16(float x, float y, uint32_t& hi, uint32_t& mid,
+                                            uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  const float rx = x - hf.x, ry = y - hf.y;
+  const __nv_bfloat162 m = __floats2bfloat162_rn(rx, ry);
+  const float2 mf = __bfloat1622float2(m);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(rx - mf.x, ry - mf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  mid = *reinterpret_cast<const uint32_t*>(&m);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 __device__ __forceinline__ void ldmatrix_x4(uint32_t* a, const void* smem_row) {
@@ -265,11 +298,18 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
     m_run[k] = -INFINITY;
     l_run[k] = 0.f;
   }
-  float acc[kMaxG][kMaxDpl];
+  constexpr bool kTcPV = std::is_same<T, __nv_bfloat16>::value;  // p.V on tensor cores
+  constexpr int kNT = kTcPV ? 16 : 1;    // n-tiles of 8 d (D <= 128)
+  float cpv[kNT][4];                      // o[g = lane/4][d = nt*8 + 2*(lane%4) + {0,1}]
 #pragma unroll
-  for (int g = 0; g < kMaxG; ++g)
+  for (int nt = 0; nt < kNT; ++nt)
 #pragma unroll
-    for (int i = 0; i < kMaxDpl; ++i) acc[g][i] = 0.f;
+    for (int i = 0; i < 4; ++i) cpv[nt][i] = 0.f;
+  float acc[kTcPV ? 1 : kMaxG][kTcPV ? 1 : kMaxDpl];
+#pragma unroll
+  for (int g = 0; g < (kTcPV ? 1 : kMaxG); ++g)
+#pragma unroll
+    for (int i = 0; i < (kTcPV ? 1 : kMaxDpl); ++i) acc[g][i] = 0.f;
   const bool dspan = (D % 32) == 0 && D / 32 <= kMaxDpl;
   const int dper = dspan ? D / 32 : 0;
   const int dpl = (D + 31) / 32;
@@ -371,7 +411,50 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
 
     // ---- phase 3: o = alpha*o + sum_j p_j V_j  (warp = head) ---------------
     const T* vb = reinterpret_cast<const T*>(buf + p.boff_v);
-    if (warp < H) {
+    if constexpr (kTcPV) {
+      // mma m16n8k16 (bf16): A = P^T (rows = query g of head h, K = 16 tokens),
+      // split exactly into 3 bf16 parts; B = V tile via ldmatrix.trans.
+      if (warp < H) {
+        const int h = warp, g4 = lane >> 2, tig = lane & 3;
+        const float al = g4 < G ? alpha_s[h * G + g4] : 0.f;
+#pragma unroll
+        for (int nt = 0; nt < kNT; ++nt) {
+          cpv[nt][0] *= al;
+          cpv[nt][1] *= al;
+        }
+        // A fragment: row g4, token columns 2tig,2tig+1 (a0) and 2tig+8,+9 (a2)
+        float pa[4] = {0.f, 0.f, 0.f, 0.f};
+        if (g4 < G) {
+          const int j0 = 2 * tig, j1 = 2 * tig + 8;
+          pa[0] = j0 < ns ? lg[j0 * HG + h * G + g4] : 0.f;
+          pa[1] = j0 + 1 < ns ? lg[(j0 + 1) * HG + h * G + g4] : 0.f;
+          pa[2] = j1 < ns ? lg[j1 * HG + h * G + g4] : 0.f;
+          pa[3] = j1 + 1 < ns ? lg[(j1 + 1) * HG + h * G + g4] : 0.f;
+        }
+        uint32_t a0h, a0m, a0l, a2h, a2m, a2l;
+        split3_bf16(pa[0], pa[1], a0h, a0m, a0l);
+        split3_bf16(pa[2], pa[3], a2h, a2m, a2l);
+        // ldmatrix.trans: matrix m = (token half m%2, d half m/2) of a pair of n-tiles
+        const int vrow_j = (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int vcol = (lane >> 4) * 8;
+        const unsigned char* vbase = buf + p.boff_v + (size_t)(vrow_j < ns ? vrow_j : 0) * p.vrow +
+                                     (size_t)(h * D + vcol) * 2;
+#pragma unroll
+        for (int np = 0; np < kNT / 2; ++np) {
+          if (np * 16 < D) {
+            uint32_t bfr[4];
+            ldmatrix_x4_trans(bfr, vbase + np * 32);
+            // n-tile 2np: {bfr[0], bfr[1]}, n-tile 2np+1: {bfr[2], bfr[3]}
+            mma16816_bf16(cpv[2 * np], a0h, a2h, bfr[0], bfr[1]);
+            mma16816_bf16(cpv[2 * np], a0m, a2m, bfr[0], bfr[1]);
+            mma16816_bf16(cpv[2 * np], a0l, a2l, bfr[0], bfr[1]);
+            mma16816_bf16(cpv[2 * np + 1], a0h, a2h, bfr[2], bfr[3]);
+            mma16816_bf16(cpv[2 * np + 1], a0m, a2m, bfr[2], bfr[3]);
+            mma16816_bf16(cpv[2 * np + 1], a0l, a2l, bfr[2], bfr[3]);
+          }
+        }
+      }
+    } else if (warp < H) {
       const int h = warp;
 #pragma unroll
       for (int g = 0; g < kMaxG; ++g) {
@@ -422,7 +505,22 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
       p.pl[pb + hg] = l_run[k];
     }
   }
-  if (warp < H) {
+  if constexpr (kTcPV) {
+    if (warp < H) {
+      const int h = warp, g4 = lane >> 2, tig = lane & 3;
+      if (g4 < G) {
+#pragma unroll
+        for (int nt = 0; nt < kNT; ++nt) {
+          const int d = nt * 8 + 2 * tig;
+          if (d < D) {
+            float* dst = p.po + (pb + h * G + g4) * D + d;
+            dst[0] = cpv[nt][0];
+            dst[1] = cpv[nt][1];
+          }
+        }
+      }
+    }
+  } else if (warp < H) {
     const int h = warp;
 #pragma unroll
     for (int g = 0; g < kMaxG; ++g) {
@@ -572,6 +670,7 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
   if (lrow && ((lrow / 16) % 2 == 0)) lrow += 16;  // odd multiple of 16 B: ldmatrix conflict-free
   p.lrow = lrow;
   p.vrow = (E * esz + 15) & ~15;
+  if ((p.vrow / 16) % 2 == 0) p.vrow += 16;  // odd multiple of 16 B: conflict-free ldmatrix
   p.boff_l = a.tt * p.krow;
   p.boff_v = p.boff_l + (svd ? 16 : a.tt) * p.lrow;  // ldmatrix reads 16 rows
   p.buf_bytes = (p.boff_v + a.tt * p.vrow + 127) & ~127;
@@ -666,14 +765,20 @@ __global__ void k_merge_attention(const float* __restrict__ op, const float* __r
                                   int parts, int rows, int D, float* __restrict__ out,
                                   float* __restrict__ lse) {
   const int row = blockIdx.x;
+  // parts with no tokens carry lse = -inf (and a NaN output): weight 0, skipped
   float M = -INFINITY;
   for (int i = 0; i < parts; ++i) M = fmaxf(M, lp[(size_t)i * rows + row]);
   float L = 0.f;
-  for (int i = 0; i < parts; ++i) L += expf(lp[(size_t)i * rows + row] - M);
+  for (int i = 0; i < parts; ++i) {
+    const float li = lp[(size_t)i * rows + row];
+    if (li != -INFINITY) L += expf(li - M);
+  }
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float acc = 0.f;
-    for (int i = 0; i < parts; ++i)
-      acc = fmaf(op[((size_t)i * rows + row) * D + d], expf(lp[(size_t)i * rows + row] - M), acc);
+    for (int i = 0; i < parts; ++i) {
+      const float li = lp[(size_t)i * rows + row];
+      if (li != -INFINITY) acc = fmaf(op[((size_t)i * rows + row) * D + d], expf(li - M), acc);
+    }
     out[(size_t)row * D + d] = acc / L;
   }
   if (lse && threadIdx.x == 0) lse[row] = M + logf(L);

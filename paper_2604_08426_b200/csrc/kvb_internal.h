@@ -78,7 +78,13 @@ struct SelectLaunch {
   int cap;
   int with_residents;
   int32_t* err_flag;        // device int, set on capacity overflow
+  float* sel_scores = nullptr;  // [B][K] scores of the selected items (optional)
+  int id_offset = 0;            // added to emitted item ids (sharding)
 };
+// Token union for an explicit chunk list (global ids, offset mapped).
+cudaError_t launch_tokens_from_chunks(const kvb_store* s, const int32_t* chunk_ids, int k,
+                                      int chunk_offset, int32_t* token_ids, int32_t* n_tokens,
+                                      int cap, cudaStream_t st);
 cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_t st);
 size_t select_smem_bytes(const kvb_store* s, int K, int mode);
 

@@ -41,7 +41,57 @@ struct SelParams {
   const uint32_t* res_bitmap;
   int n, cs, W, P;
   int stage;  // keys staged in shared memory
+  float* sel_scores;
+  int id_offset;
 };
+
+// Sorted union of selected items' tokens with the resident bitmap, compacted
+// by a block scan (ascending token ids; the reference's np.unique).
+// item(r) gives the r-th selected item; mode 0 items are chunks (minus
+// chunk_lo; ids outside [0, n_chunks) skipped), mode 1 items index cand_tok.
+template <typename ItemFn>
+__device__ __forceinline__ void token_union(const uint32_t* rb, int with_residents, int W,
+                                            uint32_t* bm, ItemFn item, int K, int mode, int cs,
+                                            int n, const int32_t* cand_tok, int chunk_lo,
+                                            int n_chunks, int32_t* dst, int cap, int32_t* n_out,
+                                            int32_t* err_flag, int* red) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int w = tid; w < W; w += nthr) bm[w] = with_residents ? rb[w] : 0u;
+  __syncthreads();
+  for (int r = tid; r < K; r += nthr) {
+    const int it = item(r);
+    if (mode == 0) {
+      const int c = it - chunk_lo;
+      if (it < 0 || c < 0 || c >= n_chunks) continue;
+      const int t0 = c * cs;
+      const int t1 = min(t0 + cs, n);
+      for (int t = t0; t < t1; ++t) atomicOr(&bm[t >> 5], 1u << (t & 31));
+    } else {
+      const int t = cand_tok[it];
+      atomicOr(&bm[t >> 5], 1u << (t & 31));
+    }
+  }
+  __syncthreads();
+  const int wpt = (W + nthr - 1) / nthr;
+  const int w0 = tid * wpt;
+  int cnt = 0;
+  for (int w = w0; w < w0 + wpt && w < W; ++w) cnt += __popc(bm[w]);
+  int total;
+  int pos = block_excl_scan(cnt, red, &total);
+  for (int w = w0; w < w0 + wpt && w < W; ++w) {
+    uint32_t bits = bm[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos < cap) dst[pos] = w * 32 + bit;
+      ++pos;
+    }
+  }
+  if (tid == 0) {
+    *n_out = total < cap ? total : cap;
+    if (total > cap && err_flag) atomicOr(err_flag, 1);
+  }
+}
 
 __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -203,50 +253,26 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
         }
         __syncthreads();
       }
-    for (int r = tid; r < p.K; r += nthr)
-      out_ids[r] = r < K ? (int32_t)(0xffffffffu - (uint32_t)keys64[r]) : -1;
+    for (int r = tid; r < p.K; r += nthr) {
+      const int id = r < K ? (int)(0xffffffffu - (uint32_t)keys64[r]) : -1;
+      out_ids[r] = id < 0 ? -1 : id + p.id_offset;
+      if (p.sel_scores) p.sel_scores[(size_t)b * p.K + r] = id < 0 ? -INFINITY : sc[id];
+    }
   } else {
-    for (int r = tid; r < p.K; r += nthr) out_ids[r] = r < K ? ids[r] : -1;
+    for (int r = tid; r < p.K; r += nthr) {
+      const int id = r < K ? ids[r] : -1;
+      out_ids[r] = id < 0 ? -1 : id + p.id_offset;
+      if (p.sel_scores) p.sel_scores[(size_t)b * p.K + r] = id < 0 ? -INFINITY : sc[id];
+    }
   }
   if (!p.token_ids) return;
   __syncthreads();
 
   // ---- 4. token union ----------------------------------------------------------
-  const uint32_t* rb = p.res_bitmap + (size_t)b * p.W;
-  for (int w = tid; w < p.W; w += nthr) bm[w] = p.with_residents ? rb[w] : 0u;
-  __syncthreads();
-  for (int r = tid; r < K; r += nthr) {
-    const int item = p.rank_order ? (int)(0xffffffffu - (uint32_t)keys64[r]) : ids[r];
-    if (p.mode == 0) {
-      const int t0 = item * p.cs;
-      const int t1 = min(t0 + p.cs, p.n);
-      for (int t = t0; t < t1; ++t) atomicOr(&bm[t >> 5], 1u << (t & 31));
-    } else {
-      const int t = p.cand_tok[(size_t)b * p.M_stride + item];
-      atomicOr(&bm[t >> 5], 1u << (t & 31));
-    }
-  }
-  __syncthreads();
-  const int wpt = (p.W + nthr - 1) / nthr;
-  const int w0 = tid * wpt;
-  int cnt = 0;
-  for (int w = w0; w < w0 + wpt && w < p.W; ++w) cnt += __popc(bm[w]);
-  int total;
-  int pos = block_excl_scan(cnt, red, &total);
-  int32_t* dst = p.token_ids + (size_t)b * p.cap;
-  for (int w = w0; w < w0 + wpt && w < p.W; ++w) {
-    uint32_t bits = bm[w];
-    while (bits) {
-      const int bit = __ffs(bits) - 1;
-      bits &= bits - 1;
-      if (pos < p.cap) dst[pos] = w * 32 + bit;
-      ++pos;
-    }
-  }
-  if (tid == 0) {
-    p.n_tokens[b] = total < p.cap ? total : p.cap;
-    if (total > p.cap && p.err_flag) atomicOr(p.err_flag, 1);
-  }
+  token_union(p.res_bitmap + (size_t)b * p.W, p.with_residents, p.W, bm,
+              [&](int r) { return p.rank_order ? (int)(0xffffffffu - (uint32_t)keys64[r]) : ids[r]; },
+              K, p.mode, p.cs, p.n, p.cand_tok + (p.mode ? (size_t)b * p.M_stride : 0), 0, 1 << 30,
+              p.token_ids + (size_t)b * p.cap, p.cap, p.n_tokens + b, p.err_flag, red);
 }
 
 int next_pow2(int x) {
@@ -278,6 +304,8 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
   p.cap = a.cap;
   p.with_residents = a.with_residents;
   p.err_flag = a.err_flag;
+  p.sel_scores = a.sel_scores;
+  p.id_offset = a.id_offset;
   p.res_bitmap = s->res_bitmap;
   p.n = s->d.n_tokens;
   p.cs = s->d.chunk_size;
@@ -290,6 +318,32 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
   ensure_smem((const void*)k2_select, smem);
   count_launch();
   k2_select<<<s->d.batch, kSelThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k2_union_chunks(const int32_t* __restrict__ ids, int k, int chunk_lo, int n_chunks,
+                const uint32_t* __restrict__ res_bitmap, int W, int cs, int n,
+                int32_t* __restrict__ token_ids, int32_t* __restrict__ n_tokens, int cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int red[33];
+  const int b = blockIdx.x;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
+  const int32_t* row = ids + (size_t)b * k;
+  token_union(res_bitmap + (size_t)b * W, 1, W, bm, [&](int r) { return row[r]; }, k, 0, cs, n,
+              nullptr, chunk_lo, n_chunks, token_ids + (size_t)b * cap, cap, n_tokens + b,
+              nullptr, red);
+}
+
+cudaError_t launch_tokens_from_chunks(const kvb_store* s, const int32_t* chunk_ids, int k,
+                                      int chunk_offset, int32_t* token_ids, int32_t* n_tokens,
+                                      int cap, cudaStream_t st) {
+  const size_t smem = (size_t)s->W * 4;
+  ensure_smem((const void*)k2_union_chunks, smem);
+  count_launch();
+  k2_union_chunks<<<s->d.batch, kSelThreads, smem, st>>>(chunk_ids, k, chunk_offset, s->C,
+                                                          s->res_bitmap, s->W, s->d.chunk_size,
+                                                          s->d.n_tokens, token_ids, n_tokens, cap);
   return cudaGetLastError();
 }
 

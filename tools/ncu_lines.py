@@ -23,10 +23,13 @@ rows = list(csv.reader(io.StringIO(out)))
 kname = rows[0][1]
 h = rows[1]
 ai, si, wi = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
+ei = h.index("Instructions Executed")
+stall_cols = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
 ins = []
 for r in rows[2:]:
     try:
-        ins.append((int(r[ai], 16), r[si].strip(), int(r[wi] or 0)))
+        st = {c: int(r[i] or 0) for i, c in stall_cols}
+        ins.append((int(r[ai], 16), r[si].strip(), int(r[wi] or 0), int(r[ei] or 0), st))
     except Exception:
         pass
 base = ins[0][0]
@@ -55,18 +58,29 @@ for (fn, off), v in lines_at.items():
 best, score = None, -1
 for fn, d in fns.items():
     s = 0
-    for a, src, _ in ins[:200]:
+    for a, src, *_ in ins[:200]:
         v = d.get(a - base)
         if v and v[1].split()[0].rstrip(";") in src:
             s += 1
     if s > score:
         best, score = fn, s
 agg = defaultdict(int)
+execd = defaultdict(int)
+reasons = defaultdict(lambda: defaultdict(int))
+total_reasons = defaultdict(int)
 tot = 0
-for a, src, w in ins:
+for a, src, w, ex, st in ins:
     v = fns[best].get(a - base)
-    agg[v[0] if v else "?"] += w
+    key = v[0] if v else "?"
+    agg[key] += w
+    execd[key] += ex
     tot += w
+    for c, n in st.items():
+        reasons[key][c] += n
+        total_reasons[c] += n
 print(f"kernel {kname[:80]}  (function {best[:60]}, match {score}/200)  samples {tot}")
+print("overall stalls:", ", ".join(f"{c[6:]}={n}" for c, n in sorted(total_reasons.items(), key=lambda x: -x[1])[:6]))
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
-    print(f"{v:7d} {100 * v / max(tot, 1):5.1f}%  {k}")
+    rs = sorted(reasons[k].items(), key=lambda x: -x[1])[:3]
+    print(f"{v:7d} {100 * v / max(tot, 1):5.1f}%  {k:28s} inst={execd[k]:9d}  " +
+          " ".join(f"{c[6:]}={n}" for c, n in rs))
