@@ -132,70 +132,127 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   }
   auto key_at = [&](int i) -> uint32_t { return p.stage ? ukeys[i] : score_key(__ldg(sc + i)); };
 
-  // ---- 1. radix select ----------------------------------------------------
-  uint32_t prefix = 0u, pmask = 0u;
-  int krem = K, eqcnt = 0;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int i = lane; i < 256; i += 32) whist[warp][i] = 0;
-    __syncwarp();
-    for (int base = warp * 32 * 4; base < M; base += nthr * 4) {
-      uint32_t u4[4];
+  // ---- 1. find T = K-th largest key and how many ties at T to take -----------
+  uint32_t T;
+  int krem, eqcnt;
+  constexpr int kRegItems = 32;  // register path when M <= 32 * 1024
+  uint32_t rk[kRegItems];
+  const bool regpath = M <= kRegItems * nthr;
+  if (regpath) {
+    // keys of ids i = r * nthr + tid, r < kRegItems, held in registers
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = base + k * 32 + lane;
-        u4[k] = i < M ? key_at(i) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = base + k * 32 + lane;
-        if (i < M && (u4[k] & pmask) == prefix) atomicAdd(&whist[warp][(u4[k] >> shift) & 255u], 1);
-      }
+    for (int r = 0; r < kRegItems; ++r) {
+      const int i = r * nthr + tid;
+      rk[r] = i < M ? key_at(i) : 0u;  // key 0 is below every finite score
     }
-    __syncthreads();
-    for (int bin = tid; bin < 256; bin += nthr) {
+    // exact bisection over the 32-bit key space: largest T with
+    // #(key >= T) >= K; counts via redux.sync + one barrier per round
+    __shared__ int cntw[2][kSelThreads / 32];
+    uint32_t lo = 0u, hi = 0xffffffffu;
+    int round = 0;
+    while (lo < hi) {
+      const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
       int c = 0;
+#pragma unroll
+      for (int r = 0; r < kRegItems; ++r) c += rk[r] >= mid ? 1 : 0;
+      c = __reduce_add_sync(FULL, c);
+      if (lane == 0) cntw[round & 1][warp] = c;
+      __syncthreads();
+      int tot = 0;
 #pragma unroll 8
-      for (int w = 0; w < kSelThreads / 32; ++w) c += whist[w][bin];
-      hist[bin] = c;
+      for (int w = 0; w < kSelThreads / 32; ++w) tot += cntw[round & 1][w];
+      if (tot >= K) lo = mid; else hi = mid - 1u;
+      ++round;
+    }
+    T = lo;
+    int gt = 0, eq = 0;
+#pragma unroll
+    for (int r = 0; r < kRegItems; ++r) {
+      gt += rk[r] > T ? 1 : 0;
+      eq += rk[r] == T ? 1 : 0;
+    }
+    gt = __reduce_add_sync(FULL, gt);
+    eq = __reduce_add_sync(FULL, eq);
+    __shared__ int gtw[kSelThreads / 32], eqw[kSelThreads / 32];
+    if (lane == 0) {
+      gtw[warp] = gt;
+      eqw[warp] = eq;
     }
     __syncthreads();
-    if (warp == 0) {
-      int c[8], loc = 0;
+    int gsum = 0, esum = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) {
+      gsum += gtw[w];
+      esum += eqw[w];
+    }
+    krem = K - gsum;
+    eqcnt = esum;
+  } else {
+  // ---- 1. radix select ----------------------------------------------------
+    uint32_t prefix = 0u, pmask = 0u;
+    int krem = K, eqcnt = 0;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int i = lane; i < 256; i += 32) whist[warp][i] = 0;
+      __syncwarp();
+      for (int base = warp * 32 * 4; base < M; base += nthr * 4) {
+        uint32_t u4[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = hist[lane * 8 + j];
-        loc += c[j];
-      }
-      int suf = loc;
+        for (int k = 0; k < 4; ++k) {
+          const int i = base + k * 32 + lane;
+          u4[k] = i < M ? key_at(i) : 0u;
+        }
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_down_sync(FULL, suf, o);
-        if (lane + o < 32) suf += t;
-      }
-      const int above = suf - loc;
-      const bool hit = (above < krem) && (krem <= suf);
-      if (hit) {
-        int acc = above;
-        for (int j = 7; j >= 0; --j) {
-          if (acc + c[j] >= krem) {
-            s_digit = lane * 8 + j;
-            s_krem = krem - acc;
-            s_eq = c[j];
-            break;
-          }
-          acc += c[j];
+        for (int k = 0; k < 4; ++k) {
+          const int i = base + k * 32 + lane;
+          if (i < M && (u4[k] & pmask) == prefix) atomicAdd(&whist[warp][(u4[k] >> shift) & 255u], 1);
         }
       }
+      __syncthreads();
+      for (int bin = tid; bin < 256; bin += nthr) {
+        int c = 0;
+#pragma unroll 8
+        for (int w = 0; w < kSelThreads / 32; ++w) c += whist[w][bin];
+        hist[bin] = c;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int c[8], loc = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          c[j] = hist[lane * 8 + j];
+          loc += c[j];
+        }
+        int suf = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_down_sync(FULL, suf, o);
+          if (lane + o < 32) suf += t;
+        }
+        const int above = suf - loc;
+        const bool hit = (above < krem) && (krem <= suf);
+        if (hit) {
+          int acc = above;
+          for (int j = 7; j >= 0; --j) {
+            if (acc + c[j] >= krem) {
+              s_digit = lane * 8 + j;
+              s_krem = krem - acc;
+              s_eq = c[j];
+              break;
+            }
+            acc += c[j];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)s_digit << shift;
+      pmask |= 0xffu << shift;
+      krem = s_krem;
+      eqcnt = s_eq;
+      __syncthreads();
     }
-    __syncthreads();
-    prefix |= (uint32_t)s_digit << shift;
-    pmask |= 0xffu << shift;
-    krem = s_krem;
-    eqcnt = s_eq;
-    __syncthreads();
+    T = prefix;
   }
-  const uint32_t T = prefix;
+
 
   // ---- 2. collect ----------------------------------------------------------
   if (tid == 0) s_cnt = 0;
@@ -207,16 +264,30 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     else
       ids[pos] = i;
   };
-  for (int base = warp * 32; base < M; base += nthr) {
-    const int i = base + lane;
-    const bool valid = i < M;
-    const uint32_t u = valid ? key_at(i) : 0u;
-    const bool take = valid && (u > T || (all_ties && u == T));
-    const unsigned m = __ballot_sync(FULL, take);
-    int wb = 0;
-    if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
-    wb = __shfl_sync(FULL, wb, 0);
-    if (take) put(wb + __popc(m & ((1u << lane) - 1u)), u, i);
+  if (regpath) {
+#pragma unroll
+    for (int r = 0; r < kRegItems; ++r) {
+      const int i = r * nthr + tid;
+      const uint32_t u = rk[r];
+      const bool take = i < M && (u > T || (all_ties && u == T));
+      const unsigned m = __ballot_sync(FULL, take);
+      int wb = 0;
+      if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+      wb = __shfl_sync(FULL, wb, 0);
+      if (take) put(wb + __popc(m & ((1u << lane) - 1u)), u, i);
+    }
+  } else {
+    for (int base = warp * 32; base < M; base += nthr) {
+      const int i = base + lane;
+      const bool valid = i < M;
+      const uint32_t u = valid ? key_at(i) : 0u;
+      const bool take = valid && (u > T || (all_ties && u == T));
+      const unsigned m = __ballot_sync(FULL, take);
+      int wb = 0;
+      if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+      wb = __shfl_sync(FULL, wb, 0);
+      if (take) put(wb + __popc(m & ((1u << lane) - 1u)), u, i);
+    }
   }
   __syncthreads();
   if (!all_ties) {

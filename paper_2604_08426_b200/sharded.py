@@ -1,0 +1,220 @@
+"""Sequence sharding of one long context across P GPUs (BASELINE config C4,
+SURVEY.md section 8e). The reference is single-process; this is
+new, built so that the sharded step reproduces the single-store decode:
+
+* partition: rank p owns the chunk-aligned token range
+  [chunk_lo*cs, min(chunk_hi*cs, n)), chunk_lo = p*C // P;
+* prefill: chunk means are chunk-local (identical to the unsharded ones); the
+  outlier order is global (kvstore.py:181-189), so per-chunk cosines are
+  all-gathered and every rank runs the same greedy fill (kvb_choose_outliers);
+  the local window (the last w tokens) lands on the last rank(s); the
+  head-concatenated SVD uses the all-reduced Gram matrix K^T K;
+* decode, exchange 1: each rank's local top-K (score, global chunk id) are
+  all-gathered and merged by kvb_merge_topk on (score desc, global id asc) --
+  exactly the global stable top-K, because every global winner is in the
+  top-K of its own shard;
+* decode, exchange 2: each rank attends to its selected + resident tokens and
+  returns (o, lse); all-gather + kvb_merge_attention is the exact LSE merge.
+
+Collectives go through an ``Exchange`` (torch.distributed: NCCL on GPUs,
+gloo in the CPU tests) or ``LocalExchange`` (all shards in one process, used
+by the single-GPU parity test).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    n_tokens: int
+    chunk_size: int
+    parts: int
+    rank: int
+
+    @property
+    def n_chunks(self) -> int:
+        return -(-self.n_tokens // self.chunk_size)
+
+    @property
+    def chunk_lo(self) -> int:
+        return self.rank * self.n_chunks // self.parts
+
+    @property
+    def chunk_hi(self) -> int:
+        return (self.rank + 1) * self.n_chunks // self.parts
+
+    @property
+    def token_lo(self) -> int:
+        return self.chunk_lo * self.chunk_size
+
+    @property
+    def token_hi(self) -> int:
+        return min(self.chunk_hi * self.chunk_size, self.n_tokens)
+
+    @property
+    def n_local(self) -> int:
+        return self.token_hi - self.token_lo
+
+    def local_window(self, w: int) -> np.ndarray:
+        """Local ids of the global last-w tokens that fall in this shard."""
+        w = min(w, self.n_tokens)
+        lo = max(self.n_tokens - w, self.token_lo)
+        hi = self.token_hi
+        return np.arange(lo, hi) - self.token_lo if hi > lo else np.empty(0, np.int64)
+
+
+class Exchange:
+    """all_gather / all_reduce over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.parts = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.contiguous()
+        out = torch.empty((self.parts,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        try:
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the fused op
+            parts = [torch.empty_like(t) for _ in range(self.parts)]
+            self.dist.all_gather(parts, t, group=self.group)
+            out = torch.stack(parts)
+        return out
+
+    def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+class LocalExchange:
+    """Single-process stand-in: the caller supplies every shard's tensor."""
+
+    def __init__(self, parts: int):
+        self.parts = parts
+
+    @staticmethod
+    def all_gather_list(ts) -> torch.Tensor:
+        return torch.stack([t.contiguous() for t in ts])
+
+
+def gather_padded(ex, t: torch.Tensor, length: int, fill) -> torch.Tensor:
+    """all_gather of per-rank [B, m_p] rows with different m_p: pad to
+    `length` with `fill`, gather -> [P, B, length]."""
+    pad = torch.full((t.shape[0], length), fill, dtype=t.dtype, device=t.device)
+    pad[:, : t.shape[1]] = t
+    return ex.all_gather(pad)
+
+
+def global_outliers(per_chunk_all: np.ndarray, counts, n_tokens: int, chunk_size: int,
+                    budget: int) -> tuple:
+    """Greedy outlier choice over the concatenated per-chunk cosines of all
+    shards (kvstore.py:181-190), identical on every rank."""
+    lib = L.load()
+    pc = np.ascontiguousarray(np.concatenate([per_chunk_all[p, : counts[p]]
+                                              for p in range(len(counts))]), dtype=np.float64)
+    out = np.zeros(max(1, len(pc)), dtype=np.int32)
+    cnt = C.c_int32()
+    L.check(lib.kvb_choose_outliers(pc.ctypes.data_as(C.c_void_p), len(pc), n_tokens, chunk_size,
+                                    budget, out.ctypes.data_as(C.c_void_p), C.byref(cnt)),
+            "kvb_choose_outliers")
+    return tuple(int(c) for c in out[: cnt.value])
+
+
+def local_outliers(global_chunks: tuple, spec: ShardSpec) -> tuple:
+    return tuple(c - spec.chunk_lo for c in global_chunks if spec.chunk_lo <= c < spec.chunk_hi)
+
+
+# ---------------------------------------------------------------------------
+# per-shard decode primitives (each one libkvb call on the shard's store)
+# ---------------------------------------------------------------------------
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def local_candidates(store, q: torch.Tensor, k: int, chunk_lo: int, aggregation: str = "sum"):
+    """(scores [B, k] f32, global chunk ids [B, k] i32) of this shard's top-k."""
+    G = store._check_q(q)
+    sc = torch.empty((store.batch, k), dtype=torch.float32, device="cuda")
+    ids = torch.empty((store.batch, k), dtype=torch.int32, device="cuda")
+    nb = store.lib.kvb_select_candidates_workspace_bytes(store.h, k)
+    ws = store.workspace(nb)
+    agg = L.KVB_AGG_SUM if aggregation == "sum" else L.KVB_AGG_MAX
+    L.check(store.lib.kvb_select_candidates(store.h, _ptr(q), G, k, agg, chunk_lo, _ptr(sc),
+                                            _ptr(ids), _ptr(ws), ws.numel(), _stream()),
+            "kvb_select_candidates")
+    return sc, ids
+
+
+def merge_candidates(scores_all: torch.Tensor, ids_all: torch.Tensor, k: int) -> torch.Tensor:
+    """[P, B, k] candidates -> global top-k chunk ids [B, k] (rank order)."""
+    P, B, kk = scores_all.shape
+    out = torch.empty((B, kk), dtype=torch.int32, device="cuda")
+    L.check(L.load().kvb_merge_topk(_ptr(scores_all.contiguous()), _ptr(ids_all.contiguous()), P,
+                                    B, kk, _ptr(out), _stream()), "kvb_merge_topk")
+    if kk != k:
+        out = out[:, :k].contiguous()
+    return out
+
+
+def local_tokens(store, chunk_ids: torch.Tensor, chunk_lo: int, cap: int):
+    tok = torch.empty((store.batch, cap), dtype=torch.int32, device="cuda")
+    ntok = torch.empty(store.batch, dtype=torch.int32, device="cuda")
+    L.check(store.lib.kvb_tokens_from_chunks(store.h, _ptr(chunk_ids), chunk_ids.shape[1],
+                                             chunk_lo, _ptr(tok), _ptr(ntok), cap, _stream()),
+            "kvb_tokens_from_chunks")
+    return tok, ntok
+
+
+def merge_attention(out_all: torch.Tensor, lse_all: torch.Tensor) -> tuple:
+    """[P, B, H, G, D] + [P, B, H, G] -> exact LSE merge (out, lse)."""
+    P = out_all.shape[0]
+    shape = out_all.shape[1:]
+    rows = int(np.prod(shape[:-1]))
+    D = shape[-1]
+    out = torch.empty(shape, dtype=torch.float32, device="cuda")
+    lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
+    L.check(L.load().kvb_merge_attention(_ptr(out_all.contiguous()), _ptr(lse_all.contiguous()), P,
+                                         rows, D, _ptr(out), _ptr(lse), _stream()),
+            "kvb_merge_attention")
+    return out, lse
+
+
+def global_k(n_tokens: int, chunk_size: int, sparse_fraction: float) -> int:
+    """selection.py:85 on the global context."""
+    C_ = -(-n_tokens // chunk_size)
+    return min(C_, math.ceil(sparse_fraction * n_tokens / chunk_size))
+
+
+class ShardedDecoder:
+    """One rank's view of a sequence-sharded decode step (torch.distributed)."""
+
+    def __init__(self, store, spec: ShardSpec, exchange: Exchange, k_global: int):
+        self.store, self.spec, self.ex, self.k = store, spec, exchange, k_global
+        self.k_local = min(k_global, store.C)
+        self.cap = min(store.n, k_global * store.cs + store.max_resident)
+
+    def step(self, q: torch.Tensor):
+        sc, ids = local_candidates(self.store, q, self.k, self.spec.chunk_lo)
+        chunk_ids = merge_candidates(self.ex.all_gather(sc), self.ex.all_gather(ids), self.k)
+        tok, ntok = local_tokens(self.store, chunk_ids, self.spec.chunk_lo, self.cap)
+        out_p, lse_p = self.store.attend(q, tok, ntok, want_lse=True)
+        out, lse = merge_attention(self.ex.all_gather(out_p), self.ex.all_gather(lse_p))
+        return out, lse, chunk_ids

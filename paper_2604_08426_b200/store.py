@@ -177,6 +177,14 @@ class DeviceStore:
                 "kvb_store_set_offload")
         return self
 
+    def build_landmarks(self, keys: torch.Tensor):
+        """Landmarks (and residuals) only -- kvstore.py:129-140."""
+        self._check_kv(keys, "keys")
+        L.check(self.lib.kvb_build_landmarks(self.h, _ptr(keys), _stream()), "kvb_build_landmarks")
+        if self.residual is not None:
+            L.check(self.lib.kvb_build_residuals(self.h, _ptr(keys), _stream()),
+                    "kvb_build_residuals")
+
     def svd_factors(self, keys: torch.Tensor, method: str = "auto"):
         """fp16 low-rank factors of the (head-grouped) key matrix
         (numerics.py:80-98 + quantization.py:490-497): left = U*S, right = V^T,
