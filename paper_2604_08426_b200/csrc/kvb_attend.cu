@@ -7,17 +7,23 @@
 //   other token, slow tier SVD: key = left[t] . right (quantization.py:507-513),
 //     V exact from the offload tier.
 //
-// Grid (token tiles of 64, sequences); one CTA holds all KV heads of its tile
-// because the token-major layout makes a token's K (V) one contiguous 2 KiB
-// (bf16, Llama-3-8B) row. Phase 1 computes the logits (q.k)*fp32(1/sqrt(D))
-// of every (token, head, query) into shared memory; phase 2 takes the per-row
-// max and exp; phase 3 accumulates sum_t p*V. Each tile emits (m, l, o)
-// partials; k5_combine merges them with the exact log-sum-exp rule and also
-// returns the LSE used by the cross-GPU merge.
-//
-// SVD keys, fold path (k_path 1): logits = left[t] . q~ with
-// q~[h,g] = right_h . q[h,g] precomputed once per (sequence, head) by
-// k5_fold_queries -- mathematically q.(left.right_h), 32x fewer MACs.
+// Grid (splits, sequences): one wave of persistent CTAs; each owns a
+// contiguous range of the sequence's selected tokens and streams it in
+// sub-tiles of 16 (bf16) / 8 (fp32) tokens through double-buffered cp.async
+// staging of exact K rows (head-padded), fp16 left-factor rows and V rows
+// (row strides padded to odd multiples of 16 B: conflict-free ldmatrix).
+//   phase 1  logits (q.k)*fp32(1/sqrt(D)), lane layout (head, query):
+//            SVD tokens on tensor cores -- mma.sync m16n8k16 with A = the
+//            token's exact fp16 factor row and B = q~ = right.q split into
+//            fp16 hi + lo (k5_prep), i.e. q.(left.right) to ~fp32 accuracy;
+//            exact-key tokens on CUDA cores (fp32 FMA);
+//   phase 2  online softmax (running max / sum per (head, query));
+//   phase 3  o = alpha*o + sum_t p_t V_t: bf16 stores on tensor cores
+//            (A = P^T split exactly into 3 bf16 parts, B = V via
+//            ldmatrix.trans), fp32 stores on CUDA cores.
+// Each CTA emits (m, l, o) partials; the last CTA of a sequence (ticket
+// counter) merges them with the exact log-sum-exp rule and also returns the
+// LSE used by the cross-GPU merge (kvb_merge_attention).
 
 #include <type_traits>
 
@@ -49,6 +55,9 @@ struct AttParams {
   float* pm;             // [B][splits][H*G]
   float* pl;
   float* po;             // [B][splits][H*G][D]
+  int* counters;         // [B] split tickets (zeroed per call)
+  float* out;            // [B][H][G][D]
+  float* lse;            // [B][H][G] (may be null)
   // shared-memory geometry (bytes)
   int krow, kpad_head, lrow, vrow;
   int off_qt, off_lg, off_alpha, off_tok, off_buf, buf_bytes, boff_l, boff_v;
@@ -533,6 +542,53 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
       }
     }
   }
+
+  // ---- fused split merge: the last CTA of this sequence combines ---------------
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(p.counters + b, 1) == nsplit - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float* wts = reinterpret_cast<float*>(bufs);        // [HG][nsplit] merge weights
+  float* Ls = wts + (size_t)HG * nsplit;               // [HG]
+  float* Ms = Ls + HG;                                 // [HG]
+  const size_t base = (size_t)b * nsplit * HG;
+  for (int row = warp; row < HG; row += nwarp) {
+    float m = -INFINITY;
+    for (int i = lane; i < nsplit; i += 32) {
+      const float li = __ldcg(p.pl + base + (size_t)i * HG + row);
+      const float mi = li > 0.f ? __ldcg(p.pm + base + (size_t)i * HG + row) : -INFINITY;
+      wts[row * nsplit + i] = mi;
+      m = fmaxf(m, mi);
+    }
+    m = warp_max(m);
+    float l = 0.f;
+    for (int i = lane; i < nsplit; i += 32) {
+      const float mi = wts[row * nsplit + i];
+      const float w = mi == -INFINITY ? 0.f : expf(mi - m);
+      wts[row * nsplit + i] = w;
+      l += w * __ldcg(p.pl + base + (size_t)i * HG + row);
+    }
+    l = warp_sum_butterfly(l);
+    if (lane == 0) {
+      Ls[row] = l;
+      Ms[row] = m;
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < HG * D; o += blockDim.x) {
+    const int row = o / D, d = o - row * D;
+    float a = 0.f;
+    const float* w = wts + row * nsplit;
+    for (int i = 0; i < nsplit; ++i)
+      a = fmaf(__ldcg(p.po + (base + (size_t)i * HG + row) * D + d), w[i], a);
+    p.out[((size_t)b * HG + row) * D + d] = a / Ls[row];
+  }
+  if (p.lse)
+    for (int row = tid; row < HG; row += blockDim.x)
+      p.lse[(size_t)b * HG + row] = Ms[row] + logf(Ls[row]);
 }
 
 // Per-sequence prep: q2 = q transposed to [D/2][HG][2]; for SVD stores also
@@ -545,27 +601,32 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                int H, int G, int D, int r, int sgroups) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
+  const int rs = blockIdx.z, nrs = gridDim.z;  // this CTA folds rows [r0, r1)
   const int HG = H * G;
   float* qs = fsm;                 // [G][D]
   const float* qb = q + ((size_t)b * H + h) * G * D;
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const float v = qb[i];
     qs[i] = v;
-    const int g = i / D, d = i - g * D;
-    q2[(size_t)b * HG * D + ((size_t)(d >> 1) * HG + h * G + g) * 2 + (d & 1)] = v;
+    if (rs == 0) {
+      const int g = i / D, d = i - g * D;
+      q2[(size_t)b * HG * D + ((size_t)(d >> 1) * HG + h * G + g) * 2 + (d & 1)] = v;
+    }
   }
   if (!right) return;
-  float* rs = fsm + G * D;          // [r][D+1]
+  const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
+  float* rsm = fsm + G * D;         // [r][D+1] (rows r0..r1 used)
   const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
   const int Dg = hpg * D;
   const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
   if ((D % 8) == 0 && (Dg % 8) == 0 && (col0 % 8) == 0) {
     const int cpr = D / 8;  // 16-byte chunks per row
-    for (int i = threadIdx.x; i < r * cpr; i += blockDim.x) {
-      const int rr = i / cpr, c = i - rr * cpr;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < (r1 - r0) * cpr; i += blockDim.x) {
+      const int rr = r0 + i / cpr, c = i % cpr;
       const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
       const __half2* hv = reinterpret_cast<const __half2*>(&u);
-      float* dst = rs + rr * (D + 1) + c * 8;
+      float* dst = rsm + rr * (D + 1) + c * 8;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __half22float2(hv[k]);
@@ -574,77 +635,21 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
       }
     }
   } else {
-    for (int i = threadIdx.x; i < r * D; i += blockDim.x) {
-      const int rr = i / D, d = i - rr * D;
-      rs[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+    for (int i = threadIdx.x; i < (r1 - r0) * D; i += blockDim.x) {
+      const int rr = r0 + i / D, d = i % D;
+      rsm[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
     }
   }
   __syncthreads();
-  for (int o = threadIdx.x; o < r * G; o += blockDim.x) {
-    const int g = o / r, rr = o - g * r;
-    const float* rw = rs + rr * (D + 1);
+  for (int o = threadIdx.x; o < (r1 - r0) * G; o += blockDim.x) {
+    const int g = o / (r1 - r0), rr = r0 + o % (r1 - r0);
+    const float* rw = rsm + rr * (D + 1);
     const float* qq = qs + g * D;
     float acc = 0.f;
 #pragma unroll 8
     for (int d = 0; d < D; ++d) acc = fmaf(rw[d], qq[d], acc);
     qt2[(size_t)b * HG * r + ((size_t)(rr >> 1) * HG + h * G + g) * 2 + (rr & 1)] = acc;
   }
-}
-
-// Exact LSE merge of the split partials; one CTA per (sequence, head, query).
-__global__ void __launch_bounds__(128) k5_combine(const float* __restrict__ pm,
-                                                  const float* __restrict__ pl,
-                                                  const float* __restrict__ po, int splits, int H,
-                                                  int G, int D, float* __restrict__ out,
-                                                  float* __restrict__ lse) {
-  __shared__ float w_s[1024];
-  __shared__ float red[2];
-  __shared__ float wm[4], wl[4];
-  const int row = blockIdx.x, b = blockIdx.y;  // row = h*G + g
-  const int HG = H * G;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float m = -INFINITY;
-  for (int i = threadIdx.x; i < splits; i += blockDim.x) {
-    const size_t o = ((size_t)b * splits + i) * HG + row;
-    const float mi = pl[o] > 0.f ? pm[o] : -INFINITY;
-    w_s[i] = mi;
-    m = fmaxf(m, mi);
-  }
-  m = warp_max(m);
-  if (lane == 0) wm[warp] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float M = wm[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, wm[w]);
-    red[0] = M;
-  }
-  __syncthreads();
-  const float M = red[0];
-  float lsum = 0.f;
-  for (int i = threadIdx.x; i < splits; i += blockDim.x) {
-    const size_t o = ((size_t)b * splits + i) * HG + row;
-    const float wi = w_s[i] == -INFINITY ? 0.f : expf(w_s[i] - M);
-    w_s[i] = wi;
-    lsum += pl[o] * wi;
-  }
-  lsum = warp_sum_butterfly(lsum);
-  if (lane == 0) wl[warp] = lsum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float L = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) L += wl[w];
-    red[1] = L;
-  }
-  __syncthreads();
-  const float L = red[1];
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float acc = 0.f;
-#pragma unroll 4
-    for (int i = 0; i < splits; ++i)
-      acc = fmaf(po[(((size_t)b * splits + i) * HG + row) * D + d], w_s[i], acc);
-    out[((size_t)b * HG + row) * D + d] = acc / L;
-  }
-  if (lse && threadIdx.x == 0) lse[(size_t)b * HG + row] = M + logf(L);
 }
 
 struct AttGeom {
@@ -696,7 +701,7 @@ size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
   const AttGeom g = attend_geometry(s, G, cap);
   const size_t B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim;
   size_t bytes = B * g.splits * H * G * (2 + D) * sizeof(float) + 4096;
-  bytes += B * H * G * D * sizeof(float);                       // q2
+  bytes += B * H * G * D * sizeof(float) + B * sizeof(int) + 64; // q2, split tickets
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
   return bytes;
 }
@@ -715,12 +720,14 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   float* q2 = po + (size_t)B * splits * H * G * D;
   q2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q2) + 15) & ~uintptr_t(15));
   float* qt2 = q2 + (size_t)B * H * G * D;
+  int* counters = reinterpret_cast<int*>(qt2 + (size_t)B * H * G * (svd ? r : 0));
+  cudaMemsetAsync(counters, 0, sizeof(int) * B, st);
   {
     const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
     ensure_smem((const void*)k5_prep, fs);
     count_launch();
-    k5_prep<<<dim3(H, B), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, q2, qt2, H, G, D, r,
-                                         svd ? s->d.svd_groups : 1);
+    k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, q2, qt2,
+                                                      H, G, D, r, svd ? s->d.svd_groups : 1);
   }
   AttParams& p = geo.p;
   p.tok = a.token_ids;
@@ -748,7 +755,10 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   p.pm = pm;
   p.pl = pl;
   p.po = po;
-  count_launch(2);
+  p.counters = counters;
+  p.out = a.out;
+  p.lse = a.lse;
+  count_launch(1);
   if (s->d.kv_dtype == KVB_BF16) {
     ensure_smem((const void*)k5_attend<__nv_bfloat16, 16>, geo.smem);
     k5_attend<__nv_bfloat16, 16><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
@@ -756,7 +766,6 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
     ensure_smem((const void*)k5_attend<float, 8>, geo.smem);
     k5_attend<float, 8><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
   }
-  k5_combine<<<dim3(H * G, B), 128, 0, st>>>(pm, pl, po, splits, H, G, D, a.out, a.lse);
   return cudaGetLastError();
 }
 
