@@ -177,6 +177,8 @@ typedef struct kvb_select_args {
   int32_t aggregation;      /* kvb_aggregation (selection.py:46-52)          */
   int32_t rank_order;       /* 1: chunk_ids in rank order (best first)       */
   int32_t token_capacity;   /* row stride of token_ids                       */
+  int32_t exact_scores;     /* 1: bit-reproducible CUDA-core scoring order;
+                               0: fastest (HIGGS 2-bit on tensor cores)      */
 } kvb_select_args;
 
 /* select_by_landmarks (selection.py:72-87): scores, deterministic top-K

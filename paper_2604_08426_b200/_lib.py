@@ -40,7 +40,7 @@ class StoreInfo(C.Structure):
 class SelectArgs(C.Structure):
     _fields_ = [("queries_per_head", C.c_int32), ("n_select", C.c_int32),
                 ("aggregation", C.c_int32), ("rank_order", C.c_int32),
-                ("token_capacity", C.c_int32)]
+                ("token_capacity", C.c_int32), ("exact_scores", C.c_int32)]
 
 
 class ResidualArgs(C.Structure):

@@ -504,9 +504,10 @@ kvb_status kvb_store_set_residuals_higgs(kvb_store* s, const uint8_t* codes, con
 // ---- decode ----------------------------------------------------------------
 
 static kvb_status score_landmarks(kvb_store* s, const float* q, int G, int agg, float* scores,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, uint32_t* hist = nullptr) {
   if (s->d.landmark_kind == KVB_LM_DENSE)
-    KVB_CUDA(launch_score_dense(s, q, G, agg, scores, st), "landmark scoring");
+    KVB_CUDA(launch_score_dense(s, q, G, agg, scores, agg == KVB_AGG_SUM ? hist : nullptr, st),
+             "landmark scoring");
   else
     KVB_CUDA(launch_score_higgs(s, q, G, agg, scores, st), "HIGGS landmark scoring");
   return KVB_OK;
@@ -523,7 +524,9 @@ kvb_status kvb_score_landmarks(kvb_store* s, const float* q, int32_t G, int32_t 
 
 int64_t kvb_select_workspace_bytes(const kvb_store* s, const kvb_select_args* a) {
   if (!s || !a) return -1;
-  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned(4) + 256);
+  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned(4) +
+                   aligned(higgs_tc_ws_bytes(s)) + aligned((size_t)s->d.batch * kTopHistBins * 4) +
+                   256);
 }
 
 static kvb_status check_select(const kvb_store* s, const kvb_select_args* a) {
@@ -552,7 +555,18 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
   Carve cv(ws, ws_bytes);
   float* sc = scores ? scores : cv.take<float>((size_t)s->d.batch * s->C);
   int32_t* err = cv.take<int32_t>(1);
-  if ((ks = score_landmarks(s, q, a->queries_per_head, a->aggregation, sc, st)) != KVB_OK) return ks;
+  void* tcws = cv.take<char>(higgs_tc_ws_bytes(s));
+  uint32_t* hist = cv.take<uint32_t>((size_t)s->d.batch * kTopHistBins);
+  const bool use_hist = s->d.landmark_kind == KVB_LM_DENSE && a->aggregation == KVB_AGG_SUM;
+  if (use_hist)
+    KVB_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+  if (!a->exact_scores && a->aggregation == KVB_AGG_SUM && higgs_tc_supported(s)) {
+    KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, sc, tcws, st),
+             "HIGGS tensor-core scoring");
+  } else if ((ks = score_landmarks(s, q, a->queries_per_head, a->aggregation, sc, st,
+                                   use_hist ? hist : nullptr)) != KVB_OK) {
+    return ks;
+  }
   SelectLaunch L{};
   L.scores = sc;
   L.M_stride = s->C;
@@ -566,6 +580,7 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
   L.cap = a->token_capacity;
   L.with_residents = 1;
   L.err_flag = nullptr;
+  L.hist = use_hist ? hist : nullptr;
   (void)err;
   KVB_CUDA(launch_select(s, L, st), "top-k selection");
   return KVB_OK;

@@ -700,7 +700,12 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
 size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
   const AttGeom g = attend_geometry(s, G, cap);
   const size_t B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim;
-  size_t bytes = B * g.splits * H * G * (2 + D) * sizeof(float) + 4096;
+  size_t splits = g.splits;
+  if (attend_wh_supported(s, G)) {
+    const size_t sw = attend_wh_splits(s, cap);
+    if (sw > splits) splits = sw;
+  }
+  size_t bytes = B * splits * H * G * (2 + D) * sizeof(float) + 4096;
   bytes += B * H * G * D * sizeof(float) + B * sizeof(int) + 64; // q2, split tickets
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
   return bytes;
@@ -712,7 +717,8 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   if (geo.smem > 227 * 1024) return cudaErrorInvalidValue;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
-  const int splits = geo.splits;
+  const bool wh = attend_wh_supported(s, G);
+  const int splits = wh ? attend_wh_splits(s, a.cap) : geo.splits;
   float* ws = static_cast<float*>(a.ws);
   float* pm = ws;
   float* pl = pm + (size_t)B * splits * H * G;
@@ -729,6 +735,9 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
     k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, q2, qt2,
                                                       H, G, D, r, svd ? s->d.svd_groups : 1);
   }
+  if (wh)
+    return launch_attend_wh(s, a.q, G, a.token_ids, a.n_tokens, a.cap, qt2, pm, pl, po, splits,
+                            a.out, a.lse, st);
   AttParams& p = geo.p;
   p.tok = a.token_ids;
   p.ntok = a.n_tokens;

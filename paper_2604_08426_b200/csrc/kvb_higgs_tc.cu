@@ -1,0 +1,207 @@
+// K1-H fast path -- HIGGS landmark scoring on tensor cores (rotated domain).
+//
+// The reference dequantises a group of g = R*D landmark values (R rows of
+// one head, D = 128) as x = signs (.) H_g (vq * c) / sqrt(g)
+// (quantization.py:459-477, numerics.py:111-125) and scores row k of the
+// group as s_k = sum_d qbar[d] x[k*D + d] (selection.py:83-84, sum over
+// queries folded into qbar). With Sylvester ordering H_g = H_R (x) H_D, so
+//
+//   s_k = c/sqrt(g) * sum_a H_R[k,a] * (vq_a . w_k),   w_k = H_D (signs_k (.) qbar)
+//
+// i.e. the transform moves to the query side (R rotated queries per head,
+// computed once per step by k1h_prep) and the scan is a GEMM of the decoded
+// codewords [rows x D] by W_h [D x R]. It runs on mma.sync m16n8k16 with the
+// codewords and W split into fp16 hi + lo (A_hi B_hi + A_hi B_lo + A_lo B_hi,
+// ~2^-20 relative, fp32 accumulation), the codeword pairs coming straight
+// from a shared-memory LUT indexed by the packed code byte -- decoded values
+// never touch memory. The H_R combine is a 3-level butterfly over the lanes
+// holding the R slices; heads are summed in head order.
+//
+// Scores are fp32-class (tensor-core accumulation order) rather than the
+// bit-reproducible order of k1_higgs; selection parity vs kvlab is then
+// set-equality up to near-ties (SURVEY 7 hard part 1, contract (b)).
+// Fast path: d = 2, n = 16 (2-bit), group 1024, head_dim 128 (R = 8).
+
+#include "kvb_common.cuh"
+#include "kvb_internal.h"
+
+namespace kvb {
+
+namespace {
+
+constexpr int kR = 8;      // rows per group
+constexpr int kD = 128;    // head dim
+constexpr int kTileRows = 16;
+
+__device__ __forceinline__ void mma_f16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                        uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// W[b][h][k][d] = (H_128 (signs[k*128 + .] * qbar_h))[d]  (unnormalised FWHT,
+// same butterfly schedule as fwht_rows); one warp per (k, h, b).
+__global__ void k1h_prep(const float* __restrict__ q, const float* __restrict__ signs,
+                         float* __restrict__ W, int H, int G) {
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x, b = blockIdx.y;
+  __shared__ float xs[kR][kD];
+  const float* qb = q + (((size_t)b * H + h) * G) * kD;
+  for (int d = lane; d < kD; d += 32) {
+    float s = qb[d];
+    for (int g = 1; g < G; ++g) s = s + qb[(size_t)g * kD + d];
+    xs[k][d] = s * signs[k * kD + d];
+  }
+  __syncwarp();
+  for (int hh = 1; hh < kD; hh <<= 1) {
+    for (int p = lane; p < kD / 2; p += 32) {
+      const int i = (p / hh) * 2 * hh + (p % hh);
+      const float a = xs[k][i], c = xs[k][i + hh];
+      xs[k][i] = a + c;
+      xs[k][i + hh] = a - c;
+    }
+    __syncwarp();
+  }
+  for (int d = lane; d < kD; d += 32) W[(((size_t)b * H + h) * kR + k) * kD + d] = xs[k][d];
+}
+
+// One CTA per (slab of row tiles, sequence); warp w = head w. Codes are
+// packed 4-bit pairs: row r of head h = 32 bytes at codes[(b,h)][r*32].
+template <int HMAX>
+__global__ void __launch_bounds__(HMAX * 32) k1h_score(
+    const uint8_t* __restrict__ codes, const float* __restrict__ factors,
+    const float* __restrict__ W, const float* __restrict__ cb, float* __restrict__ scores,
+    int rows, int H, int ngroups, int gbytes, int tiles_per_cta) {
+  __shared__ uint4 lut[256];                 // byte -> (hi c0, hi c1, lo c0, lo c1)
+  __shared__ float part[HMAX][kTileRows];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g4 = lane >> 2, tig = lane & 3;
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int c0 = i & 15, c1 = i >> 4;
+    const float x0 = cb[2 * c0], y0 = cb[2 * c0 + 1];
+    const float x1 = cb[2 * c1], y1 = cb[2 * c1 + 1];
+    const __half2 h0 = __floats2half2_rn(x0, y0), h1 = __floats2half2_rn(x1, y1);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    lut[i] = make_uint4(h2u(h0), h2u(h1), h2u(__floats2half2_rn(x0 - f0.x, y0 - f0.y)),
+                        h2u(__floats2half2_rn(x1 - f1.x, y1 - f1.y)));
+  }
+  // B fragments: thread (g4, tig) owns w_{g4}[32*tig + 4*ks + 0..3], ks = 0..7
+  uint32_t bhi[8][2], blo[8][2];
+  const int h = warp;
+  if (h < H) {
+    const float* w = W + (((size_t)b * H + h) * kR + g4) * kD + 32 * tig;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const float4 v = *reinterpret_cast<const float4*>(w + 4 * ks);
+      const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      bhi[ks][0] = h2u(h01);
+      bhi[ks][1] = h2u(h23);
+      blo[ks][0] = h2u(__floats2half2_rn(v.x - f01.x, v.y - f01.y));
+      blo[ks][1] = h2u(__floats2half2_rn(v.z - f23.x, v.w - f23.y));
+    }
+  }
+  __syncthreads();
+  const int ntiles = (rows + kTileRows - 1) / kTileRows;
+  const int t_begin = blockIdx.x * tiles_per_cta;
+  const int t_end = min(ntiles, t_begin + tiles_per_cta);
+  const uint8_t* cbase = codes + ((size_t)b * H + (h < H ? h : 0)) * (size_t)ngroups * gbytes;
+  const float* fbase = factors + ((size_t)b * H + (h < H ? h : 0)) * ngroups;
+  // sign of H_8[k][a] for this lane's rows a = g4 and columns k = 2tig, 2tig+1
+  const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
+  const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
+  uint2 nxt0 = make_uint2(0, 0), nxt1 = make_uint2(0, 0);
+  auto load = [&](int t, uint2& r0, uint2& r1) {
+    const int row0 = t * kTileRows + g4;
+    const int row1 = row0 + 8;
+    r0 = row0 < rows ? *reinterpret_cast<const uint2*>(cbase + (size_t)row0 * 32 + 8 * tig)
+                     : make_uint2(0, 0);
+    r1 = row1 < rows ? *reinterpret_cast<const uint2*>(cbase + (size_t)row1 * 32 + 8 * tig)
+                     : make_uint2(0, 0);
+  };
+  if (h < H && t_begin < t_end) load(t_begin, nxt0, nxt1);
+  for (int t = t_begin; t < t_end; ++t) {
+    const uint2 cur0 = nxt0, cur1 = nxt1;
+    if (h < H && t + 1 < t_end) load(t + 1, nxt0, nxt1);
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    if (h < H) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t w0 = ks < 4 ? cur0.x : cur0.y;
+        const uint32_t w1 = ks < 4 ? cur1.x : cur1.y;
+        const uint4 e0 = lut[(w0 >> (8 * (ks & 3))) & 255u];
+        const uint4 e1 = lut[(w1 >> (8 * (ks & 3))) & 255u];
+        // a0 (row g4, code 16tig+2ks) a2 (row g4, code +1); a1/a3: row g4 + 8
+        mma_f16(c, e0.x, e1.x, e0.y, e1.y, bhi[ks][0], bhi[ks][1]);
+        mma_f16(c, e0.x, e1.x, e0.y, e1.y, blo[ks][0], blo[ks][1]);
+        mma_f16(c, e0.z, e1.z, e0.w, e1.w, bhi[ks][0], bhi[ks][1]);
+      }
+    }
+    // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)
+    float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] += __shfl_xor_sync(FULL, v[i], 4);
+      v[i] += __shfl_xor_sync(FULL, v[i], 8);
+      v[i] += __shfl_xor_sync(FULL, v[i], 16);
+    }
+    if (h < H && g4 == 0) {
+      const int gam0 = t * 2, gam1 = t * 2 + 1;  // groups of this tile
+      const float f0 = gam0 < ngroups ? fbase[gam0] * (1.0f / 32.0f) : 0.f;
+      const float f1 = gam1 < ngroups ? fbase[gam1] * (1.0f / 32.0f) : 0.f;
+      part[h][2 * tig] = v[0] * f0;
+      part[h][2 * tig + 1] = v[1] * f0;
+      part[h][8 + 2 * tig] = v[2] * f1;
+      part[h][8 + 2 * tig + 1] = v[3] * f1;
+    }
+    __syncthreads();
+    if (threadIdx.x < kTileRows) {
+      const int row = t * kTileRows + threadIdx.x;
+      if (row < rows) {
+        float s = part[0][threadIdx.x];
+        for (int hh = 1; hh < H; ++hh) s = s + part[hh][threadIdx.x];
+        scores[(size_t)b * rows + row] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+bool higgs_tc_supported(const kvb_store* s) {
+  const kvb_higgs_dev& h = s->lm_h;
+  return s->d.landmark_kind == KVB_LM_HIGGS && h.d == 2 && h.n == 16 && h.group == 1024 &&
+         s->d.head_dim == kD && s->d.kv_heads <= 8;
+}
+
+size_t higgs_tc_ws_bytes(const kvb_store* s) {
+  return (size_t)s->d.batch * s->d.kv_heads * kR * kD * sizeof(float) + 256;
+}
+
+cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, float* scores,
+                                  void* ws, cudaStream_t st) {
+  const kvb_higgs_dev& hd = s->lm_h;
+  const int B = s->d.batch, H = s->d.kv_heads;
+  float* W = static_cast<float*>(ws);
+  count_launch(2);
+  k1h_prep<<<dim3(H, B), kR * 32, 0, st>>>(q, hd.signs, W, H, G);
+  const int rows = s->C;
+  const int ntiles = (rows + kTileRows - 1) / kTileRows;
+  const int slots = sm_count() * resident_ctas((const void*)k1h_score<8>, 256, 0);
+  int ctas = slots / B;
+  if (ctas < 1) ctas = 1;
+  if (ctas > ntiles) ctas = ntiles;
+  const int per = (ntiles + ctas - 1) / ctas;
+  k1h_score<8><<<dim3((ntiles + per - 1) / per, B), 256, 0, st>>>(
+      hd.codes, hd.factor, W, hd.codebook, scores, rows, H, hd.groups, hd.group_bytes, per);
+  return cudaGetLastError();
+}
+
+}  // namespace kvb

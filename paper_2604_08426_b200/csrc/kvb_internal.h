@@ -58,10 +58,17 @@ int sm_count();
 int resident_ctas(const void* func, int threads, size_t smem);
 
 // ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
+// hist (may be null): [B][2048] uint32, zeroed by the caller; receives the
+// histogram of the top 11 bits of the score keys (sum aggregation only).
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, cudaStream_t st);
+                               float* scores, uint32_t* hist, cudaStream_t st);
+constexpr int kTopHistBins = 2048;
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);
+bool higgs_tc_supported(const kvb_store* s);
+size_t higgs_tc_ws_bytes(const kvb_store* s);
+cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, float* scores,
+                                  void* ws, cudaStream_t st);
 // Top-K + token union. mode 0: items are chunks (M = C); mode 1: items are
 // positions in cand_tok (M = per-sequence count m_count[b]).
 struct SelectLaunch {
@@ -79,6 +86,7 @@ struct SelectLaunch {
   int with_residents;
   int32_t* err_flag;        // device int, set on capacity overflow
   float* sel_scores = nullptr;  // [B][K] scores of the selected items (optional)
+  const uint32_t* hist = nullptr;  // [B][2048] top-11-bit key histogram from K1 (optional)
   int id_offset = 0;            // added to emitted item ids (sharding)
 };
 // Token union for an explicit chunk list (global ids, offset mapped).
@@ -112,6 +120,11 @@ struct AttendLaunch {
   void* ws;
 };
 size_t attend_ws_bytes(const kvb_store* s, int G, int cap);
+bool attend_wh_supported(const kvb_store* s, int G);
+int attend_wh_splits(const kvb_store* s, int cap);
+cudaError_t launch_attend_wh(const kvb_store* s, const float* q, int G, const int32_t* tok,
+                             const int32_t* ntok, int cap, const float* qt2, float* pm, float* pl,
+                             float* po, int splits, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
                                    int D, float* out, float* lse, cudaStream_t st);

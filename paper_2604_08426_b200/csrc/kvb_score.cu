@@ -44,14 +44,21 @@ __device__ __forceinline__ void load_qbar(const float* __restrict__ qb, int Hkv,
 // Lane l owns vectors v = l, l+32, l+64, ... of VW elements each; within a
 // vector elements are FMA'd in order; then warp_sum_butterfly.
 // ---------------------------------------------------------------------------
+// First radix level of K2 fused into the scan: a 2048-bin histogram of the
+// top 11 bits of every score key (kHistBits), per sequence.
+constexpr int kHistBins = 2048;
+
 template <typename T, int VW, int NV>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
-             int C, int Hkv, int G, int D) {
+             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist) {
   extern __shared__ float qbar[];
+  __shared__ uint32_t shist[kHistBins];
   const int E = Hkv * D;
   const int b = blockIdx.y;
   load_qbar(q + (size_t)b * Hkv * G * D, Hkv, G, D, qbar);
+  if (hist)
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) shist[i] = 0u;
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -114,8 +121,18 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
     a1 = warp_sum_butterfly(a1);
     if (lane == 0) {
       out[c] = a0;
-      if (two) out[c + 1] = a1;
+      if (hist) atomicAdd(&shist[score_key(a0) >> 21], 1u);
+      if (two) {
+        out[c + 1] = a1;
+        if (hist) atomicAdd(&shist[score_key(a1) >> 21], 1u);
+      }
     }
+  }
+  if (hist) {
+    __syncthreads();
+    uint32_t* gh = hist + (size_t)b * kHistBins;
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+      if (shist[i]) atomicAdd(gh + i, shist[i]);
   }
 }
 
@@ -123,7 +140,7 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
 template <typename T, int VW>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
-                  float* __restrict__ scores, int C, int Hkv, int G, int D) {
+                  float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist) {
   extern __shared__ float qbar[];
   const int E = Hkv * D;
   const int b = blockIdx.y;
@@ -147,7 +164,10 @@ k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
       }
     }
     a = warp_sum_butterfly(a);
-    if (lane == 0) scores[(size_t)b * C + c] = a;
+    if (lane == 0) {
+      scores[(size_t)b * C + c] = a;
+      if (hist) atomicAdd(hist + (size_t)b * kHistBins + (score_key(a) >> 21), 1u);
+    }
   }
 }
 
@@ -361,7 +381,7 @@ int score_grid_x(int C, int B, const void* func, size_t smem) {
 
 template <typename T>
 cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, int G,
-                               float* scores, cudaStream_t st) {
+                               float* scores, uint32_t* hist, cudaStream_t st) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim, E = s->E;
   constexpr int VWv = 16 / sizeof(T);
   const bool vec = (E % VWv) == 0;
@@ -381,7 +401,8 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   ensure_smem(fn, smem);
   dim3 grid(score_grid_x(C, B, fn, smem), B);
   count_launch();
-  void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D};
+  void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D,
+                  (void*)&hist};
   return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
 }
@@ -389,12 +410,12 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
 }  // namespace
 
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, cudaStream_t st) {
+                               float* scores, uint32_t* hist, cudaStream_t st) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim;
   if (agg == KVB_AGG_SUM) {
     if (s->d.kv_dtype == KVB_BF16)
-      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, st);
-    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, st);
+      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st);
+    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st);
   }
   const size_t smem = (size_t)H * G * D * sizeof(float);
   const void* fmax_fn = s->d.kv_dtype == KVB_BF16 ? (const void*)k1_dense_max<__nv_bfloat16>

@@ -15,6 +15,8 @@
 //     resident bitmap (n bits, shared memory) and compacted in ascending order
 //     by a block scan -- the sorted np.unique of the reference, with no sort.
 
+#include <algorithm>
+
 #include "kvb_common.cuh"
 #include "kvb_internal.h"
 
@@ -41,6 +43,8 @@ struct SelParams {
   const uint32_t* res_bitmap;
   int n, cs, W, P;
   int stage;  // keys staged in shared memory
+  const uint32_t* hist;
+  int cand_cap;
   float* sel_scores;
   int id_offset;
 };
@@ -133,63 +137,94 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   auto key_at = [&](int i) -> uint32_t { return p.stage ? ukeys[i] : score_key(__ldg(sc + i)); };
 
   // ---- 1. find T = K-th largest key and how many ties at T to take -----------
-  uint32_t T;
-  int krem, eqcnt;
-  constexpr int kRegItems = 32;  // register path when M <= 32 * 1024
-  uint32_t rk[kRegItems];
-  const bool regpath = M <= kRegItems * nthr;
-  if (regpath) {
-    // keys of ids i = r * nthr + tid, r < kRegItems, held in registers
-#pragma unroll
-    for (int r = 0; r < kRegItems; ++r) {
-      const int i = r * nthr + tid;
-      rk[r] = i < M ? key_at(i) : 0u;  // key 0 is below every finite score
+  uint32_t T = 0u;
+  int krem = 0, eqcnt = 0;
+  bool found = false;
+  if (p.hist) {
+    // (a) threshold bin from the top-11-bit histogram fused into K1
+    const uint32_t* hb = p.hist + (size_t)b * kTopHistBins;
+    const int b0 = kTopHistBins - 1 - 2 * tid;  // this thread: bins b0, b0-1 (descending)
+    const int c0 = tid < kTopHistBins / 2 ? (int)hb[b0] : 0;
+    const int c1 = tid < kTopHistBins / 2 ? (int)hb[b0 - 1] : 0;
+    int tot;
+    const int above = block_excl_scan(c0 + c1, red, &tot);
+    if (tid < kTopHistBins / 2 && above < K && K <= above + c0 + c1) {
+      if (K <= above + c0) {
+        s_digit = b0;
+        s_krem = K - above;
+        s_eq = c0;
+      } else {
+        s_digit = b0 - 1;
+        s_krem = K - above - c0;
+        s_eq = c1;
+      }
     }
-    // exact bisection over the 32-bit key space: largest T with
-    // #(key >= T) >= K; counts via redux.sync + one barrier per round
-    __shared__ int cntw[2][kSelThreads / 32];
-    uint32_t lo = 0u, hi = 0xffffffffu;
-    int round = 0;
-    while (lo < hi) {
-      const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
-      int c = 0;
-#pragma unroll
-      for (int r = 0; r < kRegItems; ++r) c += rk[r] >= mid ? 1 : 0;
-      c = __reduce_add_sync(FULL, c);
-      if (lane == 0) cntw[round & 1][warp] = c;
-      __syncthreads();
-      int tot = 0;
-#pragma unroll 8
-      for (int w = 0; w < kSelThreads / 32; ++w) tot += cntw[round & 1][w];
-      if (tot >= K) lo = mid; else hi = mid - 1u;
-      ++round;
-    }
-    T = lo;
-    int gt = 0, eq = 0;
-#pragma unroll
-    for (int r = 0; r < kRegItems; ++r) {
-      gt += rk[r] > T ? 1 : 0;
-      eq += rk[r] == T ? 1 : 0;
-    }
-    gt = __reduce_add_sync(FULL, gt);
-    eq = __reduce_add_sync(FULL, eq);
-    __shared__ int gtw[kSelThreads / 32], eqw[kSelThreads / 32];
-    if (lane == 0) {
-      gtw[warp] = gt;
-      eqw[warp] = eq;
-    }
+    if (tid == 0) s_cnt = 0;
     __syncthreads();
-    int gsum = 0, esum = 0;
-    for (int w = 0; w < kSelThreads / 32; ++w) {
-      gsum += gtw[w];
-      esum += eqw[w];
+    const uint32_t tb = (uint32_t)s_digit;
+    const int kb = s_krem;
+    const int nbin = s_eq;
+    // (b) candidates = keys in the threshold bin (their order does not matter)
+    uint32_t* cand = ukeys + (p.stage ? p.M_stride : 0);
+    if (nbin <= p.cand_cap) {
+      for (int base = warp * 32; base < M; base += nthr) {
+        const int i = base + lane;
+        const uint32_t u = i < M ? key_at(i) : 0u;
+        const bool in = i < M && (u >> 21) == tb;
+        const unsigned m = __ballot_sync(FULL, in);
+        int wb = 0;
+        if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+        wb = __shfl_sync(FULL, wb, 0);
+        if (in) cand[wb + __popc(m & ((1u << lane) - 1u))] = u;
+      }
+      __syncthreads();
+      // (c) exact bisection over the low 21 bits inside the bin
+      __shared__ int cntw[2][kSelThreads / 32];
+      uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
+      int round = 0;
+      while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+        int c = 0;
+        for (int i = tid; i < nbin; i += nthr) c += cand[i] >= mid ? 1 : 0;
+        c = __reduce_add_sync(FULL, c);
+        if (lane == 0) cntw[round & 1][warp] = c;
+        __syncthreads();
+        int t = 0;
+#pragma unroll 8
+        for (int w = 0; w < kSelThreads / 32; ++w) t += cntw[round & 1][w];
+        if (t >= kb) lo = mid; else hi = mid - 1u;
+        ++round;
+      }
+      T = lo;
+      int gt = 0, eq = 0;
+      for (int i = tid; i < nbin; i += nthr) {
+        gt += cand[i] > T ? 1 : 0;
+        eq += cand[i] == T ? 1 : 0;
+      }
+      gt = __reduce_add_sync(FULL, gt);
+      eq = __reduce_add_sync(FULL, eq);
+      __syncthreads();
+      if (lane == 0) {
+        cntw[0][warp] = gt;
+        cntw[1][warp] = eq;
+      }
+      __syncthreads();
+      int gs = 0, es = 0;
+      for (int w = 0; w < kSelThreads / 32; ++w) {
+        gs += cntw[0][w];
+        es += cntw[1][w];
+      }
+      krem = kb - gs;
+      eqcnt = es;
+      found = true;
+      __syncthreads();
     }
-    krem = K - gsum;
-    eqcnt = esum;
-  } else {
+  }
+  if (!found) {
   // ---- 1. radix select ----------------------------------------------------
     uint32_t prefix = 0u, pmask = 0u;
-    int krem = K, eqcnt = 0;
+    krem = K;
+    eqcnt = 0;
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
       for (int i = lane; i < 256; i += 32) whist[warp][i] = 0;
@@ -264,19 +299,7 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     else
       ids[pos] = i;
   };
-  if (regpath) {
-#pragma unroll
-    for (int r = 0; r < kRegItems; ++r) {
-      const int i = r * nthr + tid;
-      const uint32_t u = rk[r];
-      const bool take = i < M && (u > T || (all_ties && u == T));
-      const unsigned m = __ballot_sync(FULL, take);
-      int wb = 0;
-      if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
-      wb = __shfl_sync(FULL, wb, 0);
-      if (take) put(wb + __popc(m & ((1u << lane) - 1u)), u, i);
-    }
-  } else {
+  {
     for (int base = warp * 32; base < M; base += nthr) {
       const int i = base + lane;
       const bool valid = i < M;
@@ -376,6 +399,7 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
   p.with_residents = a.with_residents;
   p.err_flag = a.err_flag;
   p.sel_scores = a.sel_scores;
+  p.hist = (a.mode == 0 && !a.m_count) ? a.hist : nullptr;
   p.id_offset = a.id_offset;
   p.res_bitmap = s->res_bitmap;
   p.n = s->d.n_tokens;
@@ -386,6 +410,13 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
   size_t smem = sel + (a.token_ids ? (size_t)((s->W + 3) & ~3) * 4 : 0);
   p.stage = (smem + (size_t)a.M_stride * 4 <= 200 * 1024) ? 1 : 0;
   if (p.stage) smem += (size_t)a.M_stride * 4;
+  p.cand_cap = 0;
+  if (p.hist) {  // candidate buffer of the threshold bin
+    const size_t room = 220 * 1024 > smem ? 220 * 1024 - smem : 0;
+    p.cand_cap = (int)std::min<size_t>(room / 4, 16384);
+    if (p.cand_cap < 256) p.hist = nullptr;
+    else smem += (size_t)p.cand_cap * 4;
+  }
   ensure_smem((const void*)k2_select, smem);
   count_launch();
   k2_select<<<s->d.batch, kSelThreads, smem, st>>>(p);

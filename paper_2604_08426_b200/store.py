@@ -308,14 +308,15 @@ class DeviceStore:
         return out
 
     def select(self, q: torch.Tensor, n_select: int, aggregation: str = "sum",
-               rank_order: bool = True, want_scores: bool = True):
+               rank_order: bool = True, want_scores: bool = True, exact: bool = True):
         """select_by_landmarks (selection.py:72-87), batched. Returns
         (chunk_ids [B,K] int32, scores [B,C] f32 | None, token_ids [B,cap]
         int32, n_tokens [B] int32)."""
         G = self._check_q(q)
         cap = self.token_capacity(n_select)
         a = L.SelectArgs(G, n_select, L.KVB_AGG_SUM if aggregation == "sum" else
-                         (L.KVB_AGG_MAX if aggregation == "max" else -1), int(rank_order), cap)
+                         (L.KVB_AGG_MAX if aggregation == "max" else -1), int(rank_order), cap,
+                         int(exact))
         if aggregation not in ("sum", "max"):
             raise ValueError(f"unknown aggregation {aggregation!r}")
         chunk_ids = torch.empty((self.batch, n_select), dtype=torch.int32, device="cuda")
@@ -372,7 +373,7 @@ class DeviceStore:
     def decode_plan(self, G: int, n_select: int, k_path: int = 0):
         """Pre-sized arguments + buffers for repeated decode steps (graph-capturable)."""
         cap = self.token_capacity(n_select)
-        sa = L.SelectArgs(G, n_select, L.KVB_AGG_SUM, 0, cap)
+        sa = L.SelectArgs(G, n_select, L.KVB_AGG_SUM, 0, cap, 0)  # fastest scoring path
         aa = L.AttendArgs(G, cap, k_path)
         nb = self.lib.kvb_decode_workspace_bytes(self.h, C.byref(sa), C.byref(aa))
         return DecodePlan(self, sa, aa, nb)

@@ -162,3 +162,34 @@ def test_decode_step_matches_select_then_attend():
     o_ref, _ = dev.attend(q, tok, ntok)
     assert torch.equal(plan.ntok, ntok)
     assert torch.allclose(o_step, o_ref, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_higgs2_tensor_core_scores(seed):
+    """HIGGS 2-bit landmarks at chunk 1 (the paper's proposed selection):
+    the rotated-domain tensor-core scan (fast path, used by decode) agrees
+    with the bit-exact CUDA-core scan to fp32 accuracy, and selects the same
+    chunks up to exact near-ties."""
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    B, n = 2, 16384
+    rng = np.random.default_rng(100 + seed)
+    k = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
+    v = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
+    q = torch.from_numpy(rng.standard_normal((B, H, G, D)).astype(np.float32)).cuda()
+    dev = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=1,
+                      dtype=torch.bfloat16, landmark=S.scheme_higgs(2), outlier_tokens=64,
+                      local_window=32)
+    dev.build(k, v)
+    K = dev.n_select(256 / n)
+    c_ex, s_ex, t_ex, n_ex = dev.select(q, K, exact=True)
+    c_tc, s_tc, t_tc, n_tc = dev.select(q, K, exact=False)
+    se, st_ = s_ex.cpu().numpy().astype(np.float64), s_tc.cpu().numpy().astype(np.float64)
+    scale = np.abs(se).max()
+    assert np.abs(se - st_).max() < 2e-5 * scale, np.abs(se - st_).max() / scale
+    lm = dev.landmarks_dequantized().cpu().numpy()
+    for b in range(B):
+        s64 = np.einsum("hgd,chd->c", q[b].cpu().numpy().astype(np.float64), lm[b].astype(np.float64))
+        tol = 4e-5 * scale
+        compare_ranking(c_tc[b].cpu().numpy(), c_ex[b].cpu().numpy(), s64, tol, "tc vs exact")

@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [top]
+usage: [KVB_LIB=libkvb.so-as-profiled] python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [top]
 Reads the SASS source page of the report (per-instruction samples), maps
 instruction offsets to file:line with nvdisasm -g on libkvb.so's cubin.
 """
@@ -15,8 +15,8 @@ from collections import defaultdict
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                   "paper_2604_08426_b200", "libkvb.so")
+lib = os.environ.get("KVB_LIB") or os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2604_08426_b200", "libkvb.so")
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
