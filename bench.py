@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--budget", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--also", default="higgs2c1",
+                    help="comma-separated secondary variants reported under 'variants'")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N eager steps after setup (for ncu) and exit")
     return ap.parse_args()
@@ -287,24 +289,16 @@ def _ref_slice(i):
 
 
 # ---------------------------------------------------------------------------
-def main():
-    a = parse()
-    if a.impl == "reference":
-        run_reference(a)
-        return
+def measure(a, variant, rank, world, local, timed_breakdown=True):
+    """Build one variant's 32-layer state, time the decode step (CUDA graph),
+    the public-API end-to-end step and per-stage device time; free the state."""
     import torch
     import torch.distributed as dist
 
     from paper_2604_08426_b200 import _lib
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
-
+    a.variant = variant
     t_build = time.perf_counter()
     stores, (H, G, D) = build_layers(a, rank)
     t_build = time.perf_counter() - t_build
@@ -327,14 +321,12 @@ def main():
         for _ in range(a.profile_steps):
             step()
         torch.cuda.synchronize()
-        return
+        return None
 
-    # launches per step (counted on one eager step)
     c0 = lib.kvb_launch_count()
     step()
     torch.cuda.synchronize()
     launches_per_step = lib.kvb_launch_count() - c0
-
     graph = None
     if not a.no_graph:
         graph = torch.cuda.CUDAGraph()
@@ -342,7 +334,6 @@ def main():
             step()
         torch.cuda.synchronize()
     run = graph.replay if graph is not None else step
-
     for _ in range(a.warmup):
         run()
     torch.cuda.synchronize()
@@ -360,14 +351,12 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1) / a.steps
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ev0.elapsed_time(ev1) / a.steps], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * B / (ms_max / 1e3)
 
-    # ---- end to end through the public API with host buffers ---------------
+    # end to end through the public API with host buffers
     def e2e_step():
         q_dev.copy_(q_host, non_blocking=True)
         for l in range(L_):
@@ -388,14 +377,12 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - w0) * 1e3 / a.steps
-    e2e_ms = max(e0.elapsed_time(e1) / a.steps, wall_ms)
-    te = torch.tensor([e2e_ms], device="cuda")
+    te = torch.tensor([max(e0.elapsed_time(e1) / a.steps, wall_ms)], device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B / (float(te.item()) / 1e3)
+    e2e_ms = float(te.item())
 
-    # ---- per-stage device timing: one CUDA graph per stage over all layers,
-    # replayed between CUDA events on the launching stream ---------------------
+    # per-stage device time: one CUDA graph per stage over all layers
     st0 = stores[0]
     scores = [torch.empty((B, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
 
@@ -411,74 +398,128 @@ def main():
     def stage_ms(g, reps=10):
         g.replay()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
         for _ in range(reps):
             g.replay()
-        e1.record(stream)
+        s1.record(stream)
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / (reps * L_)
+        return s0.elapsed_time(s1) / (reps * L_)
 
-    g_score = stage_graph(lambda: [stores[l].score(q_dev[l], out=scores[l]) for l in range(L_)])
+    if variant == "shadowkv":
+        g_score = stage_graph(lambda: [stores[l].score(q_dev[l], out=scores[l]) for l in range(L_)])
+        k1_kernel = "k1_dense_sum (kvb_score_landmarks)"
+    else:
+        g_score = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
+        k1_kernel = "k1h_score + k2_select (kvb_select, HIGGS tensor-core scan)"
     g_select = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
     g_attend = stage_graph(lambda: [plans[l].attend_only(q_dev[l], out_dev[l]) for l in range(L_)])
     k1_ms = stage_ms(g_score)
     sel_ms = stage_ms(g_select)
     att_ms = stage_ms(g_attend)
-    hbm, peak_kind = peaks()
     ab = algorithmic_bytes(a, st0, G)
-    lm_key = "landmarks" if a.variant == "shadowkv" else "landmark_codes"
+    lm_key = "landmarks" if variant == "shadowkv" else "landmark_codes"
     k1_bytes = B * (ab[lm_key] + H * G * D * 4)
-    k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
     step_bytes = L_ * B * sum(ab.values())
-    step_gbs = step_bytes / (ms_max / 1e3) / 1e9
+    res = {
+        "variant": variant, "ms_per_step": ms_max, "value": world * B / (ms_max / 1e3),
+        "e2e_ms": e2e_ms, "e2e_value": world * B / (e2e_ms / 1e3),
+        "k1_ms": k1_ms, "sel_ms": sel_ms, "att_ms": att_ms, "k1_bytes": k1_bytes,
+        "k1_kernel": k1_kernel, "step_bytes": step_bytes, "per_layer_seq_bytes": ab,
+        "launches_per_step": launches_per_step, "K": K, "chunk": st0.cs, "graph": graph is not None,
+        "clocks": sampler.summary(), "build_s": t_build,
+        "h2d": q_host.numel() * 4, "d2h": out_host.numel() * 4,
+    }
+    for st in stores:
+        st.close()
+    del stores, plans, graph, g_score, g_select, g_attend
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
 
-    out = None
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    primary = a.variant
+    r = measure(a, primary, rank, world, local)
+    if r is None:
+        return
+    extra = {}
+    for v in [x for x in a.also.split(",") if x and x != primary]:
+        try:
+            rv = measure(a, v, rank, world, local)
+            hbm, _ = peaks()
+            extra[v] = {"value": round(rv["value"], 2), "unit": "tok/s",
+                        "ms_per_step": round(rv["ms_per_step"], 4),
+                        "e2e_value": round(rv["e2e_value"], 2),
+                        "workload": f"C2 {VARIANTS[v]}", "chunk": rv["chunk"], "K": rv["K"],
+                        "step_frac_of_hbm": round(rv["step_bytes"] / (rv["ms_per_step"] / 1e3) / 1e9 / hbm, 4),
+                        "breakdown_ms_per_layer": {"select": round(rv["sel_ms"], 5),
+                                                   "attend": round(rv["att_ms"], 5)},
+                        "per_layer_seq_bytes": rv["per_layer_seq_bytes"],
+                        "build_s": round(rv["build_s"], 1), "clocks": rv["clocks"]}
+        except Exception as exc:  # a secondary variant never loses the primary line
+            extra[v] = {"error": repr(exc)[:300]}
+        a.variant = primary
+    hbm, peak_kind = peaks()
+    k1_gbs = r["k1_bytes"] / (r["k1_ms"] / 1e3) / 1e9
+    step_gbs = r["step_bytes"] / (r["ms_per_step"] / 1e3) / 1e9
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu_baseline:
             try:
                 cpu = cpu_baseline(a)
-            except Exception as exc:  # never lose the GPU line over the baseline
+            except Exception as exc:
                 cpu = {"value": None, "error": repr(exc)}
-        clk = sampler.summary()
         out = {
-            "metric": METRIC, "value": round(value, 2), "unit": "tok/s", "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 4),
+            "metric": METRIC, "value": round(r["value"], 2), "unit": "tok/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(r["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.randn K/V per layer; random queries)",
-            "config": {"workload": f"C2 {VARIANTS[a.variant]}",
+            "config": {"workload": f"C2 {VARIANTS[primary]}",
                        "model": "Llama-3.1-8B shape (32 layers, 32 q / 8 kv heads, d 128)",
-                       "global_batch": world * B, "seq_len": a.ctx, "layers": L_,
-                       "chunk": st0.cs, "budget_tokens": a.budget, "selected_chunks": K,
+                       "global_batch": world * a.batch, "seq_len": a.ctx, "layers": a.layers,
+                       "chunk": r["chunk"], "budget_tokens": a.budget, "selected_chunks": r["K"],
                        "parallelism": f"dp{world} (replicas)",
-                       "l2": f"inputs exceed L2: {step_bytes / 1e9:.1f} GB algorithmic bytes per step",
-                       "cuda_graph": graph is not None},
-            "roofline": {"bound": "hbm", "kernel": "k1 landmark scan (kvb_score_landmarks)",
-                         "achieved": round(k1_gbs, 1), "peak": hbm, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": round(k1_gbs / hbm, 4),
-                         "algorithmic_bytes_per_launch": k1_bytes,
-                         "avg_launch_ms": round(k1_ms, 5), "traffic": None},
+                       "l2": f"inputs exceed L2: {r['step_bytes'] / 1e9:.1f} GB algorithmic bytes per step",
+                       "cuda_graph": r["graph"]},
+            "roofline": {"bound": "hbm", "kernel": r["k1_kernel"], "achieved": round(k1_gbs, 1),
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(k1_gbs / hbm, 4),
+                         "algorithmic_bytes_per_launch": r["k1_bytes"],
+                         "avg_launch_ms": round(r["k1_ms"], 5), "traffic": None},
             "step_roofline": {"achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s",
                               "frac": round(step_gbs / hbm, 4),
-                              "algorithmic_bytes_per_step": step_bytes,
-                              "per_layer_seq_bytes": ab},
-            "breakdown_ms_per_layer": {"k1_score": round(k1_ms, 5),
-                                       "select_incl_k1": round(sel_ms, 5),
-                                       "k2_topk_union": round(sel_ms - k1_ms, 5),
-                                       "attend_incl_fold_combine": round(att_ms, 5),
+                              "algorithmic_bytes_per_step": r["step_bytes"],
+                              "per_layer_seq_bytes": r["per_layer_seq_bytes"]},
+            "breakdown_ms_per_layer": {"k1_score": round(r["k1_ms"], 5),
+                                       "select_incl_k1": round(r["sel_ms"], 5),
+                                       "k2_topk_union": round(r["sel_ms"] - r["k1_ms"], 5),
+                                       "attend_incl_prep_merge": round(r["att_ms"], 5),
                                        "how": "per-stage CUDA graphs over all layers, CUDA events"},
-            "e2e": {"value": round(e2e_value, 2), "unit": "tok/s",
-                    "h2d_bytes_per_step": q_host.numel() * 4,
-                    "d2h_bytes_per_step": out_host.numel() * 4,
-                    "ms_per_step": round(float(te.item()), 4),
+            "e2e": {"value": round(r["e2e_value"], 2), "unit": "tok/s",
+                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                    "ms_per_step": round(r["e2e_ms"], 4),
                     "path": "pinned host q -> 32 x kvb_decode_step (C-ABI via ctypes) -> pinned host out"},
-            "gpu_launches": int(launches_per_step * a.steps),
-            "launches_per_step": int(launches_per_step),
+            "gpu_launches": int(r["launches_per_step"] * a.steps),
+            "launches_per_step": int(r["launches_per_step"]),
             "cpu_baseline": cpu,
-            "clocks": clk,
-            "build_s": round(t_build, 1),
+            "clocks": r["clocks"],
+            "build_s": round(r["build_s"], 1),
+            "variants": extra,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -47,7 +47,7 @@ struct WhParams {
   float* pm;                 // [B][splits][H*G]
   float* pl;
   float* po;                 // [B][splits][H*G][D]
-  int krow, vrow, stage_bytes, off_tok, off_warp;
+  int krow, vrow, stage_bytes, off_tok, off_ptr, off_warp;
 };
 
 __device__ __forceinline__ void cp16w(void* dst, const void* src) {
@@ -122,13 +122,28 @@ __global__ void __launch_bounds__(kWhWarps * 32, 1) k5_attend_wh(WhParams p) {
   const int cnt = max(0, min(Tb, t0 + per) - t0);
   int* tok_s = reinterpret_cast<int*>(sm + p.off_tok);
   int* slot_s = tok_s + p.max_per;
+  // per token: V row and key row (K row or factor row) base pointers, head 0
+  const unsigned char** vptr = reinterpret_cast<const unsigned char**>(sm + p.off_ptr);
+  const unsigned char** kptr = vptr + p.max_per;
   {
     const uint32_t* bm = p.res_bm + (size_t)b * p.W;
     const int32_t* pre = p.res_prefix + (size_t)b * p.W;
+    const size_t rowB = (size_t)H * kWhD * 2;
+    const size_t lrowB = SVD ? (size_t)p.sgroups * p.r * 2 : 0;
     for (int i = tid; i < cnt; i += blockDim.x) {
       const int t = p.tok[(size_t)b * p.cap + t0 + i];
+      const int slot = slot_of(bm, pre, t);
       tok_s[i] = t;
-      slot_s[i] = slot_of(bm, pre, t);
+      slot_s[i] = slot;
+      const unsigned char* rv = reinterpret_cast<const unsigned char*>(p.res_v);
+      const unsigned char* rk = reinterpret_cast<const unsigned char*>(p.res_k);
+      const unsigned char* ov = reinterpret_cast<const unsigned char*>(p.off_v);
+      const unsigned char* ok = reinterpret_cast<const unsigned char*>(p.off_k);
+      vptr[i] = slot >= 0 ? rv + ((size_t)b * p.Rcap + slot) * rowB : ov + ((size_t)b * p.n + t) * rowB;
+      if (!SVD || slot >= 0)
+        kptr[i] = slot >= 0 ? rk + ((size_t)b * p.Rcap + slot) * rowB : ok + ((size_t)b * p.n + t) * rowB;
+      else
+        kptr[i] = reinterpret_cast<const unsigned char*>(p.left) + ((size_t)b * p.n + t) * lrowB;
     }
   }
   __syncthreads();
@@ -137,7 +152,6 @@ __global__ void __launch_bounds__(kWhWarps * 32, 1) k5_attend_wh(WhParams p) {
 
   unsigned char* wbuf = sm + p.off_warp + (size_t)warp * 2 * p.stage_bytes;
   const int hgrp = SVD ? h / (H / p.sgroups) : 0;
-  const size_t rowE = (size_t)H * kWhD;  // elements per K/V row
 
   // ---- A fragments of the query side (rows = g, zero for g >= G) ----------------
   // exact keys: q_h split in 3 bf16 parts over k-steps of d. Kept in registers
@@ -180,26 +194,24 @@ __global__ void __launch_bounds__(kWhWarps * 32, 1) k5_attend_wh(WhParams p) {
 
   // ---- staging of one sub-tile into a warp-private buffer ------------------------
   const int lbytes_h = SVD ? p.r * 2 : 0;  // this head's factor slice
+  const int lchunks = SVD ? p.r * 2 / 16 : 0;      // 16-byte chunks of a factor slice
+  const size_t hoffV = (size_t)h * kWhD * 2;        // head offset inside a K/V row
+  const size_t hoffL = (size_t)hgrp * lbytes_h;     // group offset inside a factor row
   auto stage = [&](int i0, int ns, unsigned char* buf) {
     unsigned char* kb = buf;
     unsigned char* vb = buf + kWhTT * p.krow;
+    const int c = lane & 15;
+    // V slices: two tokens per instruction, 16 lanes x 16 B = one 256-B slice
+    for (int j2 = 0; j2 < ns; j2 += 2) {
+      const int j = j2 + (lane >> 4);
+      if (j < ns) cp16w(vb + j * p.vrow + c * 16, vptr[i0 + j] + hoffV + c * 16);
+    }
+    // key slices: bf16 K slice (16 chunks) or fp16 factor slice (lchunks)
     for (int j = 0; j < ns; ++j) {
-      const int slot = slot_s[i0 + j];
-      const size_t tk = (size_t)tok_s[i0 + j];
-      const bool exact = !SVD || slot >= 0;
-      const __nv_bfloat16* vsrc = (slot >= 0 ? p.res_v + ((size_t)b * p.Rcap + slot) * rowE
-                                             : p.off_v + ((size_t)b * p.n + tk) * rowE) + h * kWhD;
-      if (lane < 16) cp16w(vb + j * p.vrow + lane * 16, vsrc + lane * 8);
-      if (exact) {
-        const __nv_bfloat16* ksrc = (slot >= 0 ? p.res_k + ((size_t)b * p.Rcap + slot) * rowE
-                                               : p.off_k + ((size_t)b * p.n + tk) * rowE) + h * kWhD;
-        if (lane >= 16) cp16w(kb + j * p.krow + (lane - 16) * 16, ksrc + (lane - 16) * 8);
-      } else {
-        const unsigned char* lsrc = reinterpret_cast<const unsigned char*>(p.left) +
-                                    (((size_t)b * p.n + tk) * p.sgroups + hgrp) * lbytes_h;
-        for (int c = lane - 16; c >= 0 && c < lbytes_h / 16; c += 16)
-          cp16w(kb + j * p.krow + c * 16, lsrc + c * 16);
-      }
+      const bool exact = !SVD || slot_s[i0 + j] >= 0;
+      const int kc = exact ? 16 : lchunks;
+      const unsigned char* src = kptr[i0 + j] + (exact ? hoffV : hoffL);
+      if (lane < kc) cp16w(kb + j * p.krow + lane * 16, src + lane * 16);
     }
   };
 
@@ -457,7 +469,8 @@ cudaError_t launch_attend_wh(const kvb_store* s, const float* q, int G, const in
   p.stage_bytes = (kWhTT * (krow + vrow) + 127) & ~127;
   p.max_per = (cap + splits - 1) / splits;
   p.off_tok = 0;
-  p.off_warp = (2 * p.max_per * 4 + 127) & ~127;
+  p.off_ptr = (2 * p.max_per * 4 + 15) & ~15;
+  p.off_warp = (p.off_ptr + 2 * p.max_per * 8 + 127) & ~127;
   const size_t smem = (size_t)p.off_warp + (size_t)kWhWarps * 2 * p.stage_bytes;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   count_launch(2);

@@ -178,46 +178,37 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
         if (in) cand[wb + __popc(m & ((1u << lane) - 1u))] = u;
       }
       __syncthreads();
-      // (c) exact bisection over the low 21 bits inside the bin
-      __shared__ int cntw[2][kSelThreads / 32];
-      uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
-      int round = 0;
-      while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-        int c = 0;
-        for (int i = tid; i < nbin; i += nthr) c += cand[i] >= mid ? 1 : 0;
-        c = __reduce_add_sync(FULL, c);
-        if (lane == 0) cntw[round & 1][warp] = c;
-        __syncthreads();
-        int t = 0;
-#pragma unroll 8
-        for (int w = 0; w < kSelThreads / 32; ++w) t += cntw[round & 1][w];
-        if (t >= kb) lo = mid; else hi = mid - 1u;
-        ++round;
-      }
-      T = lo;
-      int gt = 0, eq = 0;
-      for (int i = tid; i < nbin; i += nthr) {
-        gt += cand[i] > T ? 1 : 0;
-        eq += cand[i] == T ? 1 : 0;
-      }
-      gt = __reduce_add_sync(FULL, gt);
-      eq = __reduce_add_sync(FULL, eq);
-      __syncthreads();
-      if (lane == 0) {
-        cntw[0][warp] = gt;
-        cntw[1][warp] = eq;
+      // (c) exact bisection over the low 21 bits inside the bin -- the bin
+      // holds few keys, so one warp does it without block barriers
+      __shared__ uint32_t s_T;
+      __shared__ int s_gt, s_eqc;
+      if (warp == 0) {
+        uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
+        while (lo < hi) {
+          const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+          int c = 0;
+          for (int i = lane; i < nbin; i += 32) c += cand[i] >= mid ? 1 : 0;
+          c = __reduce_add_sync(FULL, c);
+          if (c >= kb) lo = mid; else hi = mid - 1u;
+        }
+        int gt = 0, eq = 0;
+        for (int i = lane; i < nbin; i += 32) {
+          gt += cand[i] > lo ? 1 : 0;
+          eq += cand[i] == lo ? 1 : 0;
+        }
+        gt = __reduce_add_sync(FULL, gt);
+        eq = __reduce_add_sync(FULL, eq);
+        if (lane == 0) {
+          s_T = lo;
+          s_gt = gt;
+          s_eqc = eq;
+        }
       }
       __syncthreads();
-      int gs = 0, es = 0;
-      for (int w = 0; w < kSelThreads / 32; ++w) {
-        gs += cntw[0][w];
-        es += cntw[1][w];
-      }
-      krem = kb - gs;
-      eqcnt = es;
+      T = s_T;
+      krem = kb - s_gt;
+      eqcnt = s_eqc;
       found = true;
-      __syncthreads();
     }
   }
   if (!found) {
