@@ -38,8 +38,9 @@ HBM_FALLBACK = 6650.0
 
 VARIANTS = {
     # name: (description, landmark, chunk, slow, budget tokens, outliers, local)
-    "shadowkv": "ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
-    "higgs2c1": "paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
+    "shadowkv": "C2 ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
+    "higgs2c1": "C2 paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
+    "shadowkv_host": "C3 ShadowKV with V offloaded to pinned, device-mapped host memory (zero-copy gather over the host link)",
 }
 
 
@@ -139,11 +140,12 @@ def build_layers(a, rank):
         shape = (a.batch, a.ctx, H, D)
         k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
         v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
-        if a.variant == "shadowkv":
+        if a.variant in ("shadowkv", "shadowkv_host"):
             st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
                              dtype=torch.bfloat16, landmark=S.scheme_none(),
                              slow=S.scheme_svd(160, H * D), svd_groups=1,
-                             outlier_tokens=384, local_window=32)
+                             outlier_tokens=384, local_window=32,
+                             offload="host" if a.variant == "shadowkv_host" else "hbm")
         else:
             st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=1,
                              dtype=torch.bfloat16, landmark=S.scheme_higgs(2),
@@ -155,6 +157,27 @@ def build_layers(a, rank):
     return stores, (H, G, D)
 
 
+def host_link_gbs(nbytes=1 << 30):
+    """Pinned host -> device copy bandwidth (the host-link roofline)."""
+    import torch
+
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        d.copy_(h, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    gbs = 5 * nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del h, d
+    return gbs
+
+
 def algorithmic_bytes(a, st, G):
     """Per (layer, sequence) bytes the step must move, bf16."""
     H, D, n = st.heads, st.dim, st.n
@@ -163,7 +186,7 @@ def algorithmic_bytes(a, st, G):
     S_tok = K * st.cs
     R = st.max_resident
     q = H * G * D * 4 + H * G * D * 4  # queries in, output out
-    if a.variant == "shadowkv":
+    if a.variant in ("shadowkv", "shadowkv_host"):
         lm = st.C * E * 2
         r = st.slow.rank
         return {"landmarks": lm, "left_rows": S_tok * r * 2, "right": r * E * 2,
@@ -185,7 +208,7 @@ def oracle_slice(a, seed=0):
     rng = np.random.default_rng(seed)
     k = rng.standard_normal((H, n, D), dtype=np.float32)
     v = rng.standard_normal((H, n, D), dtype=np.float32)
-    if a.variant == "shadowkv":
+    if a.variant != "higgs2c1":
         cs = 8
         lm = np.stack([P.chunk_means(k[h], cs) for h in range(H)])
         outl = P.outlier_chunks(k, lm, cs, 384)
@@ -259,7 +282,7 @@ def run_reference(a):
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(ms_full_step, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"C2 {VARIANTS[a.variant]}", "layers": a.layers,
+            "config": {"workload": VARIANTS[a.variant], "layers": a.layers,
                        "batch": a.batch, "ctx": a.ctx, "budget_tokens": a.budget},
             "cpu_baseline": {"value": round(tok_s, 4), "unit": "tok/s", "cores": workers,
                              "kind": "port",
@@ -407,7 +430,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         torch.cuda.synchronize()
         return s0.elapsed_time(s1) / (reps * L_)
 
-    if variant == "shadowkv":
+    if variant in ("shadowkv", "shadowkv_host"):
         g_score = stage_graph(lambda: [stores[l].score(q_dev[l], out=scores[l]) for l in range(L_)])
         k1_kernel = "k1_dense_sum (kvb_score_landmarks)"
     else:
@@ -419,7 +442,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     sel_ms = stage_ms(g_select)
     att_ms = stage_ms(g_attend)
     ab = algorithmic_bytes(a, st0, G)
-    lm_key = "landmarks" if variant == "shadowkv" else "landmark_codes"
+    lm_key = "landmarks" if variant != "higgs2c1" else "landmark_codes"
     k1_bytes = B * (ab[lm_key] + H * G * D * 4)
     step_bytes = L_ * B * sum(ab.values())
     res = {
@@ -465,7 +488,7 @@ def main():
             extra[v] = {"value": round(rv["value"], 2), "unit": "tok/s",
                         "ms_per_step": round(rv["ms_per_step"], 4),
                         "e2e_value": round(rv["e2e_value"], 2),
-                        "workload": f"C2 {VARIANTS[v]}", "chunk": rv["chunk"], "K": rv["K"],
+                        "workload": VARIANTS[v], "chunk": rv["chunk"], "K": rv["K"],
                         "step_frac_of_hbm": round(rv["step_bytes"] / (rv["ms_per_step"] / 1e3) / 1e9 / hbm, 4),
                         "breakdown_ms_per_layer": {"select": round(rv["sel_ms"], 5),
                                                    "attend": round(rv["att_ms"], 5)},
@@ -475,6 +498,14 @@ def main():
             extra[v] = {"error": repr(exc)[:300]}
         a.variant = primary
     hbm, peak_kind = peaks()
+    host_link = None
+    if primary == "shadowkv_host":
+        link = host_link_gbs()
+        vb = r["per_layer_seq_bytes"]["values"] * a.layers * a.batch
+        host_link = {"measured_h2d_gbs": round(link, 1),
+                     "host_bytes_per_step": vb,
+                     "achieved_gbs": round(vb / (r["ms_per_step"] / 1e3) / 1e9, 1),
+                     "frac": round(vb / (r["ms_per_step"] / 1e3) / 1e9 / link, 4)}
     k1_gbs = r["k1_bytes"] / (r["k1_ms"] / 1e3) / 1e9
     step_gbs = r["step_bytes"] / (r["ms_per_step"] / 1e3) / 1e9
     if rank == 0:
@@ -489,7 +520,7 @@ def main():
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(r["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.randn K/V per layer; random queries)",
-            "config": {"workload": f"C2 {VARIANTS[primary]}",
+            "config": {"workload": VARIANTS[primary],
                        "model": "Llama-3.1-8B shape (32 layers, 32 q / 8 kv heads, d 128)",
                        "global_batch": world * a.batch, "seq_len": a.ctx, "layers": a.layers,
                        "chunk": r["chunk"], "budget_tokens": a.budget, "selected_chunks": r["K"],
@@ -521,6 +552,8 @@ def main():
             "build_s": round(r["build_s"], 1),
             "variants": extra,
         }
+        if host_link:
+            out["host_link_roofline"] = host_link
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
