@@ -557,11 +557,13 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
   int32_t* err = cv.take<int32_t>(1);
   void* tcws = cv.take<char>(higgs_tc_ws_bytes(s));
   uint32_t* hist = cv.take<uint32_t>((size_t)s->d.batch * kTopHistBins);
-  const bool use_hist = s->d.landmark_kind == KVB_LM_DENSE && a->aggregation == KVB_AGG_SUM;
+  const bool use_tc = !a->exact_scores && a->aggregation == KVB_AGG_SUM && higgs_tc_supported(s);
+  const bool use_hist = a->aggregation == KVB_AGG_SUM &&
+                        (s->d.landmark_kind == KVB_LM_DENSE || use_tc);
   if (use_hist)
     KVB_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
-  if (!a->exact_scores && a->aggregation == KVB_AGG_SUM && higgs_tc_supported(s)) {
-    KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, sc, tcws, st),
+  if (use_tc) {
+    KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, sc, tcws, hist, st),
              "HIGGS tensor-core scoring");
   } else if ((ks = score_landmarks(s, q, a->queries_per_head, a->aggregation, sc, st,
                                    use_hist ? hist : nullptr)) != KVB_OK) {

@@ -32,6 +32,7 @@ namespace {
 constexpr int kR = 8;      // rows per group
 constexpr int kD = 128;    // head dim
 constexpr int kTileRows = 16;
+constexpr int kTPI = 4;      // tiles per iteration (64 landmark rows)
 
 __device__ __forceinline__ void mma_f16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
                                         uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -76,9 +77,12 @@ template <int HMAX>
 __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     const uint8_t* __restrict__ codes, const float* __restrict__ factors,
     const float* __restrict__ W, const float* __restrict__ cb, float* __restrict__ scores,
-    int rows, int H, int ngroups, int gbytes, int tiles_per_cta) {
+    int rows, int H, int ngroups, int gbytes, int tiles_per_cta, uint32_t* __restrict__ hist) {
   __shared__ uint4 lut[256];                 // byte -> (hi c0, hi c1, lo c0, lo c1)
-  __shared__ float part[HMAX][kTileRows];
+  __shared__ float part[HMAX][kTPI * kTileRows];
+  __shared__ uint32_t shist[kTopHistBins];   // first radix level of K2 (see k1_dense_sum)
+  if (hist)
+    for (int i = threadIdx.x; i < kTopHistBins; i += blockDim.x) shist[i] = 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y;
@@ -116,60 +120,81 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   // sign of H_8[k][a] for this lane's rows a = g4 and columns k = 2tig, 2tig+1
   const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
   const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
-  uint2 nxt0 = make_uint2(0, 0), nxt1 = make_uint2(0, 0);
-  auto load = [&](int t, uint2& r0, uint2& r1) {
-    const int row0 = t * kTileRows + g4;
-    const int row1 = row0 + 8;
-    r0 = row0 < rows ? *reinterpret_cast<const uint2*>(cbase + (size_t)row0 * 32 + 8 * tig)
-                     : make_uint2(0, 0);
-    r1 = row1 < rows ? *reinterpret_cast<const uint2*>(cbase + (size_t)row1 * 32 + 8 * tig)
-                     : make_uint2(0, 0);
-  };
-  if (h < H && t_begin < t_end) load(t_begin, nxt0, nxt1);
-  for (int t = t_begin; t < t_end; ++t) {
-    const uint2 cur0 = nxt0, cur1 = nxt1;
-    if (h < H && t + 1 < t_end) load(t + 1, nxt0, nxt1);
-    float c[4] = {0.f, 0.f, 0.f, 0.f};
-    if (h < H) {
+  // kTPI tiles per iteration, the next kTPI prefetched into registers
+  uint2 nxt[kTPI][2];
+  auto load = [&](int t0) {
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint32_t w0 = ks < 4 ? cur0.x : cur0.y;
-        const uint32_t w1 = ks < 4 ? cur1.x : cur1.y;
-        const uint4 e0 = lut[(w0 >> (8 * (ks & 3))) & 255u];
-        const uint4 e1 = lut[(w1 >> (8 * (ks & 3))) & 255u];
-        // a0 (row g4, code 16tig+2ks) a2 (row g4, code +1); a1/a3: row g4 + 8
-        mma_f16(c, e0.x, e1.x, e0.y, e1.y, bhi[ks][0], bhi[ks][1]);
-        mma_f16(c, e0.x, e1.x, e0.y, e1.y, blo[ks][0], blo[ks][1]);
-        mma_f16(c, e0.z, e1.z, e0.w, e1.w, bhi[ks][0], bhi[ks][1]);
+    for (int u = 0; u < kTPI; ++u) {
+      const int row0 = (t0 + u) * kTileRows + g4;
+      const int row1 = row0 + 8;
+      nxt[u][0] = (h < H && t0 + u < t_end && row0 < rows)
+                      ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row0 * 32 + 8 * tig))
+                      : make_uint2(0, 0);
+      nxt[u][1] = (h < H && t0 + u < t_end && row1 < rows)
+                      ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row1 * 32 + 8 * tig))
+                      : make_uint2(0, 0);
+    }
+  };
+  load(t_begin);
+  for (int t = t_begin; t < t_end; t += kTPI) {
+    uint2 cur[kTPI][2];
+#pragma unroll
+    for (int u = 0; u < kTPI; ++u) {
+      cur[u][0] = nxt[u][0];
+      cur[u][1] = nxt[u][1];
+    }
+    load(t + kTPI);
+#pragma unroll
+    for (int u = 0; u < kTPI; ++u) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      if (h < H) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t w0 = ks < 4 ? cur[u][0].x : cur[u][0].y;
+          const uint32_t w1 = ks < 4 ? cur[u][1].x : cur[u][1].y;
+          const uint4 e0 = lut[(w0 >> (8 * (ks & 3))) & 255u];
+          const uint4 e1 = lut[(w1 >> (8 * (ks & 3))) & 255u];
+          // a0 (row g4, code 16tig+2ks) a2 (row g4, code +1); a1/a3: row g4 + 8
+          mma_f16(c, e0.x, e1.x, e0.y, e1.y, bhi[ks][0], bhi[ks][1]);
+          mma_f16(c, e0.x, e1.x, e0.y, e1.y, blo[ks][0], blo[ks][1]);
+          mma_f16(c, e0.z, e1.z, e0.w, e1.w, bhi[ks][0], bhi[ks][1]);
+        }
+      }
+      // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)
+      float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] += __shfl_xor_sync(FULL, v[i], 4);
+        v[i] += __shfl_xor_sync(FULL, v[i], 8);
+        v[i] += __shfl_xor_sync(FULL, v[i], 16);
+      }
+      if (h < H && g4 == 0) {
+        const int gam0 = (t + u) * 2, gam1 = gam0 + 1;  // groups of this tile
+        const float f0 = gam0 < ngroups ? __ldg(fbase + gam0) * (1.0f / 32.0f) : 0.f;
+        const float f1 = gam1 < ngroups ? __ldg(fbase + gam1) * (1.0f / 32.0f) : 0.f;
+        float* pr = part[h] + u * kTileRows;
+        pr[2 * tig] = v[0] * f0;
+        pr[2 * tig + 1] = v[1] * f0;
+        pr[8 + 2 * tig] = v[2] * f1;
+        pr[8 + 2 * tig + 1] = v[3] * f1;
       }
     }
-    // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)
-    float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v[i] += __shfl_xor_sync(FULL, v[i], 4);
-      v[i] += __shfl_xor_sync(FULL, v[i], 8);
-      v[i] += __shfl_xor_sync(FULL, v[i], 16);
-    }
-    if (h < H && g4 == 0) {
-      const int gam0 = t * 2, gam1 = t * 2 + 1;  // groups of this tile
-      const float f0 = gam0 < ngroups ? fbase[gam0] * (1.0f / 32.0f) : 0.f;
-      const float f1 = gam1 < ngroups ? fbase[gam1] * (1.0f / 32.0f) : 0.f;
-      part[h][2 * tig] = v[0] * f0;
-      part[h][2 * tig + 1] = v[1] * f0;
-      part[h][8 + 2 * tig] = v[2] * f1;
-      part[h][8 + 2 * tig + 1] = v[3] * f1;
-    }
     __syncthreads();
-    if (threadIdx.x < kTileRows) {
+    if (threadIdx.x < kTPI * kTileRows) {
       const int row = t * kTileRows + threadIdx.x;
-      if (row < rows) {
+      if (row < rows && t * kTileRows + threadIdx.x < t_end * kTileRows) {
         float s = part[0][threadIdx.x];
         for (int hh = 1; hh < H; ++hh) s = s + part[hh][threadIdx.x];
         scores[(size_t)b * rows + row] = s;
+        if (hist) atomicAdd(&shist[score_key(s) >> 21], 1u);
       }
     }
     __syncthreads();
+  }
+  if (hist) {
+    uint32_t* gh = hist + (size_t)b * kTopHistBins;
+    for (int i = threadIdx.x; i < kTopHistBins; i += blockDim.x)
+      if (shist[i]) atomicAdd(gh + i, shist[i]);
   }
 }
 
@@ -186,7 +211,7 @@ size_t higgs_tc_ws_bytes(const kvb_store* s) {
 }
 
 cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, float* scores,
-                                  void* ws, cudaStream_t st) {
+                                  void* ws, uint32_t* hist, cudaStream_t st) {
   const kvb_higgs_dev& hd = s->lm_h;
   const int B = s->d.batch, H = s->d.kv_heads;
   float* W = static_cast<float*>(ws);
@@ -200,7 +225,7 @@ cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, flo
   if (ctas > ntiles) ctas = ntiles;
   const int per = (ntiles + ctas - 1) / ctas;
   k1h_score<8><<<dim3((ntiles + per - 1) / per, B), 256, 0, st>>>(
-      hd.codes, hd.factor, W, hd.codebook, scores, rows, H, hd.groups, hd.group_bytes, per);
+      hd.codes, hd.factor, W, hd.codebook, scores, rows, H, hd.groups, hd.group_bytes, per, hist);
   return cudaGetLastError();
 }
 

@@ -68,7 +68,7 @@ cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int ag
 bool higgs_tc_supported(const kvb_store* s);
 size_t higgs_tc_ws_bytes(const kvb_store* s);
 cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, float* scores,
-                                  void* ws, cudaStream_t st);
+                                  void* ws, uint32_t* hist, cudaStream_t st);
 // Top-K + token union. mode 0: items are chunks (M = C); mode 1: items are
 // positions in cand_tok (M = per-sequence count m_count[b]).
 struct SelectLaunch {

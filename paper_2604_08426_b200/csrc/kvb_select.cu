@@ -167,15 +167,23 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     // (b) candidates = keys in the threshold bin (their order does not matter)
     uint32_t* cand = ukeys + (p.stage ? p.M_stride : 0);
     if (nbin <= p.cand_cap) {
-      for (int base = warp * 32; base < M; base += nthr) {
-        const int i = base + lane;
-        const uint32_t u = i < M ? key_at(i) : 0u;
-        const bool in = i < M && (u >> 21) == tb;
-        const unsigned m = __ballot_sync(FULL, in);
-        int wb = 0;
-        if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
-        wb = __shfl_sync(FULL, wb, 0);
-        if (in) cand[wb + __popc(m & ((1u << lane) - 1u))] = u;
+      for (int base = warp * 128; base < M; base += nthr * 4) {
+        uint32_t u4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = base + 32 * k + lane;
+          u4[k] = i < M ? key_at(i) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = base + 32 * k + lane;
+          const bool in = i < M && (u4[k] >> 21) == tb;
+          const unsigned m = __ballot_sync(FULL, in);
+          int wb = 0;
+          if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+          wb = __shfl_sync(FULL, wb, 0);
+          if (in) cand[wb + __popc(m & ((1u << lane) - 1u))] = u4[k];
+        }
       }
       __syncthreads();
       // (c) exact bisection over the low 21 bits inside the bin -- the bin
@@ -290,12 +298,18 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
     else
       ids[pos] = i;
   };
-  {
-    for (int base = warp * 32; base < M; base += nthr) {
-      const int i = base + lane;
-      const bool valid = i < M;
-      const uint32_t u = valid ? key_at(i) : 0u;
-      const bool take = valid && (u > T || (all_ties && u == T));
+  for (int base = warp * 128; base < M; base += nthr * 4) {
+    uint32_t u4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + 32 * k + lane;
+      u4[k] = i < M ? key_at(i) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + 32 * k + lane;
+      const uint32_t u = u4[k];
+      const bool take = i < M && (u > T || (all_ties && u == T));
       const unsigned m = __ballot_sync(FULL, take);
       int wb = 0;
       if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
