@@ -149,6 +149,9 @@ void free_higgs(kvb_higgs_dev& h) {
 }
 
 void free_store(kvb_store* s) {
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->side) cudaStreamDestroy(s->side);
   cudaFree(s->lm_dense);
   free_higgs(s->lm_h);
   free_higgs(s->res_h);
@@ -196,8 +199,12 @@ kvb_status check_queries(const kvb_store* s, int G) {
   return KVB_OK;
 }
 
-kvb_status check_ready_landmarks(const kvb_store* s) {
-  (void)s;
+kvb_status check_attend_shape(const kvb_store* s) {
+  if (s->d.kv_heads > 8 || s->d.head_dim > 128 || (s->d.head_dim & 1))
+    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel supports kv_heads <= 8, even head_dim <= 128");
+  if (s->d.slow_kind == KVB_SLOW_SVD &&
+      ((s->d.svd_rank & 1) || s->d.svd_rank * s->d.svd_groups > 256))
+    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel needs an even SVD rank, groups*rank <= 256");
   return KVB_OK;
 }
 
@@ -672,11 +679,7 @@ kvb_status kvb_attend(kvb_store* s, const float* q, const kvb_attend_args* a,
   kvb_status ks = check_queries(s, a->queries_per_head);
   if (ks != KVB_OK) return ks;
   if (a->token_capacity < 1) KVB_FAIL(KVB_EINVAL, "token_capacity must be >= 1");
-  if (s->d.kv_heads > 8 || s->d.head_dim > 128 || (s->d.head_dim & 1))
-    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel supports kv_heads <= 8, even head_dim <= 128");
-  if (s->d.slow_kind == KVB_SLOW_SVD &&
-      ((s->d.svd_rank & 1) || s->d.svd_rank * s->d.svd_groups > 256))
-    KVB_FAIL(KVB_EUNSUPPORTED, "attention kernel needs an even SVD rank, groups*rank <= 256");
+  if ((ks = check_attend_shape(s)) != KVB_OK) return ks;
   if (s->d.slow_kind == KVB_SLOW_SVD && a->k_path == 2)
     KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
   if (!ws || ws_bytes < kvb_attend_workspace_bytes(s, a)) KVB_FAIL(KVB_EINVAL, "workspace too small");
@@ -719,9 +722,39 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   void* aws = cv.take<char>((size_t)ab);
   kvb_select_args a2 = *sel;
   a2.rank_order = 0;
+  if ((ks = check_queries(s, att->queries_per_head)) != KVB_OK) return ks;
+  if ((ks = check_attend_shape(s)) != KVB_OK) return ks;
+  if (att->queries_per_head != sel->queries_per_head) KVB_FAIL(KVB_EINVAL, "G mismatch");
+  if (s->d.slow_kind == KVB_SLOW_SVD && att->k_path == 2)
+    KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
+  // fork: per-step query prep (q transpose, q~ = right.q) on the side stream,
+  // overlapping the landmark scan and top-K on the caller's stream; join
+  // before the attention. Capturable into CUDA graphs as a parallel branch.
+  cudaStream_t st = as_stream(stream);
+  if (!s->side) {
+    KVB_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "side stream");
+    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming), "fork event");
+    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming), "join event");
+  }
+  AttendLaunch L{};
+  L.q = q;
+  L.G = att->queries_per_head;
+  L.token_ids = token_ids;
+  L.n_tokens = n_tokens;
+  L.cap = att->token_capacity;
+  L.out = out;
+  L.lse = lse;
+  L.k_path = att->k_path;
+  L.ws = aws;
+  KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
+  KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
+  KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
+  KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
   if ((ks = kvb_select(s, q, &a2, cid, nullptr, token_ids, n_tokens, sws, sb, stream)) != KVB_OK)
     return ks;
-  return kvb_attend(s, q, att, token_ids, n_tokens, out, lse, aws, ab, stream);
+  KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+  KVB_CUDA(launch_attend_main(s, L, st), "sparse attention");
+  return KVB_OK;
 }
 
 int64_t kvb_select_candidates_workspace_bytes(const kvb_store* s, int32_t k) {

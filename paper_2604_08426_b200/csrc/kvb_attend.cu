@@ -711,33 +711,60 @@ size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
   return bytes;
 }
 
-cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
+namespace {
+
+struct AttWs {
+  float *pm, *pl, *po, *q2, *qt2;
+  int* counters;
+  int splits;
+  bool wh;
+};
+
+AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo) {
+  AttWs w{};
+  const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
+  const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
+  const int r = svd ? s->d.svd_rank : 0;
+  w.wh = attend_wh_supported(s, G);
+  w.splits = w.wh ? attend_wh_splits(s, a.cap) : geo.splits;
+  float* ws = static_cast<float*>(a.ws);
+  w.pm = ws;
+  w.pl = w.pm + (size_t)B * w.splits * H * G;
+  w.po = w.pl + (size_t)B * w.splits * H * G;
+  float* q2 = w.po + (size_t)B * w.splits * H * G * D;
+  w.q2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q2) + 15) & ~uintptr_t(15));
+  w.qt2 = w.q2 + (size_t)B * H * G * D;
+  w.counters = reinterpret_cast<int*>(w.qt2 + (size_t)B * H * G * (svd ? r : 0));
+  return w;
+}
+
+}  // namespace
+
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
+  const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
+  AttGeom geo = attend_geometry(s, G, a.cap);
+  AttWs w = carve_att_ws(s, a, geo);
+  const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
+  const int r = svd ? s->d.svd_rank : 0;
+  const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
+  ensure_smem((const void*)k5_prep, fs);
+  count_launch();
+  k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, w.q2, w.qt2,
+                                                    H, G, D, r, svd ? s->d.svd_groups : 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
   const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
   AttGeom geo = attend_geometry(s, G, a.cap);
   if (geo.smem > 227 * 1024) return cudaErrorInvalidValue;
+  AttWs w = carve_att_ws(s, a, geo);
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
-  const bool wh = attend_wh_supported(s, G);
-  const int splits = wh ? attend_wh_splits(s, a.cap) : geo.splits;
-  float* ws = static_cast<float*>(a.ws);
-  float* pm = ws;
-  float* pl = pm + (size_t)B * splits * H * G;
-  float* po = pl + (size_t)B * splits * H * G;
-  float* q2 = po + (size_t)B * splits * H * G * D;
-  q2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q2) + 15) & ~uintptr_t(15));
-  float* qt2 = q2 + (size_t)B * H * G * D;
-  int* counters = reinterpret_cast<int*>(qt2 + (size_t)B * H * G * (svd ? r : 0));
-  cudaMemsetAsync(counters, 0, sizeof(int) * B, st);
-  {
-    const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
-    ensure_smem((const void*)k5_prep, fs);
-    count_launch();
-    k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, q2, qt2,
-                                                      H, G, D, r, svd ? s->d.svd_groups : 1);
-  }
-  if (wh)
-    return launch_attend_wh(s, a.q, G, a.token_ids, a.n_tokens, a.cap, qt2, pm, pl, po, splits,
-                            a.out, a.lse, st);
+  if (w.wh)
+    return launch_attend_wh(s, a.q, G, a.token_ids, a.n_tokens, a.cap, w.qt2, w.pm, w.pl, w.po,
+                            w.splits, a.out, a.lse, st);
+  cudaMemsetAsync(w.counters, 0, sizeof(int) * B, st);
   AttParams& p = geo.p;
   p.tok = a.token_ids;
   p.ntok = a.n_tokens;
@@ -757,25 +784,31 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
   p.off_k = s->off_k_dev;
   p.off_v = s->off_v_dev;
   p.left = s->svd_left;
-  p.q2 = q2;
-  p.qt2 = qt2;
+  p.q2 = w.q2;
+  p.qt2 = w.qt2;
   p.scale = (float)(1.0 / sqrt((double)D));
   p.slow_svd = svd ? 1 : 0;
-  p.pm = pm;
-  p.pl = pl;
-  p.po = po;
-  p.counters = counters;
+  p.pm = w.pm;
+  p.pl = w.pl;
+  p.po = w.po;
+  p.counters = w.counters;
   p.out = a.out;
   p.lse = a.lse;
   count_launch(1);
   if (s->d.kv_dtype == KVB_BF16) {
     ensure_smem((const void*)k5_attend<__nv_bfloat16, 16>, geo.smem);
-    k5_attend<__nv_bfloat16, 16><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
+    k5_attend<__nv_bfloat16, 16><<<dim3(w.splits, B), kAttThreads, geo.smem, st>>>(p);
   } else {
     ensure_smem((const void*)k5_attend<float, 8>, geo.smem);
-    k5_attend<float, 8><<<dim3(splits, B), kAttThreads, geo.smem, st>>>(p);
+    k5_attend<float, 8><<<dim3(w.splits, B), kAttThreads, geo.smem, st>>>(p);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
+  cudaError_t e = launch_attend_prep(s, a, st);
+  if (e != cudaSuccess) return e;
+  return launch_attend_main(s, a, st);
 }
 
 // Cross-shard LSE merge: rows = B*H*G.

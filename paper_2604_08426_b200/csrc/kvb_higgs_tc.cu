@@ -13,8 +13,9 @@
 // codewords [rows x D] by W_h [D x R]. It runs on mma.sync m16n8k16 with the
 // codewords and W split into fp16 hi + lo (A_hi B_hi + A_hi B_lo + A_lo B_hi,
 // ~2^-20 relative, fp32 accumulation), the codeword pairs coming straight
-// from a shared-memory LUT indexed by the packed code byte -- decoded values
-// never touch memory. The H_R combine is a 3-level butterfly over the lanes
+// from a shared-memory LUT indexed by the 4-bit code -- decoded values
+// never touch memory (16-entry LUT of 8-byte hi/lo pairs: conflict-free).
+// The H_R combine is a 3-level butterfly over the lanes
 // holding the R slices; heads are summed in head order.
 //
 // Scores are fp32-class (tensor-core accumulation order) rather than the
@@ -78,7 +79,9 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     const uint8_t* __restrict__ codes, const float* __restrict__ factors,
     const float* __restrict__ W, const float* __restrict__ cb, float* __restrict__ scores,
     int rows, int H, int ngroups, int gbytes, int tiles_per_cta, uint32_t* __restrict__ hist) {
-  __shared__ uint4 lut[256];                 // byte -> (hi c0, hi c1, lo c0, lo c1)
+  // code -> (hi half2, lo half2): 16 entries x 8 B span the 32 banks exactly,
+  // so any lane->entry pattern is conflict-free
+  __shared__ uint2 lut[16];
   __shared__ float part[HMAX][kTPI * kTileRows];
   __shared__ uint32_t shist[kTopHistBins];   // first radix level of K2 (see k1_dense_sum)
   if (hist)
@@ -86,14 +89,11 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y;
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    const int c0 = i & 15, c1 = i >> 4;
-    const float x0 = cb[2 * c0], y0 = cb[2 * c0 + 1];
-    const float x1 = cb[2 * c1], y1 = cb[2 * c1 + 1];
-    const __half2 h0 = __floats2half2_rn(x0, y0), h1 = __floats2half2_rn(x1, y1);
-    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
-    lut[i] = make_uint4(h2u(h0), h2u(h1), h2u(__floats2half2_rn(x0 - f0.x, y0 - f0.y)),
-                        h2u(__floats2half2_rn(x1 - f1.x, y1 - f1.y)));
+  if (threadIdx.x < 16) {
+    const float x = cb[2 * threadIdx.x], y = cb[2 * threadIdx.x + 1];
+    const __half2 hh = __floats2half2_rn(x, y);
+    const float2 f = __half22float2(hh);
+    lut[threadIdx.x] = make_uint2(h2u(hh), h2u(__floats2half2_rn(x - f.x, y - f.y)));
   }
   // B fragments: thread (g4, tig) owns w_{g4}[32*tig + 4*ks + 0..3], ks = 0..7
   uint32_t bhi[8][2], blo[8][2];
@@ -152,12 +152,14 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
         for (int ks = 0; ks < 8; ++ks) {
           const uint32_t w0 = ks < 4 ? cur[u][0].x : cur[u][0].y;
           const uint32_t w1 = ks < 4 ? cur[u][1].x : cur[u][1].y;
-          const uint4 e0 = lut[(w0 >> (8 * (ks & 3))) & 255u];
-          const uint4 e1 = lut[(w1 >> (8 * (ks & 3))) & 255u];
-          // a0 (row g4, code 16tig+2ks) a2 (row g4, code +1); a1/a3: row g4 + 8
-          mma_f16(c, e0.x, e1.x, e0.y, e1.y, bhi[ks][0], bhi[ks][1]);
-          mma_f16(c, e0.x, e1.x, e0.y, e1.y, blo[ks][0], blo[ks][1]);
-          mma_f16(c, e0.z, e1.z, e0.w, e1.w, bhi[ks][0], bhi[ks][1]);
+          const uint32_t sh = 8 * (ks & 3);
+          // a0 (row g4, code 16tig+2ks = low nibble), a2 (code +1 = high nibble);
+          // a1/a3: the same for row g4 + 8
+          const uint2 l0 = lut[(w0 >> sh) & 15u], h0 = lut[(w0 >> (sh + 4)) & 15u];
+          const uint2 l1 = lut[(w1 >> sh) & 15u], h1 = lut[(w1 >> (sh + 4)) & 15u];
+          mma_f16(c, l0.x, l1.x, h0.x, h1.x, bhi[ks][0], bhi[ks][1]);
+          mma_f16(c, l0.x, l1.x, h0.x, h1.x, blo[ks][0], blo[ks][1]);
+          mma_f16(c, l0.y, l1.y, h0.y, h1.y, bhi[ks][0], bhi[ks][1]);
         }
       }
       // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)

@@ -44,6 +44,9 @@ struct kvb_store {
   void* off_k_dev = nullptr;     // device alias when host-mapped
   void* off_v_dev = nullptr;
   bool off_host = false;
+  // side stream + events for the fork/join of decode-step work (prep || scan)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace kvb {
@@ -126,6 +129,9 @@ cudaError_t launch_attend_wh(const kvb_store* s, const float* q, int G, const in
                              const int32_t* ntok, int cap, const float* qt2, float* pm, float* pl,
                              float* po, int splits, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
+// the two halves of launch_attend: per-step query prep, then the attention
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
+cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
                                    int D, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
