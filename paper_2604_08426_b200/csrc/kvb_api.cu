@@ -533,7 +533,7 @@ int64_t kvb_select_workspace_bytes(const kvb_store* s, const kvb_select_args* a)
   if (!s || !a) return -1;
   return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned(4) +
                    aligned(higgs_tc_ws_bytes(s)) + aligned((size_t)s->d.batch * kTopHistBins * 4) +
-                   256);
+                   aligned(select2_ws_bytes(s, a->n_select)) + 256);
 }
 
 static kvb_status check_select(const kvb_store* s, const kvb_select_args* a) {
@@ -591,6 +591,12 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
   L.err_flag = nullptr;
   L.hist = use_hist ? hist : nullptr;
   (void)err;
+  if (use_hist) {
+    // histogram-carrying scan: whole-GPU split (K2a) + per-sequence finish (K2b)
+    void* s2ws = cv.take<char>(select2_ws_bytes(s, a->n_select));
+    KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "top-k selection");
+    return KVB_OK;
+  }
   KVB_CUDA(launch_select(s, L, st), "top-k selection");
   return KVB_OK;
 }

@@ -98,6 +98,11 @@ cudaError_t launch_tokens_from_chunks(const kvb_store* s, const int32_t* chunk_i
                                       int cap, cudaStream_t st);
 cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_t st);
 size_t select_smem_bytes(const kvb_store* s, int K, int mode);
+// Two-kernel top-K for histogram-carrying scans (mode 0, no m_count). The
+// caller must check *overflow (device) only if it needs the fallback.
+size_t select2_ws_bytes(const kvb_store* s, int K);
+cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, cudaStream_t st,
+                           int32_t** overflow_out);
 
 // Ascending list of the tokens of the selected chunks (Appendix-E stage 2).
 cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,

@@ -25,6 +25,7 @@ namespace kvb {
 namespace {
 
 constexpr int kSelThreads = 1024;
+constexpr int kCandCap = 32768;  // threshold-bin candidates per sequence (K2a/K2b)
 
 struct SelParams {
   const float* scores;
@@ -97,8 +98,7 @@ __device__ __forceinline__ void token_union(const uint32_t* rb, int with_residen
   }
 }
 
-__global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __noinline__ void select_body(const SelParams& p, unsigned char* smem_raw) {
   __shared__ int hist[256];
   __shared__ int whist[kSelThreads / 32][256];  // per-warp private histograms
   __shared__ int red[33];
@@ -374,6 +374,249 @@ __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
               p.token_ids + (size_t)b * p.cap, p.cap, p.n_tokens + b, p.err_flag, red);
 }
 
+__global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  select_body(p, smem_raw);
+}
+
+// ---------------------------------------------------------------------------
+// Two-kernel top-K for scans that produced the fused 2048-bin key histogram.
+// K2a (whole GPU): every CTA derives the threshold bin tb from the histogram
+// and scans its slice of keys: bin > tb -> selected, bin == tb -> candidate
+// (key, id). K2b (one CTA per sequence): exact bisection over the candidates'
+// low 21 bits (single warp), lowest-id tie rule, optional rank sort, token
+// union. Candidate overflow (pathological ties) falls back to k2_select.
+// ---------------------------------------------------------------------------
+struct K2Meta {
+  int tb, kb;       // threshold bin, items to take inside it
+  int nsel, ncand;  // appended counts (atomics)
+};
+
+__device__ __forceinline__ void hist_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
+                                               int* s_kb, int* s_nb) {
+  // bins in descending order, 8 per thread with 256 threads
+  const int tid = threadIdx.x;
+  const int per = kTopHistBins / blockDim.x;
+  int loc = 0;
+  for (int j = 0; j < per; ++j) loc += (int)hb[kTopHistBins - 1 - (tid * per + j)];
+  int tot;
+  int above = block_excl_scan(loc, red, &tot);
+  if (above < K && K <= above + loc) {
+    for (int j = 0; j < per; ++j) {
+      const int bin = kTopHistBins - 1 - (tid * per + j);
+      const int c = (int)hb[bin];
+      if (above + c >= K) {
+        *s_tb = bin;
+        *s_kb = K - above;
+        *s_nb = c;
+        break;
+      }
+      above += c;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k2a_split(const float* __restrict__ scores, int M, int K,
+                                                 const uint32_t* __restrict__ hist,
+                                                 K2Meta* __restrict__ meta,
+                                                 int32_t* __restrict__ sel, int sel_stride,
+                                                 uint64_t* __restrict__ cand, int cand_cap) {
+  __shared__ int red[33];
+  __shared__ int s_tb, s_kb, s_nb;
+  const int b = blockIdx.y, lane = threadIdx.x & 31;
+  const int Kc = K < M ? K : M;
+  hist_threshold(hist + (size_t)b * kTopHistBins, Kc, red, &s_tb, &s_kb, &s_nb);
+  const uint32_t tb = (uint32_t)s_tb;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta[b].tb = s_tb;
+    meta[b].kb = s_kb;
+  }
+  const float* sc = scores + (size_t)b * M;
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * per, i1 = min(M, i0 + per);
+  for (int base = i0 + (threadIdx.x & ~31) * 4; base < i1; base += blockDim.x * 4) {
+    uint32_t u4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + 32 * k + lane;
+      u4[k] = i < i1 ? score_key(__ldg(sc + i)) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + 32 * k + lane;
+      const uint32_t bin = u4[k] >> 21;
+      const bool is_sel = i < i1 && bin > tb;
+      const bool is_cand = i < i1 && bin == tb;
+      unsigned m = __ballot_sync(FULL, is_sel);
+      if (m) {
+        int wb = 0;
+        if (lane == 0) wb = atomicAdd(&meta[b].nsel, __popc(m));
+        wb = __shfl_sync(FULL, wb, 0);
+        if (is_sel) sel[(size_t)b * sel_stride + wb + __popc(m & ((1u << lane) - 1u))] = i;
+      }
+      m = __ballot_sync(FULL, is_cand);
+      if (m) {
+        int wb = 0;
+        if (lane == 0) wb = atomicAdd(&meta[b].ncand, __popc(m));
+        wb = __shfl_sync(FULL, wb, 0);
+        const int pos = wb + __popc(m & ((1u << lane) - 1u));
+        if (is_cand && pos < cand_cap)
+          cand[(size_t)b * cand_cap + pos] = ((uint64_t)u4[k] << 32) | (uint32_t)i;
+      }
+    }
+  }
+}
+
+struct K2bParams {
+  const K2Meta* meta;
+  int32_t* sel;          // [B][K] (K2a appended the certain winners)
+  const uint64_t* cand;  // [B][cand_cap]
+  int cand_cap, K, M, rank_order;
+  const float* scores;
+  int32_t* out_ids;      // [B][K]
+  int32_t* token_ids;
+  int32_t* n_tokens;
+  int cap;
+  const uint32_t* res_bitmap;
+  int n, cs, W, P;
+  int32_t* overflow;     // [B] set when K2a overflowed (caller falls back)
+};
+
+__global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int red[33];
+  __shared__ uint32_t s_T;
+  __shared__ int s_gt, s_eq, s_cnt;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x;
+  const K2Meta mt = p.meta[b];
+  const int K = p.K < p.M ? p.K : p.M;
+  uint64_t* keys64 = reinterpret_cast<uint64_t*>(smem_raw);                 // [P] rank sort
+  const size_t selb = std::max((size_t)p.P * 8, (size_t)((p.K + 3) & ~3) * 4);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + selb);              // [W]
+  int32_t* ids = p.sel + (size_t)b * p.K;
+  if (mt.ncand > p.cand_cap) {
+    // pathological ties (> cand_cap keys share the top 11 bits): exact 4-pass
+    // radix select over every key of this sequence, in this CTA
+    if (tid == 0) p.overflow[b] = 1;
+    SelParams q{};
+    q.scores = p.scores;
+    q.M_stride = p.M;
+    q.K = p.K;
+    q.rank_order = p.rank_order;
+    q.mode = 0;
+    q.sel_ids = p.out_ids;
+    q.token_ids = p.token_ids;
+    q.n_tokens = p.n_tokens;
+    q.cap = p.cap;
+    q.with_residents = 1;
+    q.res_bitmap = p.res_bitmap;
+    q.n = p.n;
+    q.cs = p.cs;
+    q.W = p.W;
+    q.P = p.P ? p.P : 1;
+    q.stage = 0;
+    q.hist = nullptr;
+    q.id_offset = 0;
+    q.sel_scores = nullptr;
+    select_body(q, smem_raw);
+    return;
+  }
+  const uint64_t* cd = p.cand + (size_t)b * p.cand_cap;
+  const int nc = mt.ncand, kb = mt.kb;
+  if (warp == 0) {
+    uint32_t lo = (uint32_t)mt.tb << 21, hi = lo | 0x1fffffu;
+    while (lo < hi) {
+      const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+      int c = 0;
+      for (int i = lane; i < nc; i += 32) c += (uint32_t)(cd[i] >> 32) >= mid ? 1 : 0;
+      c = __reduce_add_sync(FULL, c);
+      if (c >= kb) lo = mid; else hi = mid - 1u;
+    }
+    int gt = 0, eq = 0;
+    for (int i = lane; i < nc; i += 32) {
+      const uint32_t u = (uint32_t)(cd[i] >> 32);
+      gt += u > lo ? 1 : 0;
+      eq += u == lo ? 1 : 0;
+    }
+    gt = __reduce_add_sync(FULL, gt);
+    eq = __reduce_add_sync(FULL, eq);
+    if (lane == 0) {
+      s_T = lo;
+      s_gt = gt;
+      s_eq = eq;
+      s_cnt = mt.nsel;
+    }
+  }
+  __syncthreads();
+  const uint32_t T = s_T;
+  const int krem = kb - s_gt;
+  const bool all_ties = krem == s_eq;
+  // candidates strictly above T, and every tie when all are needed
+  for (int base = warp * 32; base < nc; base += nthr) {
+    const int i = base + lane;
+    const uint32_t u = i < nc ? (uint32_t)(cd[i] >> 32) : 0u;
+    const bool take = i < nc && (u > T || (all_ties && u == T));
+    const unsigned m = __ballot_sync(FULL, take);
+    int wb = 0;
+    if (lane == 0 && m) wb = atomicAdd(&s_cnt, __popc(m));
+    wb = __shfl_sync(FULL, wb, 0);
+    if (take) ids[wb + __popc(m & ((1u << lane) - 1u))] = (int32_t)(uint32_t)cd[i];
+  }
+  __syncthreads();
+  if (!all_ties) {
+    // the krem lowest ids among the ties: rank ties by id (counting smaller ids)
+    const int start = s_cnt;
+    for (int i = tid; i < nc; i += nthr) {
+      if ((uint32_t)(cd[i] >> 32) != T) continue;
+      const uint32_t id = (uint32_t)cd[i];
+      int rank = 0;
+      for (int j = 0; j < nc; ++j)
+        rank += ((uint32_t)(cd[j] >> 32) == T && (uint32_t)cd[j] < id) ? 1 : 0;
+      if (rank < krem) ids[start + rank] = (int32_t)id;
+    }
+  }
+  __syncthreads();
+  // ids[0..K) now holds the top-K set; rank order on request
+  if (p.rank_order) {
+    const float* sc = p.scores + (size_t)b * p.M;
+    for (int i = tid; i < p.P; i += nthr) {
+      uint64_t v = 0ull;
+      if (i < K) {
+        const uint32_t id = (uint32_t)ids[i];
+        v = ((uint64_t)score_key(sc[id]) << 32) | (uint64_t)(0xffffffffu - id);
+      }
+      keys64[i] = v;
+    }
+    __syncthreads();
+    for (int k = 2; k <= p.P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = tid; t < p.P / 2; t += nthr) {
+          const int i = (t / j) * 2 * j + (t % j);
+          const int l = i + j;
+          const bool desc = (i & k) == 0;
+          const uint64_t a = keys64[i], c = keys64[l];
+          if ((a < c) == desc) {
+            keys64[i] = c;
+            keys64[l] = a;
+          }
+        }
+        __syncthreads();
+      }
+    for (int r = tid; r < p.K; r += nthr)
+      p.out_ids[(size_t)b * p.K + r] = r < K ? (int32_t)(0xffffffffu - (uint32_t)keys64[r]) : -1;
+  } else if (p.out_ids != p.sel) {
+    for (int r = tid; r < p.K; r += nthr)
+      p.out_ids[(size_t)b * p.K + r] = r < K ? ids[r] : -1;
+  }
+  if (!p.token_ids) return;
+  __syncthreads();
+  token_union(p.res_bitmap + (size_t)b * p.W, 1, p.W, bm, [&](int r) { return (int)ids[r]; }, K,
+              0, p.cs, p.n, nullptr, 0, 1 << 30, p.token_ids + (size_t)b * p.cap, p.cap,
+              p.n_tokens + b, nullptr, red);
+}
+
 int next_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -386,6 +629,58 @@ size_t select_smem_bytes(const kvb_store* s, int K, int mode) {
   (void)mode;
   const size_t sel = (size_t)next_pow2(K < 1 ? 1 : K) * 8;
   return sel + (size_t)s->W * 4;
+}
+
+size_t select2_ws_bytes(const kvb_store* s, int K) {
+  const size_t B = s->d.batch;
+  const size_t cap = kCandCap;
+  return B * sizeof(K2Meta) + B * K * 4 + B * cap * 8 + B * 4 + 1024;
+}
+
+cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, cudaStream_t st,
+                           int32_t** overflow_out) {
+  const int B = s->d.batch;
+  char* w = static_cast<char*>(ws);
+  K2Meta* meta = reinterpret_cast<K2Meta*>(w);
+  w += ((B * sizeof(K2Meta) + 255) & ~size_t(255));
+  int32_t* overflow = reinterpret_cast<int32_t*>(w);
+  w += ((B * 4 + 255) & ~size_t(255));
+  int32_t* sel = reinterpret_cast<int32_t*>(w);
+  w += (((size_t)B * a.K * 4 + 255) & ~size_t(255));
+  uint64_t* cand = reinterpret_cast<uint64_t*>(w);
+  cudaMemsetAsync(meta, 0, B * sizeof(K2Meta), st);
+  cudaMemsetAsync(overflow, 0, B * 4, st);
+  const int per_seq = std::max(1, sm_count() * 2 / B);
+  count_launch(2);
+  k2a_split<<<dim3(per_seq, B), 256, 0, st>>>(a.scores, a.M_stride, a.K, a.hist, meta, sel, a.K,
+                                              cand, kCandCap);
+  K2bParams p{};
+  p.meta = meta;
+  p.sel = sel;
+  p.cand = cand;
+  p.cand_cap = kCandCap;
+  p.K = a.K;
+  p.M = a.M_stride;
+  p.rank_order = a.rank_order;
+  p.scores = a.scores;
+  p.out_ids = a.sel_ids;
+  p.token_ids = a.token_ids;
+  p.n_tokens = a.n_tokens;
+  p.cap = a.cap;
+  p.res_bitmap = s->res_bitmap;
+  p.n = s->d.n_tokens;
+  p.cs = s->d.chunk_size;
+  p.W = s->W;
+  p.P = a.rank_order ? next_pow2(a.K < 1 ? 1 : a.K) : 0;
+  p.overflow = overflow;
+  // room for the in-kernel radix fallback too: max(P*8, K*4) + bitmap
+  const int Pf = next_pow2(a.K < 1 ? 1 : a.K);
+  const size_t smem = std::max((size_t)(a.rank_order ? Pf : 0) * 8, (size_t)((a.K + 3) & ~3) * 4) +
+                      (size_t)s->W * 4;
+  ensure_smem((const void*)k2b_finish, smem);
+  k2b_finish<<<B, kSelThreads, smem, st>>>(p);
+  if (overflow_out) *overflow_out = overflow;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_t st) {
