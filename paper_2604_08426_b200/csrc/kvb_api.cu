@@ -26,10 +26,19 @@ void set_error(const std::string& msg) { g_err = msg; }
 void count_launch(int n) { g_launches += n; }
 
 cudaError_t ensure_smem(const void* func, size_t bytes) {
+  // opt in whenever static + dynamic shared memory exceeds the 48 KB default
   static std::mutex mu;
   static std::unordered_map<const void*, size_t> done;
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::unordered_map<const void*, size_t> static_bytes;
   std::lock_guard<std::mutex> lock(mu);
+  auto sb = static_bytes.find(func);
+  if (sb == static_bytes.end()) {
+    cudaFuncAttributes attr{};
+    size_t v = 0;
+    if (cudaFuncGetAttributes(&attr, func) == cudaSuccess) v = attr.sharedSizeBytes;
+    sb = static_bytes.emplace(func, v).first;
+  }
+  if (bytes + sb->second <= 48 * 1024) return cudaSuccess;
   auto it = done.find(func);
   if (it != done.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
