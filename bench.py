@@ -41,6 +41,7 @@ VARIANTS = {
     "shadowkv": "C2 ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
     "higgs2c1": "C2 paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
     "shadowkv_host": "C3 ShadowKV with V offloaded to pinned, device-mapped host memory (zero-copy gather over the host link)",
+    "c4": "C4 Qwen2.5-7B-1M shape (28 q / 4 kv heads), 1M ctx, batch 1, ShadowKV r160/cs8, sequence-sharded over the GPUs: global top-K + LSE merge by NCCL all-gather",
 }
 
 
@@ -462,6 +463,79 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     return res
 
 
+def run_c4(a, rank, world, local):
+    """C4: one 1M-token sequence sharded over `world` GPUs (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_08426_b200 import sharded as SH
+
+    H, G, D, cs = 4, 7, 128, 8
+    n = a.ctx if a.ctx != 131072 else 1 << 20
+    L_ = a.layers if a.layers != 32 else 28
+    B = 1
+    frac = 0.0156
+    spec = SH.ShardSpec(n, cs, world, rank)
+    ex = SH.Exchange() if world > 1 else SH.SoloExchange()
+    gen = torch.Generator(device="cuda")
+    t_build = time.perf_counter()
+    decs = []
+    K = SH.global_k(n, cs, frac)
+    for layer in range(L_):
+        gen.manual_seed(7919 * layer + rank)
+        shape = (B, spec.n_local, H, D)
+        k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
+        v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
+        st = SH.build_shard(k, v, spec, ex)
+        del k, v
+        decs.append(SH.ShardedDecoder(st, spec, ex, K))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+    qgen = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn((L_, B, H, G, D), generator=qgen, device="cuda")
+
+    def step():
+        for l in range(L_):
+            decs[l].step(q[l])
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record()
+        for _ in range(a.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / a.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    st0 = decs[0].store
+    E = H * D
+    per_layer = (spec.n_chunks * E * 2 + K * cs * (160 * 2 + E * 2) + 160 * E * 2 * world +
+                 world * st0.max_resident * E * 4)
+    hbm, kind = peaks()
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(B / (ms / 1e3), 2), "unit": "tok/s", "n_gpus": world,
+               "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic (torch.randn K/V per layer and rank)",
+               "config": {"workload": VARIANTS["c4"], "seq_len": n, "layers": L_, "global_batch": B,
+                          "selected_chunks": K, "parallelism": f"sequence-sharded x{world}"},
+               "step_roofline": {"achieved": round(L_ * per_layer / (ms / 1e3) / 1e9, 1),
+                                 "peak": hbm * world, "unit": "GB/s",
+                                 "frac": round(L_ * per_layer / (ms / 1e3) / 1e9 / (hbm * world), 4)},
+               "collectives_per_layer": 4, "clocks": sampler.summary(),
+               "build_s": round(t_build, 1)}
+        print(json.dumps(out), flush=True)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -477,6 +551,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     primary = a.variant
+    if primary == "c4":
+        run_c4(a, rank, world, local)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     r = measure(a, primary, rank, world, local)
     if r is None:
         return

@@ -99,6 +99,20 @@ class Exchange:
         return t
 
 
+class SoloExchange:
+    """World size 1: every collective is the identity."""
+
+    parts, rank = 1, 0
+
+    @staticmethod
+    def all_gather(t: torch.Tensor) -> torch.Tensor:
+        return t.contiguous()[None]
+
+    @staticmethod
+    def all_reduce_sum(t: torch.Tensor) -> torch.Tensor:
+        return t
+
+
 class LocalExchange:
     """Single-process stand-in: the caller supplies every shard's tensor."""
 
@@ -201,6 +215,47 @@ def global_k(n_tokens: int, chunk_size: int, sparse_fraction: float) -> int:
     """selection.py:85 on the global context."""
     C_ = -(-n_tokens // chunk_size)
     return min(C_, math.ceil(sparse_fraction * n_tokens / chunk_size))
+
+
+def build_shard(keys: torch.Tensor, values: torch.Tensor, spec: ShardSpec, ex, *, rank_r: int = 160,
+                outlier_tokens: int = 384, local_window: int = 32, dtype=torch.bfloat16):
+    """Prefill of one shard with the global-agreement steps of SURVEY 8e:
+    chunk-local landmarks; head-concatenated rank-r SVD from the all-reduced
+    Gram matrix K^T K (every rank gets identical `right`); outliers from the
+    all-gathered per-chunk cosines; the global local-window on the last rank."""
+    from .schemes import scheme_none, scheme_svd
+    from .store import DeviceStore
+
+    B, n_local, H, D = keys.shape
+    st = DeviceStore(batch=B, n_tokens=n_local, kv_heads=H, head_dim=D, chunk_size=spec.chunk_size,
+                     dtype=dtype, landmark=scheme_none(), slow=scheme_svd(rank_r, H * D),
+                     svd_groups=1, outlier_tokens=outlier_tokens, local_window=local_window)
+    st.build_landmarks(keys)
+    E = H * D
+    left = torch.empty((B, n_local, 1, rank_r), dtype=torch.float16, device=keys.device)
+    right = torch.empty((B, 1, rank_r, E), dtype=torch.float16, device=keys.device)
+    for b in range(B):
+        kb = keys[b].reshape(n_local, E).float()
+        gram = ex.all_reduce_sum((kb.T @ kb).double())
+        _, V = torch.linalg.eigh(gram)
+        V = V.flip(1)[:, :rank_r]
+        left[b, :, 0] = (kb.double() @ V).float().half()
+        right[b, 0] = V.T.float().half()
+        del kb
+    st.import_svd(left, right)
+    del left
+    counts = [ShardSpec(spec.n_tokens, spec.chunk_size, spec.parts, p).chunk_hi -
+              ShardSpec(spec.n_tokens, spec.chunk_size, spec.parts, p).chunk_lo
+              for p in range(spec.parts)]
+    pc = st.chunk_cosine(keys)
+    allpc = gather_padded(ex, pc, max(counts), 0.0).cpu().numpy()  # [P, B, maxc]
+    outl = [local_outliers(global_outliers(allpc[:, b], counts, spec.n_tokens, spec.chunk_size,
+                                           outlier_tokens), spec) for b in range(B)]
+    win = spec.local_window(local_window)
+    st.local_window = len(win)  # the global window's share (a suffix of this shard)
+    st.build_residency(keys, values, outliers=outl)
+    st.import_offload(keys, values)
+    return st
 
 
 class ShardedDecoder:
