@@ -65,6 +65,22 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(variant, kernel_prefix):
+    """DRAM bytes (read + write) per launch of the roofline kernel from the newest
+    committed `ncu --set full` summary of this variant (tools/ncu_summary.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_{variant}_*.json")))
+    for f in reversed(files):
+        try:
+            ks = json.load(open(f))["kernels"]
+        except Exception:
+            continue
+        for name, k in ks.items():
+            if name.startswith(kernel_prefix) and k.get("traffic_bytes"):
+                return int(k["traffic_bytes"]), os.path.relpath(f, ROOT)
+    return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -587,6 +603,7 @@ def main():
                      "achieved_gbs": round(vb / (r["ms_per_step"] / 1e3) / 1e9, 1),
                      "frac": round(vb / (r["ms_per_step"] / 1e3) / 1e9 / link, 4)}
     k1_gbs = r["k1_bytes"] / (r["k1_ms"] / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(primary, r["k1_kernel"].split(" ")[0])
     step_gbs = r["step_bytes"] / (r["ms_per_step"] / 1e3) / 1e9
     if rank == 0:
         cpu = None
@@ -611,7 +628,8 @@ def main():
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(k1_gbs / hbm, 4),
                          "algorithmic_bytes_per_launch": r["k1_bytes"],
-                         "avg_launch_ms": round(r["k1_ms"], 5), "traffic": None},
+                         "avg_launch_ms": round(r["k1_ms"], 5), "traffic": traffic,
+                         "traffic_source": traffic_src},
             "step_roofline": {"achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s",
                               "frac": round(step_gbs / hbm, 4),
                               "algorithmic_bytes_per_step": r["step_bytes"],
