@@ -111,6 +111,13 @@ const char* kvb_last_error(void);
 int32_t kvb_abi_version(void);
 /* Number of kernels this library launched since load (all entry points). */
 int64_t kvb_launch_count(void);
+/* Profiling hook (not part of the reference interface): when enabled, the
+ * bulk attention kernel writes per-CTA %globaltimer phase stamps
+ * [B][splits][8] (start, setup, prologue, first tile, loop end, ticket,
+ * merge end, smid) of its most recent launch; kvb_trace_read copies them
+ * (synchronising the device) and returns the number of words. */
+int32_t kvb_trace_enable(int32_t on);
+int64_t kvb_trace_read(uint64_t* host, int64_t max_words);
 
 /* ---- store lifecycle (kvstore.py:354-385 build_store) ------------------- */
 kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out);

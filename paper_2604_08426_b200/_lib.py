@@ -62,6 +62,8 @@ SIGNATURES = [
     ("kvb_last_error", C.c_char_p, []),
     ("kvb_abi_version", _I32, []),
     ("kvb_launch_count", _I64, []),
+    ("kvb_trace_enable", _I32, [_I32]),
+    ("kvb_trace_read", _I64, [_P, _I64]),
     ("kvb_store_create", _I32, [C.POINTER(StoreDesc), C.POINTER(_P)]),
     ("kvb_store_destroy", _I32, [_P]),
     ("kvb_store_get_info", _I32, [_P, C.POINTER(StoreInfo)]),

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "kvb_common.cuh"
+#include "kvb_fuse.cuh"
 #include "kvb_internal.h"
 
 namespace kvb {
@@ -44,6 +45,46 @@ cudaError_t ensure_smem(const void* func, size_t bytes) {
   cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess) done[func] = bytes;
   return e;
+}
+
+namespace {
+uint64_t* g_trace = nullptr;
+bool g_trace_on = false;
+}  // namespace
+
+bool trace_enable(int on) {
+  if (on && !g_trace) {
+    if (cudaMalloc(&g_trace, sizeof(uint64_t) * kTraceWords) != cudaSuccess) return false;
+    cudaMemset(g_trace, 0, sizeof(uint64_t) * kTraceWords);
+  }
+  g_trace_on = on != 0;
+  return true;
+}
+
+uint64_t* trace_buffer() { return g_trace_on ? g_trace : nullptr; }
+
+int64_t trace_read(uint64_t* host, int64_t max_words) {
+  if (!g_trace || !host) return 0;
+  const int64_t n = max_words < kTraceWords ? max_words : kTraceWords;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpy(host, g_trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
+}
+
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       void** args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 int sm_count() {
@@ -160,12 +201,21 @@ void free_higgs(kvb_higgs_dev& h) {
 void free_store(kvb_store* s) {
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->ev_sel) cudaEventDestroy(s->ev_sel);
+  if (s->ev_union) cudaEventDestroy(s->ev_union);
   if (s->side) cudaStreamDestroy(s->side);
   cudaFree(s->lm_dense);
   free_higgs(s->lm_h);
   free_higgs(s->res_h);
   cudaFree(s->res_ids);
   cudaFree(s->res_count);
+  cudaFree(s->k2_hist);
+  cudaFree(s->sel_bm);
+  cudaFree(s->sel_ckey);
+  cudaFree(s->sel_cid);
+  cudaFree(s->sel_ctr);
+  cudaFree(s->k2_meta);
+  cudaFree(s->k2_overflow);
   cudaFree(s->res_bitmap);
   cudaFree(s->res_prefix);
   cudaFree(s->res_k);
@@ -225,6 +275,12 @@ const char* kvb_last_error(void) { return g_err.c_str(); }
 int32_t kvb_abi_version(void) { return KVB_ABI_VERSION; }
 int64_t kvb_launch_count(void) { return g_launches.load(); }
 
+int32_t kvb_trace_enable(int32_t on) { return kvb::trace_enable(on) ? 1 : 0; }
+
+int64_t kvb_trace_read(uint64_t* host, int64_t max_words) {
+  return kvb::trace_read(host, max_words);
+}
+
 kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if (!desc || !out) KVB_FAIL(KVB_EINVAL, "null argument");
   *out = nullptr;
@@ -274,6 +330,17 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc(&s->res_prefix, B * s->W, "resident prefix")) != KVB_OK) return bail(st);
   if ((st = dalloc((char**)&s->res_k, B * R * E * s->esz, "resident K")) != KVB_OK) return bail(st);
   if ((st = dalloc((char**)&s->res_v, B * R * E * s->esz, "resident V")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->k2_hist, B * kTopHistBins, "K2 histogram")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
+  s->Wc = (s->C + 31) / 32;
+  if ((st = dalloc(&s->sel_bm, B * s->Wc, "selection bitmap")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->sel_ckey, B * kFuseCap, "selection candidates")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->sel_cid, B * kFuseCap, "selection candidate ids")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->sel_ctr, B * 4, "selection counters")) != KVB_OK) return bail(st);
+  cudaMemset(s->sel_ctr, 0, B * 4 * sizeof(int32_t));
+  cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
+  cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
   cudaMemset(s->res_count, 0, B * sizeof(int32_t));
   cudaMemset(s->res_bitmap, 0, B * s->W * sizeof(uint32_t));
   cudaMemset(s->res_prefix, 0, B * s->W * sizeof(int32_t));
@@ -560,24 +627,33 @@ static kvb_status check_select(const kvb_store* s, const kvb_select_args* a) {
   return KVB_OK;
 }
 
-kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, int32_t* chunk_ids,
-                      float* scores, int32_t* token_ids, int32_t* n_tokens, void* ws,
-                      int64_t ws_bytes, void* stream) {
-  kvb_status ks = check_select(s, a);
-  if (ks != KVB_OK) return ks;
-  if (!q || !chunk_ids || !token_ids || !n_tokens) KVB_FAIL(KVB_EINVAL, "null argument");
-  if (ws_bytes < kvb_select_workspace_bytes(s, a) || !ws) KVB_FAIL(KVB_EINVAL, "workspace too small");
-  cudaStream_t st = as_stream(stream);
+}  // extern "C"
+
+namespace {
+
+// Landmark scan + top-K (+ token union when token_ids != null). With
+// `sorted` the selected chunk ids come out in ascending order (K2a/K2b
+// path only); *sorted_out reports whether that path ran.
+kvb_status select_impl(kvb_store* s, const float* q, const kvb_select_args* a, int32_t* chunk_ids,
+                       float* scores, int32_t* token_ids, int32_t* n_tokens, void* ws,
+                       int64_t ws_bytes, cudaStream_t st, bool sorted, bool* sorted_out) {
   Carve cv(ws, ws_bytes);
   float* sc = scores ? scores : cv.take<float>((size_t)s->d.batch * s->C);
   int32_t* err = cv.take<int32_t>(1);
   void* tcws = cv.take<char>(higgs_tc_ws_bytes(s));
-  uint32_t* hist = cv.take<uint32_t>((size_t)s->d.batch * kTopHistBins);
+  (void)cv.take<uint32_t>((size_t)s->d.batch * kTopHistBins);  // (layout kept: ws size unchanged)
+  uint32_t* hist = s->k2_hist;
   const bool use_tc = !a->exact_scores && a->aggregation == KVB_AGG_SUM && higgs_tc_supported(s);
   const bool use_hist = a->aggregation == KVB_AGG_SUM &&
                         (s->d.landmark_kind == KVB_LM_DENSE || use_tc);
-  if (use_hist)
+  if (sorted_out) *sorted_out = false;
+  if (use_hist && s->k2_dirty) {
     KVB_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+    KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * s->d.batch * 4, st), "meta reset");
+    s->k2_dirty = false;
+  }
+  s->k2_dirty = true;  // cleared below once every launch of the chain was accepted
+  kvb_status ks;
   if (use_tc) {
     KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, sc, tcws, hist, st),
              "HIGGS tensor-core scoring");
@@ -602,12 +678,31 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
   (void)err;
   if (use_hist) {
     // histogram-carrying scan: whole-GPU split (K2a) + per-sequence finish (K2b)
+    L.sorted_ids = (sorted && !a->rank_order) ? 1 : 0;
     void* s2ws = cv.take<char>(select2_ws_bytes(s, a->n_select));
     KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "top-k selection");
+    if (sorted_out) *sorted_out = L.sorted_ids != 0;
+    s->k2_dirty = false;
     return KVB_OK;
   }
+  s->k2_dirty = false;
   KVB_CUDA(launch_select(s, L, st), "top-k selection");
   return KVB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, int32_t* chunk_ids,
+                      float* scores, int32_t* token_ids, int32_t* n_tokens, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  kvb_status ks = check_select(s, a);
+  if (ks != KVB_OK) return ks;
+  if (!q || !chunk_ids || !token_ids || !n_tokens) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (ws_bytes < kvb_select_workspace_bytes(s, a) || !ws) KVB_FAIL(KVB_EINVAL, "workspace too small");
+  return select_impl(s, q, a, chunk_ids, scores, token_ids, n_tokens, ws, ws_bytes,
+                     as_stream(stream), false, nullptr);
 }
 
 int64_t kvb_select_residual_workspace_bytes(const kvb_store* s, const kvb_residual_args* a) {
@@ -742,14 +837,19 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   if (att->queries_per_head != sel->queries_per_head) KVB_FAIL(KVB_EINVAL, "G mismatch");
   if (s->d.slow_kind == KVB_SLOW_SVD && att->k_path == 2)
     KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
-  // fork: per-step query prep (q transpose, q~ = right.q) on the side stream,
-  // overlapping the landmark scan and top-K on the caller's stream; join
-  // before the attention. Capturable into CUDA graphs as a parallel branch.
+  // fork: per-step query prep (q transpose, q~ = right.q, split tickets) on
+  // the side stream, overlapping the landmark scan and top-K on the caller's
+  // stream; join before the attention. When the selected chunks come out
+  // sorted (K2a/K2b) the attention consumes them directly (residents +
+  // selected chunks) and also writes the sorted token union the API returns.
+  // Capturable into CUDA graphs.
   cudaStream_t st = as_stream(stream);
   if (!s->side) {
     KVB_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "side stream");
     KVB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming), "fork event");
     KVB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming), "join event");
+    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_sel, cudaEventDisableTiming), "select event");
+    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_union, cudaEventDisableTiming), "union event");
   }
   AttendLaunch L{};
   L.q = q;
@@ -765,8 +865,56 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
   KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
   KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
-  if ((ks = kvb_select(s, q, &a2, cid, nullptr, token_ids, n_tokens, sws, sb, stream)) != KVB_OK)
+  const int K = sel->n_select;
+  const bool chunk_path =
+      attend_bulk_supported(s, L.G, s->d.max_resident + K * s->d.chunk_size, K);
+  if (chunk_path && sel->aggregation == KVB_AGG_SUM && s->d.landmark_kind == KVB_LM_DENSE) {
+    // scan + top-K in one kernel (kvb_fuse.cuh) -> attention over the bitmap
+    float* sc = static_cast<float*>(sws);  // select workspace starts with [B][C] scores
+    if (s->k2_dirty) {
+      KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->sel_ctr, 0, sizeof(int32_t) * s->d.batch * 4, st), "ctr reset");
+      s->k2_dirty = false;
+    }
+    FuseSel fz{};
+    fz.bm = s->sel_bm;
+    fz.ckey = s->sel_ckey;
+    fz.cid = s->sel_cid;
+    fz.ctr = s->sel_ctr;
+    fz.Wc = s->Wc;
+    fz.cap = kFuseCap;
+    fz.K = K < s->C ? K : s->C;
+    fz.on = 1;
+    fz.trace = trace_buffer() ? trace_buffer() + kTraceWords / 2 : nullptr;  // profiling hook
+    s->k2_dirty = true;
+    cudaError_t fe = launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, &fz);
+    if (fe == cudaSuccess) {
+      s->k2_dirty = false;
+      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, s->sel_bm, chunk_ids), "sparse attention");
+      return KVB_OK;
+    }
+    if (fe != cudaErrorNotSupported) KVB_CUDA(fe, "fused landmark scan + top-K");
+    (void)cudaGetLastError();
+    s->k2_dirty = false;
+  }
+  bool sorted = false;
+  if ((ks = select_impl(s, q, &a2, cid, nullptr, chunk_path ? nullptr : token_ids,
+                        chunk_path ? nullptr : n_tokens, sws, sb, st, chunk_path, &sorted)) != KVB_OK)
     return ks;
+  if (chunk_path && !sorted) {
+    // unsorted selection (no K2a/K2b path): union on the main stream, token attention
+    KVB_CUDA(launch_tokens_from_chunks(s, cid, K, 0, token_ids, n_tokens, L.cap, st), "token union");
+    KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+    KVB_CUDA(launch_attend_main(s, L, st), "sparse attention");
+    return KVB_OK;
+  }
+  if (chunk_path) {
+    // the attention also emits the sorted token union (token_ids, n_tokens)
+    KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+    KVB_CUDA(launch_attend_chunks(s, L, cid, K, st), "sparse attention");
+    return KVB_OK;
+  }
   KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
   KVB_CUDA(launch_attend_main(s, L, st), "sparse attention");
   return KVB_OK;

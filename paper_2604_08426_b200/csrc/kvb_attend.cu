@@ -25,6 +25,7 @@
 // counter) merges them with the exact log-sum-exp rule and also returns the
 // LSE used by the cross-GPU merge (kvb_merge_attention).
 
+#include <algorithm>
 #include <type_traits>
 
 #include "kvb_common.cuh"
@@ -598,9 +599,13 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
 __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                const uint16_t* __restrict__ right,
                                                float* __restrict__ q2, float* __restrict__ qt2,
-                                               int H, int G, int D, int r, int sgroups) {
+                                               int H, int G, int D, int r, int sgroups,
+                                               int* __restrict__ counters) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
+  // split tickets of the attention that follows (self-resetting; zeroed here
+  // so a fresh caller workspace needs no memset)
+  if (counters && h == 0 && blockIdx.z == 0 && threadIdx.x == 0) counters[b] = 0;
   const int rs = blockIdx.z, nrs = gridDim.z;  // this CTA folds rows [r0, r1)
   const int HG = H * G;
   float* qs = fsm;                 // [G][D]
@@ -705,6 +710,8 @@ size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
     const size_t sw = attend_wh_splits(s, cap);
     if (sw > splits) splits = sw;
   }
+  const size_t sb = (size_t)std::max(1, sm_count() / s->d.batch);  // bulk kernel (both modes)
+  if (sb > splits) splits = sb;
   size_t bytes = B * splits * H * G * (2 + D) * sizeof(float) + 4096;
   bytes += B * H * G * D * sizeof(float) + B * sizeof(int) + 64; // q2, split tickets
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
@@ -718,6 +725,7 @@ struct AttWs {
   int* counters;
   int splits;
   bool wh;
+  bool bulk;
 };
 
 AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo) {
@@ -725,13 +733,18 @@ AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo
   const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
-  w.wh = attend_wh_supported(s, G);
-  w.splits = w.wh ? attend_wh_splits(s, a.cap) : geo.splits;
+  w.bulk = attend_bulk_supported(s, G, a.cap);
+  w.wh = !w.bulk && attend_wh_supported(s, G);
+  w.splits = w.bulk ? attend_bulk_splits(s, a.cap) : w.wh ? attend_wh_splits(s, a.cap) : geo.splits;
+  // layout for the largest split count any variant uses (attend_ws_bytes)
+  size_t smax = geo.splits;
+  if (attend_wh_supported(s, G)) smax = std::max(smax, (size_t)attend_wh_splits(s, a.cap));
+  smax = std::max(smax, (size_t)std::max(1, sm_count() / B));
   float* ws = static_cast<float*>(a.ws);
   w.pm = ws;
-  w.pl = w.pm + (size_t)B * w.splits * H * G;
-  w.po = w.pl + (size_t)B * w.splits * H * G;
-  float* q2 = w.po + (size_t)B * w.splits * H * G * D;
+  w.pl = w.pm + (size_t)B * smax * H * G;
+  w.po = w.pl + (size_t)B * smax * H * G;
+  float* q2 = w.po + (size_t)B * smax * H * G * D;
   w.q2 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q2) + 15) & ~uintptr_t(15));
   w.qt2 = w.q2 + (size_t)B * H * G * D;
   w.counters = reinterpret_cast<int*>(w.qt2 + (size_t)B * H * G * (svd ? r : 0));
@@ -750,7 +763,8 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   ensure_smem((const void*)k5_prep, fs);
   count_launch();
   k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, w.q2, w.qt2,
-                                                    H, G, D, r, svd ? s->d.svd_groups : 1);
+                                                    H, G, D, r, svd ? s->d.svd_groups : 1,
+                                                    w.counters);
   return cudaGetLastError();
 }
 
@@ -761,6 +775,24 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
   AttWs w = carve_att_ws(s, a, geo);
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
+  if (w.bulk) {
+    BulkLaunch bl{};
+    bl.mode = 0;
+    bl.items = a.token_ids;
+    bl.nitems = a.n_tokens;
+    bl.cap = a.cap;
+    bl.G = G;
+    bl.q = a.q;
+    bl.qt2 = w.qt2;
+    bl.pm = w.pm;
+    bl.pl = w.pl;
+    bl.po = w.po;
+    bl.counters = w.counters;
+    bl.out = a.out;
+    bl.lse = a.lse;
+    bl.splits = w.splits;
+    return launch_attend_bulk(s, bl, st);
+  }
   if (w.wh)
     return launch_attend_wh(s, a.q, G, a.token_ids, a.n_tokens, a.cap, w.qt2, w.pm, w.pl, w.po,
                             w.splits, a.out, a.lse, st);
@@ -803,6 +835,37 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
     k5_attend<float, 8><<<dim3(w.splits, B), kAttThreads, geo.smem, st>>>(p);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
+                                 int K, cudaStream_t st, const uint32_t* sel_bm, int32_t* chunk_out) {
+  const int G = a.G;
+  const int pos_cap = s->d.max_resident + K * s->d.chunk_size;
+  if (!attend_bulk_supported(s, G, pos_cap, K)) return cudaErrorNotSupported;
+  AttGeom geo = attend_geometry(s, G, a.cap);
+  AttWs w = carve_att_ws(s, a, geo);
+  BulkLaunch bl{};
+  bl.mode = 1;
+  bl.items = chunk_ids;
+  bl.nitems = nullptr;
+  bl.cap = K;
+  bl.K = K;
+  bl.G = G;
+  bl.q = a.q;
+  bl.qt2 = w.qt2;
+  bl.pm = w.pm;
+  bl.pl = w.pl;
+  bl.po = w.po;
+  bl.counters = w.counters;
+  bl.out = a.out;
+  bl.lse = a.lse;
+  bl.splits = attend_bulk_splits(s, pos_cap);
+  bl.tok_out = const_cast<int32_t*>(a.token_ids);  // decode step: an output here
+  bl.ntok_out = const_cast<int32_t*>(a.n_tokens);
+  bl.tcap = a.cap;
+  bl.sel_bm = sel_bm;
+  bl.chunk_out = chunk_out;
+  return launch_attend_bulk(s, bl, st);
 }
 
 cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {

@@ -1,0 +1,948 @@
+// K4 + K5 (bf16 stores, HBM tiers) -- bulk-copy gather pipelined into a
+// warp-per-head split-K flash-decode on tensor cores.
+//
+// Semantics: attention.py:26-45,62-90 (softmax(q.K^T * fp32(1/sqrt(D))).V per
+// KV head over the selected + resident tokens, renormalised over the subset),
+// with the tier gather of kvstore.py:281-291 fused in: resident tokens are
+// served exact from the fast tier, every other token from the slow tier (SVD
+// factor row -> q~.left, or exact K from the offload tier).
+//
+// Execution (one CTA per (split, sequence), one warp per KV head):
+//  * prologue: the CTA's share of the work stream is classified into exact
+//    entries (resident slot / offloaded token) and SVD entries, compacted by a
+//    block scan (exact first);
+//  * production (consumer warp k % H stages tile k, two tiles ahead): one lane per token issues
+//    cp.async.bulk copies of the token's whole V row (all heads, 2 KiB) and its
+//    key-side row (K row, or the fp16 factor row) into a padded smem ring slot
+//    (odd-16-B row strides: ldmatrix conflict-free), completing on the slot's
+//    mbarrier (expect_tx); 3-deep ring, empty barriers returned by the warps;
+//  * consumer warp h (KV head h), per tile:
+//      S = q_h . k_t on mma.sync m16n8k16 with the query side STACKED in the
+//      16 A rows: rows g = high part, rows g+8 = low part (G <= 8), so one mma
+//      yields both halves and s = c[g] + c[g+8]:
+//        SVD tokens  A = q~_h (fp16 hi | lo),            B = fp16 factor rows
+//        exact keys  A = q_h  (bf16 p0 | p1) + (p2 | 0), B = bf16 K rows
+//      online softmax with a lazy rescale (only when a row max grows by > 8),
+//      O += P V with P stacked the same way (bf16 hi | lo), V via ldmatrix.trans;
+//  * epilogue: (m, l, o) partials; the last CTA of the sequence (ticket)
+//    merges them with the exact log-sum-exp rule and writes out and LSE.
+//
+// Work stream per sequence:
+//   token mode : the caller's token list (ascending ids), resident ones exact;
+//   chunk mode : [resident slots 0..R) ++ tokens of the selected chunks, with
+//                tokens of resident chunks dropped (they are in the first part),
+//                i.e. the same token set as the reference's sorted union.
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "kvb_common.cuh"
+#include "kvb_internal.h"
+
+namespace kvb {
+
+namespace {
+
+constexpr int kBD = 128;      // head dim
+constexpr int kBT = 16;       // tokens per tile
+constexpr int kBMaxKs = 10;   // SVD rank <= 160
+constexpr int kBMaxStages = 8;
+constexpr float kLazy = 8.f;  // rescale threshold (natural-log units)
+
+struct BulkParams {
+  // work stream
+  int mode;                   // 0 token list, 1 chunk list
+  const int32_t* items;       // token ids [B][cap] or chunk ids [B][cap]
+  const int32_t* nitems;      // [B] (token mode) or null (chunk mode: K)
+  int cap, K, cs;
+  const int32_t* res_count;   // [B]
+  // store
+  int G, H, n, W, Rcap, r, sgroups, svd;
+  const uint32_t* res_bm;
+  const int32_t* res_prefix;
+  const unsigned char* res_k;
+  const unsigned char* res_v;
+  const unsigned char* off_k;
+  const unsigned char* off_v;
+  const unsigned char* left;  // fp16 [B][n][sgroups][r]
+  const float* q;             // [B][H][G][D]
+  const float* qt2;           // [B][r/2][H*G][2]
+  float scale;
+  // outputs
+  float* pm;                  // [B][S][HG]
+  float* pl;
+  float* po;                  // [B][S][HG][D]
+  int* counters;              // [B] tickets, zero on entry, reset by the merger
+  float* out;                 // [B][HG][D]
+  float* lse;                 // [B][HG] or null
+  uint64_t* trace;            // profiling: [B][S][8] phase stamps or null
+  // chunk mode: the sorted token union (the reference's token_ids) is emitted
+  // here, each CTA writing its own share at merge-path ranks
+  const uint32_t* sel_bm;     // chunk mode: selected-chunk bitmap [B][Wc] (fused top-K) or null
+  int Wc;
+  int32_t* chunk_out;         // with sel_bm: ascending chunk ids [B][K] (optional)
+  int32_t* tok_out;           // [B][tcap] or null
+  int32_t* ntok_out;          // [B]
+  int tcap, Kb, C;
+  const int32_t* res_ids;     // [B][Rcap] ascending
+  int off_uni;
+  int nst;                    // ring slots (stages)
+  int ett;                    // tokens per exact-key tile (8 in SVD stores: compact slots)
+  int dbg;                    // profiling: 1 skip the math, 2 skip the copies
+  // geometry
+  int maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_bar, off_stage;
+};
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KVB_MSTAMP(k)                                                                       \
+  do {                                                                                      \
+    if (p.trace && tid == 0)                                                                \
+      p.trace[(size_t)gridDim.y * gridDim.x * 8 + (size_t)blockIdx.y * 4 + (k)] = gtimer(); \
+  } while (0)
+#define KVB_STAMP(ph)                                                                     \
+  do {                                                                                    \
+    if (p.trace && tid == 0)                                                              \
+      p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ph)] = gtimer();      \
+  } while (0)
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t u32h(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ uint32_t u32b(__nv_bfloat162 h) {
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void mma_h4(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_b4(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm4(uint32_t* r, uint32_t a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t* r, uint32_t a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ int lower_bound_i(const int32_t* a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+// bf16 parts of an fp32 pair: x = p0 + p1 + p2 exactly (3 parts), hi + lo (2)
+__device__ __forceinline__ void bparts(float x, float y, uint32_t* o, int parts) {
+  float rx = x, ry = y;
+  for (int i = 0; i < parts; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(rx, ry);
+    const float2 f = __bfloat1622float2(h);
+    o[i] = u32b(h);
+    rx -= f.x;
+    ry -= f.y;
+  }
+}
+
+// entry encoding: bits 0-29 index, bits 30-31 tier (0 resident slot, 1 offload token, 2 SVD token)
+constexpr uint32_t kTierShift = 30;
+
+template <int QW, int NKS>
+__global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ int red[33];
+  __shared__ int s_cnt[2];
+  const int b = blockIdx.y, split = blockIdx.x, S = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int H = p.H, G = p.G, HG = H * G;
+  const int nthr = blockDim.x;
+  KVB_STAMP(0);
+  // let the merge grid launch now; it waits for this grid's completion
+  pdl_trigger();
+  uint32_t* tab_ex = reinterpret_cast<uint32_t*>(sm + p.off_tab);
+  uint32_t* tab_sv = tab_ex + p.maxper;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + p.off_bar);
+  const int nst = p.nst, ett = p.ett;
+  uint64_t* empty = full + nst;
+  unsigned char* ring = sm + p.off_stage;
+
+  // ---- work share of this CTA -------------------------------------------------
+  // token mode: an even slice of the token list. Chunk mode: an even slice of
+  // the residents AND an even slice of the selected-chunk tokens, so the
+  // costlier exact-key tiles spread over all CTAs instead of the first few.
+  const int nres = p.res_count[b];
+  int i0, i1, r_lo = 0, n_rloc = 0, c_lo = 0;
+  if (p.mode == 0) {
+    const int P = p.nitems[b];
+    i0 = (int)(((long long)P * split) / S);
+    i1 = (int)(((long long)P * (split + 1)) / S);
+  } else {
+    const int KC = p.K * p.cs;
+    r_lo = (int)(((long long)nres * split) / S);
+    n_rloc = (int)(((long long)nres * (split + 1)) / S) - r_lo;
+    c_lo = (int)(((long long)KC * split) / S);
+    const int n_cloc = (int)(((long long)KC * (split + 1)) / S) - c_lo;
+    i0 = 0;
+    i1 = n_rloc + n_cloc;
+  }
+  if (tid == 0) {
+    s_cnt[0] = 0;
+    s_cnt[1] = 0;
+  }
+  if (tid < nst) {
+    mbar_init(full + tid, 1);
+    mbar_init(empty + tid, H);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  KVB_STAMP(1);
+  // consumers: issue the query-side loads now, convert after the prologue.
+  // Lane (g4, tig) holds B-fragment column g4, i.e. query qcol (QW = 4: the
+  // columns are [hi | lo] x 4 queries; QW = 8: one n-tile per part).
+  const int g4 = lane >> 2, tig = lane & 3;
+  const int qcol = QW == 4 ? (g4 & 3) : g4;
+  float qraw[8][4];
+  float2 qtraw[NKS > 0 ? NKS : 1][2];
+  if (warp < H) {
+    const bool ok = qcol < G;
+    const float* qh = p.q + (((size_t)b * H + warp) * G + (ok ? qcol : 0)) * kBD;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const float* rr = qh + ks * 16 + 2 * tig;
+      qraw[ks][0] = ok ? __ldg(rr) : 0.f;
+      qraw[ks][1] = ok ? __ldg(rr + 1) : 0.f;
+      qraw[ks][2] = ok ? __ldg(rr + 8) : 0.f;
+      qraw[ks][3] = ok ? __ldg(rr + 9) : 0.f;
+    }
+    const float* qt = p.qt2 + (size_t)b * HG * p.r;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int rr = ks * 16 + 2 * tig + 8 * hf;
+        qtraw[ks][hf] = (p.svd && ok && rr < p.r)
+                            ? *reinterpret_cast<const float2*>(qt + ((size_t)(rr >> 1) * HG + warp * G + qcol) * 2)
+                            : make_float2(0.f, 0.f);
+      }
+  }
+  const uint32_t* bm = p.res_bm + (size_t)b * p.W;
+  const int32_t* pre = p.res_prefix + (size_t)b * p.W;
+  pdl_wait();  // the selection (token / chunk list) of the previous kernel
+  // chunk mode: selected chunks (ascending), residents (ascending) and the
+  // prefix count of residents lying in selected chunks, in shared memory
+  int32_t* uc = reinterpret_cast<int32_t*>(sm + p.off_uni);  // [K]
+  int32_t* ur = uc + p.K;                                    // [Rcap]
+  int32_t* ud = ur + p.Rcap;                                 // [Rcap + 1]
+  if (p.mode == 1 && p.sel_bm) {
+    // ascending ids from the bitmap: each thread owns a run of words, one scan
+    const uint32_t* wb = p.sel_bm + (size_t)b * p.Wc;
+    const int per = (p.Wc + nthr - 1) / nthr;
+    const int w0 = min(p.Wc, tid * per), w1 = min(p.Wc, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(wb + w));
+    int tot;
+    int pos = block_excl_scan(cnt, red, &tot);
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = __ldcg(wb + w);
+      while (bits) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (pos < p.K) uc[pos] = w * 32 + bit;
+        ++pos;
+      }
+    }
+    for (int i = tot + tid; i < p.K; i += nthr) uc[i] = -1;
+    __syncthreads();
+    if (p.chunk_out && split == 0)
+      for (int i = tid; i < p.K; i += nthr) p.chunk_out[(size_t)b * p.K + i] = uc[i];
+  } else if (p.mode == 1) {
+    for (int i = tid; i < p.K; i += nthr) uc[i] = p.items[(size_t)b * p.cap + i];
+  }
+  if (p.mode == 1) {
+    for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
+    __syncthreads();
+    int run = 0;
+    for (int base = 0; base < nres; base += nthr) {
+      const int i = base + tid;
+      int f = 0;
+      if (i < nres) {
+        const int c = ur[i] / p.cs;
+        const int lb = lower_bound_i(uc, p.Kb, c);
+        f = (lb < p.Kb && uc[lb] == c) ? 1 : 0;
+      }
+      int tot;
+      const int ex = block_excl_scan(f, red, &tot);
+      if (i < nres) ud[i] = run + ex;
+      run += tot;
+    }
+    if (tid == 0) ud[nres] = run;
+    __syncthreads();
+    if (p.tok_out && split == 0 && tid == 0) {
+      const int lastlen = p.n - (p.C - 1) * p.cs;
+      const int atot = p.Kb * p.cs - ((p.Kb > 0 && uc[p.Kb - 1] == p.C - 1) ? p.cs - lastlen : 0);
+      const int total = nres + atot - ud[nres];
+      p.ntok_out[b] = total < p.tcap ? total : p.tcap;
+    }
+  }
+  for (int base = i0; base < i1; base += nthr) {
+    const int i = base + tid;
+    uint32_t e = 0;
+    int kind = -1;  // 0 exact, 1 svd
+    if (i < i1) {
+      if (p.mode == 0) {
+        const int t = p.items[(size_t)b * p.cap + i];
+        const uint32_t w = bm[t >> 5], bit = 1u << (t & 31);
+        if (w & bit) {
+          e = (uint32_t)(pre[t >> 5] + __popc(w & (bit - 1u)));
+          kind = 0;
+        } else {
+          e = (uint32_t)t | ((p.svd ? 2u : 1u) << kTierShift);
+          kind = p.svd ? 1 : 0;
+        }
+      } else if (i < n_rloc) {
+        const int gi = r_lo + i;
+        e = (uint32_t)gi;
+        kind = 0;
+        if (p.tok_out) {
+          const int r = ur[gi], c = r / p.cs;
+          const int lb = lower_bound_i(uc, p.Kb, c);
+          const bool inA = lb < p.Kb && uc[lb] == c;
+          const int pos = gi + lb * p.cs + (inA ? r - c * p.cs : 0) - ud[gi];
+          if (pos < p.tcap) p.tok_out[(size_t)b * p.tcap + pos] = r;
+        }
+      } else {
+        const int j = c_lo + i - n_rloc;
+        const int c = uc[j / p.cs];
+        const int t = c * p.cs + j % p.cs;
+        if (c >= 0 && t < p.n) {
+          const int lo = lower_bound_i(ur, nres, t);
+          if (!(lo < nres && ur[lo] == t)) {  // residents are served by the first part
+            e = (uint32_t)t | ((p.svd ? 2u : 1u) << kTierShift);
+            kind = p.svd ? 1 : 0;
+            const int pos = j + lo - ud[lo];
+            if (p.tok_out && pos < p.tcap) p.tok_out[(size_t)b * p.tcap + pos] = t;
+          }
+        }
+      }
+    }
+    int tot;
+    const int v = (kind == 0 ? 1 : 0) | (kind == 1 ? 1 << 16 : 0);
+    const int ex = block_excl_scan(v, red, &tot);
+    if (kind == 0) tab_ex[s_cnt[0] + (ex & 0xffff)] = e;
+    if (kind == 1) tab_sv[s_cnt[1] + (ex >> 16)] = e;
+    __syncthreads();
+    if (tid == 0) {
+      s_cnt[0] += tot & 0xffff;
+      s_cnt[1] += tot >> 16;
+    }
+    __syncthreads();
+  }
+  const int n_ex = s_cnt[0], n_sv = s_cnt[1];
+  KVB_STAMP(2);
+  if (p.trace && tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + 7] =
+        ((uint64_t)smid << 32) | (uint64_t)(n_ex + n_sv);
+  }
+  const int t_ex = (n_ex + ett - 1) / ett, t_sv = (n_sv + kBT - 1) / kBT;
+  const int ntiles = t_ex + t_sv;
+  const int vrow = p.vrow;
+  const int vbytes = H * kBD * 2;
+
+  // ---- production: tile k is staged by warp k % H (one lane per token) ---------------
+  // Issued by a consumer warp just before it consumes tile k - (stages - 1);
+  // the slot's previous tile k - stages has then been released by this warp,
+  // so the wait is only for slower warps. 8 warps = 2 per SM sub-partition,
+  // which leaves the consumers up to 255 registers.
+  const int lbytes = p.sgroups * p.r * 2;
+  // called for k = 0, 1, 2, ... in order by every warp (slot / round / owner
+  // tracked incrementally: no integer division in the loop)
+  int pk_stg = 0, pk_rnd = 0, pk_own = 0;
+  auto produce = [&](int k) {
+    const int stg = pk_stg, rnd = pk_rnd;
+    const bool mine = pk_own == warp;
+    if (++pk_stg == nst) {
+      pk_stg = 0;
+      ++pk_rnd;
+    }
+    if (++pk_own == H) pk_own = 0;
+    if (k >= ntiles || !mine) return;
+    if (rnd > 0) mbar_wait(empty + stg, (rnd - 1) & 1);
+    const bool sv = k >= t_ex;
+    const int tt = sv ? kBT : ett;
+    const int base = sv ? (k - t_ex) * kBT : k * ett;
+    const int cnt = min(tt, (sv ? n_sv : n_ex) - base);
+    const int j = lane & 15;
+    const uint32_t e = j < cnt ? (sv ? tab_sv : tab_ex)[base + j] : 0u;
+    const uint32_t tier = e >> kTierShift, idx = e & ((1u << kTierShift) - 1u);
+    const int krow = sv ? p.krow_sv : p.krow_ex;
+    const int kb = sv ? lbytes : vbytes;
+    uint32_t bytes = 0;
+    if (lane < 16 && j < cnt) bytes = (uint32_t)(vbytes + kb);
+    bytes = __reduce_add_sync(FULL, bytes);
+    if (p.dbg & 2) bytes = 0;
+    unsigned char* st = ring + (size_t)stg * p.stage_bytes;
+    // V rows past the tile's count are read by the P.V mma with p = 0: zero
+    // them (0 * stale bits could be NaN); K rows of those tokens only feed
+    // their own, masked, logit columns
+    for (int jj = cnt; jj < tt; ++jj)
+      for (int i = lane; i < vbytes / 16; i += 32)
+        reinterpret_cast<uint4*>(st + jj * vrow)[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) mbar_arrive_tx(full + stg, bytes);
+    __syncwarp();
+    if (j < cnt && !(p.dbg & 2)) {
+      const unsigned char* vsrc;
+      const unsigned char* ksrc;
+      if (tier == 0) {
+        const size_t off = ((size_t)b * p.Rcap + idx) * vbytes;
+        vsrc = p.res_v + off;
+        ksrc = p.res_k + off;
+      } else {
+        const size_t off = ((size_t)b * p.n + idx) * vbytes;
+        vsrc = p.off_v + off;
+        ksrc = tier == 1 ? p.off_k + off : p.left + ((size_t)b * p.n + idx) * lbytes;
+      }
+      if (lane < 16) bulk_g2s(st + j * vrow, vsrc, vbytes, full + stg);
+      else bulk_g2s(st + tt * vrow + j * krow, ksrc, kb, full + stg);
+    }
+  };
+  for (int k = 0; k < nst - 1; ++k) produce(k);
+  int c_stg = 0, c_rnd = 0;  // consumer ring position
+  auto next_slot = [&](int& stg, int& par) {
+    stg = c_stg;
+    par = c_rnd & 1;
+    if (++c_stg == nst) {
+      c_stg = 0;
+      ++c_rnd;
+    }
+  };
+
+  // ============================== consumers =====================================
+  // Transposed formulation: S^T[tokens x cols] = K_tile . Q^T and
+  // O^T[d x cols] += V_tile^T . P^T, the query side (split into fp16 hi|lo or
+  // bf16 p0|p1|p2 parts) living in the N = 8 columns of m16n8k16, so an
+  // mma covers 16 tokens x all parts of G <= 4 queries (QW = 4), or one part
+  // of G <= 8 (QW = 8). P^T reaches the B layout through movmatrix.trans.
+  constexpr int NTS = QW == 4 ? 1 : 2;  // SVD S: [hi|lo] or hi, lo
+  constexpr int NTE = QW == 4 ? 2 : 3;  // exact S: [p0|p1],[p2|0] or p0, p1, p2
+  constexpr int NTP = QW == 4 ? 1 : 2;  // P.V columns
+  const int h = warp;
+  const float scale = p.scale;
+  const int qa = QW == 4 ? 2 * (tig & 1) : 2 * tig;  // this lane's query pair (S/O columns)
+  float m_run[2] = {-INFINITY, -INFINITY};
+  float l_run[2] = {0.f, 0.f};
+  float o[8][NTP][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NTP; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[i][nt][c] = 0.f;
+  // ldmatrix lane geometry: A of S^T (non-trans, rows = tokens) and A of O^T (trans)
+  const int ka_row = (lane & 7) + ((lane >> 3) & 1) * 8, ka_col = (lane >> 4) * 16;
+  const int va_row = (lane & 7) + ((lane >> 4) << 3), va_col = ((lane >> 3) & 1) * 16;
+  const uint32_t ring_s = saddr(ring);
+
+  // softmax over the tile's logits s[token half][query] + O^T += V^T P^T
+  auto softmax_pv = [&](float (&sv)[2][2], int cnt, uint32_t st, int rmask) {
+    float mx[2];
+#pragma unroll
+    for (int th = 0; th < 2; ++th)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) sv[th][j] = g4 + 8 * th < cnt ? sv[th][j] * scale : -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      float m = fmaxf(sv[0][j], sv[1][j]);
+      m = fmaxf(m, __shfl_xor_sync(FULL, m, 4));
+      m = fmaxf(m, __shfl_xor_sync(FULL, m, 8));
+      m = fmaxf(m, __shfl_xor_sync(FULL, m, 16));
+      mx[j] = m;
+    }
+    // lazy rescale: only when some column's max grows past the threshold
+    if (__any_sync(FULL, mx[0] > m_run[0] + kLazy || mx[1] > m_run[1] + kLazy)) {
+      float al[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float mn = fmaxf(m_run[j], mx[j]);
+        al[j] = mn == -INFINITY ? 1.f : __expf(m_run[j] - mn);
+        m_run[j] = mn;
+        l_run[j] *= al[j];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NTP; ++nt) {
+          o[i][nt][0] *= al[0];
+          o[i][nt][1] *= al[1];
+          o[i][nt][2] *= al[0];
+          o[i][nt][3] *= al[1];
+        }
+    }
+    float ps[2] = {0.f, 0.f};
+#pragma unroll
+    for (int th = 0; th < 2; ++th)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float pv = sv[th][j] == -INFINITY ? 0.f : __expf(sv[th][j] - m_run[j]);
+        sv[th][j] = pv;
+        ps[j] += pv;
+      }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      float t = ps[j];
+      t += __shfl_xor_sync(FULL, t, 4);
+      t += __shfl_xor_sync(FULL, t, 8);
+      t += __shfl_xor_sync(FULL, t, 16);
+      l_run[j] += t;
+    }
+    // P^T B fragments (bf16 hi | lo parts) through movmatrix.trans
+    uint32_t bp[NTP][2];
+#pragma unroll
+    for (int th = 0; th < 2; ++th) {
+      uint32_t pr[2];
+      bparts(sv[th][0], sv[th][1], pr, 2);
+      if constexpr (QW == 4) {
+        bp[0][th] = movm_t((tig >> 1) ? pr[1] : pr[0]);
+      } else {
+        bp[0][th] = movm_t(pr[0]);
+        bp[1][th] = movm_t(pr[1]);
+      }
+    }
+    const uint32_t va = st + (uint32_t)((va_row & rmask) * vrow + va_col + h * kBD * 2);
+    uint32_t af[8][4];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) ldsm4t(af[mt], va + mt * 32);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NTP; ++nt)
+        mma_b4(o[mt][nt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], bp[nt][0], bp[nt][1]);
+  };
+  auto release = [&](int stg) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + stg);
+  };
+
+  // ---- exact-key tiles: B = q_h in 3 bf16 parts --------------------------------------
+  if (t_ex > 0) {
+    uint32_t be[8][NTE][2];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t lo[3], hi[3];
+      bparts(qraw[ks][0], qraw[ks][1], lo, 3);
+      bparts(qraw[ks][2], qraw[ks][3], hi, 3);
+      if constexpr (QW == 4) {
+        const bool first = g4 < 4;
+        be[ks][0][0] = first ? lo[0] : lo[1];
+        be[ks][0][1] = first ? hi[0] : hi[1];
+        be[ks][1][0] = first ? lo[2] : 0u;
+        be[ks][1][1] = first ? hi[2] : 0u;
+      } else {
+#pragma unroll
+        for (int pt = 0; pt < 3; ++pt) {
+          be[ks][pt][0] = lo[pt];
+          be[ks][pt][1] = hi[pt];
+        }
+      }
+    }
+    for (int k = 0; k < t_ex; ++k) {
+      produce(k + nst - 1);
+      int stg, par;
+      next_slot(stg, par);
+      mbar_wait(full + stg, par);
+      if (k == 0) KVB_STAMP(3);
+      const uint32_t st = ring_s + (uint32_t)(stg * p.stage_bytes);
+      if (p.dbg & 1) {
+        release(stg);
+        continue;
+      }
+      const int cnt = min(ett, n_ex - k * ett);
+      // half tiles (ett = 8): rows 8-15 alias rows 0-7 (finite, masked)
+      const uint32_t ka = st + (uint32_t)(ett * vrow + (ka_row & (ett - 1)) * p.krow_ex + ka_col +
+                                          h * kBD * 2);
+      // two independent accumulator chains per n-tile (even / odd k-steps)
+      float cs[2][NTE][4];
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+        for (int nt = 0; nt < NTE; ++nt)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) cs[c2][nt][c] = 0.f;
+      uint32_t af[8][4];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) ldsm4(af[ks], ka + ks * 32);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NTE; ++nt)
+          mma_b4(cs[ks & 1][nt], af[ks][0], af[ks][1], af[ks][2], af[ks][3], be[ks][nt][0], be[ks][nt][1]);
+      float sv[2][2];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < NTE; ++nt) v += cs[0][nt][e] + cs[1][nt][e];
+        if constexpr (QW == 4) v += __shfl_xor_sync(FULL, v, 2);
+        sv[e >> 1][e & 1] = v;
+      }
+      softmax_pv(sv, cnt, st, ett - 1);
+      release(stg);
+    }
+  }
+  // ---- SVD tiles: B = q~_h in fp16 hi | lo --------------------------------------------
+  if (NKS > 0 && t_sv > 0) {
+    uint32_t bq[NKS > 0 ? NKS : 1][NTS][2];
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const float2 v = qtraw[ks][hf];
+        const __half2 hi = __floats2half2_rn(v.x, v.y);
+        const float2 hf2 = __half22float2(hi);
+        const uint32_t lo = u32h(__floats2half2_rn(v.x - hf2.x, v.y - hf2.y));
+        if constexpr (QW == 4) {
+          bq[ks][0][hf] = g4 < 4 ? u32h(hi) : lo;
+        } else {
+          bq[ks][0][hf] = u32h(hi);
+          bq[ks][1][hf] = lo;
+        }
+      }
+    const int hgrp = h / (H / p.sgroups);
+    for (int k = t_ex; k < ntiles; ++k) {
+      produce(k + nst - 1);
+      int stg, par;
+      next_slot(stg, par);
+      mbar_wait(full + stg, par);
+      if (k == 0) KVB_STAMP(3);
+      const uint32_t st = ring_s + (uint32_t)(stg * p.stage_bytes);
+      if (p.dbg & 1) {
+        release(stg);
+        continue;
+      }
+      const int cnt = min(kBT, n_sv - (k - t_ex) * kBT);
+      const uint32_t ka = st + (uint32_t)(kBT * vrow + ka_row * p.krow_sv + ka_col + hgrp * p.r * 2);
+      // four independent accumulator chains (k-step mod 4): mma.sync latency
+      float cs[4][NTS][4];
+#pragma unroll
+      for (int c2 = 0; c2 < 4; ++c2)
+#pragma unroll
+        for (int nt = 0; nt < NTS; ++nt)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) cs[c2][nt][c] = 0.f;
+      uint32_t af[NKS > 0 ? NKS : 1][4];
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) ldsm4(af[ks], ka + ks * 32);
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks)
+#pragma unroll
+          for (int nt = 0; nt < NTS; ++nt)
+            mma_h4(cs[ks & 3][nt], af[ks][0], af[ks][1], af[ks][2], af[ks][3], bq[ks][nt][0], bq[ks][nt][1]);
+      float sv[2][2];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < NTS; ++nt) v += (cs[0][nt][e] + cs[1][nt][e]) + (cs[2][nt][e] + cs[3][nt][e]);
+        if constexpr (QW == 4) v += __shfl_xor_sync(FULL, v, 2);
+        sv[e >> 1][e & 1] = v;
+      }
+      softmax_pv(sv, cnt, st, kBT - 1);
+      release(stg);
+    }
+  }
+
+  KVB_STAMP(4);
+  // ---- partials (m, l, o) of this split ----------------------------------------------
+  const size_t pb = ((size_t)b * S + split) * HG + (size_t)h * G;
+  const bool writer = QW == 4 ? tig < 2 : true;
+  if (writer && g4 == 0) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (qa + j < G) {
+        p.pm[pb + qa + j] = m_run[j];
+        p.pl[pb + qa + j] = l_run[j];
+      }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v = o[mt][0][e];
+      if constexpr (QW == 4) v += __shfl_xor_sync(FULL, v, 2);
+      else v += o[mt][NTP - 1][e];
+      const int q = qa + (e & 1);
+      if (writer && q < G) p.po[(pb + q) * kBD + mt * 16 + g4 + 8 * (e >> 1)] = v;
+    }
+  KVB_STAMP(5);
+}
+
+// Exact LSE merge of the split partials: one CTA per (row = h*G + g, sequence),
+// thread d. Launched with programmatic stream serialization right behind
+// k5_attend_bulk (which triggers its dependents at entry), so its CTAs are
+// resident before the attention drains; griddepcontrol.wait then orders the
+// reads after the attention grid has completed and flushed.
+__global__ void __launch_bounds__(128, 8) k5_merge_rows(const float* __restrict__ pm,
+                                                     const float* __restrict__ pl,
+                                                     const float* __restrict__ po, int S, int HG,
+                                                     float* __restrict__ out, float* __restrict__ lse) {
+  const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const size_t base = (size_t)b * S * HG + row;
+  float m = -INFINITY, acc = 0.f, L = 0.f;
+  constexpr int CH = 8;  // splits per round: every load of a round in flight
+  for (int s0 = 0; s0 < S; s0 += CH) {
+    float mv[CH], lv[CH], ov[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int s2 = s0 + k;
+      const size_t gi = base + (size_t)s2 * HG;
+      mv[k] = s2 < S ? __ldcg(pm + gi) : -INFINITY;
+      lv[k] = s2 < S ? __ldcg(pl + gi) : 0.f;
+      ov[k] = s2 < S ? __ldcg(po + gi * 128 + d) : 0.f;
+    }
+    float mr = m;
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (lv[k] > 0.f) mr = fmaxf(mr, mv[k]);
+    const float al = (m == -INFINITY) ? 0.f : expf(m - mr);
+    acc *= al;
+    L *= al;
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (lv[k] > 0.f) {
+        const float w = expf(mv[k] - mr);
+        acc = fmaf(ov[k], w, acc);
+        L = fmaf(w, lv[k], L);
+      }
+    m = mr;
+  }
+  out[((size_t)b * HG + row) * 128 + d] = acc / L;
+  if (lse && d == 0) lse[(size_t)b * HG + row] = m + logf(L);
+}
+
+struct BulkGeom {
+  int splits, maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_uni, off_bar, off_stage, nst, ett;
+  size_t smem;
+};
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
+  BulkGeom g{};
+  const int B = s->d.batch, H = s->d.kv_heads;
+  const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
+  int splits = sm_count() / B;
+  const int tiles = (positions_cap + kBT - 1) / kBT;
+  if (splits > tiles) splits = tiles;
+  if (splits < 1) splits = 1;
+  g.splits = splits;
+  g.maxper = (positions_cap + splits - 1) / splits + 2;
+  auto odd16 = [](int x) {
+    x = (x + 15) & ~15;
+    if ((x / 16) % 2 == 0) x += 16;
+    return x;
+  };
+  g.vrow = odd16(H * kBD * 2);
+  g.krow_ex = g.vrow;
+  g.krow_sv = svd ? odd16(s->d.svd_groups * s->d.svd_rank * 2) : g.vrow;
+  // SVD stores: compact slots sized for 16 SVD tokens; exact-key tiles (the
+  // residents) then carry 8 tokens. Stores with exact offloaded keys: 16-token
+  // exact tiles.
+  g.ett = svd ? 8 : kBT;
+  if (svd) {
+    g.stage_bytes = (kBT * (g.vrow + g.krow_sv) + 127) & ~127;
+    if (g.ett * (g.vrow + g.krow_ex) > g.stage_bytes) g.ett = kBT;
+  }
+  if (g.ett == kBT) g.stage_bytes = (kBT * (g.vrow + std::max(g.krow_ex, g.krow_sv)) + 127) & ~127;
+  g.off_tab = 0;
+  g.off_uni = (2 * g.maxper * 4 + 127) & ~127;
+  g.off_bar = (g.off_uni + (K + 2 * s->d.max_resident + 1) * 4 + 127) & ~127;
+  g.off_stage = g.off_bar + 128;
+  const size_t room = 227 * 1024 - g.off_stage - 2048;  // static smem + slack
+  g.nst = std::min<int>(kBMaxStages, (int)(room / g.stage_bytes));
+  const int want = env_int("KVB_ATT_STAGES", 0);  // profiling override
+  if (want >= 2 && want < g.nst) g.nst = want;
+  g.smem = (size_t)g.off_stage + (size_t)g.nst * g.stage_bytes;
+  return g;
+}
+
+}  // namespace
+
+bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) {
+  if (s->d.kv_dtype != KVB_BF16 || s->d.head_dim != kBD || s->d.kv_heads > 8 || G > 8 || G < 1)
+    return false;
+  if (s->off_host) return false;
+  // SVD ranks: whole, even numbers of 16-wide k-steps up to 160 (compile-time k loop)
+  if (s->d.slow_kind == KVB_SLOW_SVD &&
+      (s->d.svd_rank % 32 != 0 || s->d.svd_rank > 16 * kBMaxKs ||
+       s->d.kv_heads % s->d.svd_groups != 0))
+    return false;
+  const BulkGeom g = bulk_geometry(s, positions_cap, K);
+  if (g.nst < 2) return false;
+  return g.smem <= 227 * 1024;
+}
+
+int attend_bulk_splits(const kvb_store* s, int positions_cap) {
+  return bulk_geometry(s, positions_cap).splits;
+}
+
+cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st) {
+  const int B = s->d.batch, H = s->d.kv_heads;
+  const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
+  const int positions_cap = a.mode == 0 ? a.cap : s->d.max_resident + a.K * s->d.chunk_size;
+  const BulkGeom g = bulk_geometry(s, positions_cap, a.mode == 1 ? a.K : 0);
+  if (g.splits != a.splits) return cudaErrorInvalidValue;
+  BulkParams p{};
+  p.mode = a.mode;
+  p.items = a.items;
+  p.nitems = a.nitems;
+  p.cap = a.cap;
+  p.K = a.K;
+  p.cs = s->d.chunk_size;
+  p.res_count = s->res_count;
+  p.G = a.G;
+  p.H = H;
+  p.n = s->d.n_tokens;
+  p.W = s->W;
+  p.Rcap = s->d.max_resident;
+  p.r = svd ? s->d.svd_rank : 0;
+  p.sgroups = svd ? s->d.svd_groups : 1;
+  p.svd = svd ? 1 : 0;
+  p.res_bm = s->res_bitmap;
+  p.res_prefix = s->res_prefix;
+  p.res_k = static_cast<const unsigned char*>(s->res_k);
+  p.res_v = static_cast<const unsigned char*>(s->res_v);
+  p.off_k = static_cast<const unsigned char*>(s->off_k_dev);
+  p.off_v = static_cast<const unsigned char*>(s->off_v_dev);
+  p.left = reinterpret_cast<const unsigned char*>(s->svd_left);
+  p.q = a.q;
+  p.qt2 = a.qt2;
+  p.scale = (float)(1.0 / sqrt((double)kBD));
+  p.pm = a.pm;
+  p.pl = a.pl;
+  p.po = a.po;
+  p.counters = a.counters;
+  p.out = a.out;
+  p.lse = a.lse;
+  p.trace = ((size_t)g.splits * B * 8 + B * 4 <= (size_t)kTraceWords) ? trace_buffer() : nullptr;
+  p.maxper = g.maxper;
+  p.vrow = g.vrow;
+  p.krow_ex = g.krow_ex;
+  p.krow_sv = g.krow_sv;
+  p.stage_bytes = g.stage_bytes;
+  p.off_tab = g.off_tab;
+  p.off_bar = g.off_bar;
+  p.off_stage = g.off_stage;
+  p.off_uni = g.off_uni;
+  p.tok_out = a.mode == 1 ? a.tok_out : nullptr;
+  p.sel_bm = a.mode == 1 ? a.sel_bm : nullptr;
+  p.Wc = s->Wc;
+  p.chunk_out = a.chunk_out;
+  p.ntok_out = a.ntok_out;
+  p.tcap = a.tcap;
+  p.C = s->C;
+  p.Kb = a.K < s->C ? a.K : s->C;
+  p.res_ids = s->res_ids;
+  p.nst = g.nst;
+  p.ett = g.ett;
+  const int dbg = env_int("KVB_ATT_DBG", 0);  // profiling only
+  p.dbg = dbg;
+  count_launch(2);
+  const int nks = svd ? s->d.svd_rank / 16 : 0;
+  const void* fn = nullptr;
+#define KVB_BULK_PICK(Q)                                                       \
+  switch (nks) {                                                               \
+    case 0: fn = (const void*)k5_attend_bulk<Q, 0>; break;                     \
+    case 2: fn = (const void*)k5_attend_bulk<Q, 2>; break;                     \
+    case 4: fn = (const void*)k5_attend_bulk<Q, 4>; break;                     \
+    case 6: fn = (const void*)k5_attend_bulk<Q, 6>; break;                     \
+    case 8: fn = (const void*)k5_attend_bulk<Q, 8>; break;                     \
+    case 10: fn = (const void*)k5_attend_bulk<Q, 10>; break;                   \
+    default: return cudaErrorNotSupported;                                     \
+  }
+  if (a.G <= 4) {
+    KVB_BULK_PICK(4)
+  } else {
+    KVB_BULK_PICK(8)
+  }
+#undef KVB_BULK_PICK
+  ensure_smem(fn, g.smem);
+  void* args[] = {&p};
+  cudaError_t le = launch_pdl(fn, dim3(g.splits, B), dim3(H * 32), g.smem, st, args);
+  if (le != cudaSuccess) return le;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(H * a.G, B);
+  cfg.blockDim = dim3(kBD);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
+                            (const float*)p.po, g.splits, H * a.G, p.out, p.lse);
+  return cudaGetLastError();
+}
+
+}  // namespace kvb

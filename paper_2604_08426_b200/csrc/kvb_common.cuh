@@ -112,4 +112,12 @@ __device__ __forceinline__ int block_excl_scan(int v, int* red, int* total) {
   return ex;
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream
+// launch now / wait until the previous kernel's grid completed and flushed.
+// Both are no-ops when the launch carried no programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 }  // namespace kvb

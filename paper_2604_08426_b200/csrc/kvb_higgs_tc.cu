@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y;
+  pdl_trigger();
   if (threadIdx.x < 16) {
     const float x = cb[2 * threadIdx.x], y = cb[2 * threadIdx.x + 1];
     const __half2 hh = __floats2half2_rn(x, y);

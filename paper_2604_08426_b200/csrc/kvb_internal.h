@@ -33,6 +33,20 @@ struct kvb_store {
   int32_t* res_ids = nullptr;    // [B][max_resident] sorted resident tokens
   int32_t* res_count = nullptr;  // [B]
   uint32_t* res_bitmap = nullptr;  // [B][W]
+  // K1 -> K2a -> K2b scratch owned by the store, zero at creation and re-zeroed
+  // by K2b after use (no memset nodes in the decode step). One decode step per
+  // store at a time (the store's side stream and events are per store too).
+  uint32_t* k2_hist = nullptr;     // [B][2048] top-11-bit key histogram
+  int32_t* k2_meta = nullptr;      // [B][4] threshold bin / counts
+  int32_t* k2_overflow = nullptr;  // [B]
+  bool k2_dirty = false;           // a failed launch may have left scratch dirty
+  // fused scan + top-K (kvb_fuse.cuh): selected-chunk bitmap, threshold-bin
+  // candidates and counters, same self-cleaning discipline
+  uint32_t* sel_bm = nullptr;      // [B][Wc]
+  uint32_t* sel_ckey = nullptr;    // [B][kFuseCap]
+  int32_t* sel_cid = nullptr;      // [B][kFuseCap]
+  int32_t* sel_ctr = nullptr;      // [B][4]
+  int Wc = 0;                      // ceil(C / 32)
   int32_t* res_prefix = nullptr;   // [B][W] residents before word w
   void* res_k = nullptr;         // [B][max_resident][E]
   void* res_v = nullptr;
@@ -46,7 +60,7 @@ struct kvb_store {
   bool off_host = false;
   // side stream + events for the fork/join of decode-step work (prep || scan)
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sel = nullptr, ev_union = nullptr;
 };
 
 namespace kvb {
@@ -54,6 +68,12 @@ namespace kvb {
 void set_error(const std::string& msg);
 kvb_status cuda_status(cudaError_t e, const char* what);
 void count_launch(int n = 1);
+// device phase-stamp trace of the bulk attention kernel (profiling only)
+bool trace_enable(int on);
+uint64_t* trace_buffer();  // null when disabled
+int64_t trace_read(uint64_t* host, int64_t max_words);
+constexpr int64_t kTraceWords = 1 << 16;
+constexpr int kFuseCap = 8192;  // threshold-bin candidates staged by the fused top-K
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
 cudaError_t ensure_smem(const void* func, size_t bytes);
 // Number of SMs of the current device and resident CTAs/SM for a kernel.
@@ -63,8 +83,11 @@ int resident_ctas(const void* func, int threads, size_t smem);
 // ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
 // hist (may be null): [B][2048] uint32, zeroed by the caller; receives the
 // histogram of the top 11 bits of the score keys (sum aggregation only).
+struct FuseSel;
+// fuse (optional): top-K fused into the scan tail (kvb_fuse.cuh); sum only
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st);
+                               float* scores, uint32_t* hist, cudaStream_t st,
+                               const FuseSel* fuse = nullptr);
 constexpr int kTopHistBins = 2048;
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);
@@ -91,6 +114,7 @@ struct SelectLaunch {
   float* sel_scores = nullptr;  // [B][K] scores of the selected items (optional)
   const uint32_t* hist = nullptr;  // [B][2048] top-11-bit key histogram from K1 (optional)
   int id_offset = 0;            // added to emitted item ids (sharding)
+  int sorted_ids = 0;           // emit the selected set in ascending id order (K2a/K2b path)
 };
 // Token union for an explicit chunk list (global ids, offset mapped).
 cudaError_t launch_tokens_from_chunks(const kvb_store* s, const int32_t* chunk_ids, int k,
@@ -103,6 +127,15 @@ size_t select_smem_bytes(const kvb_store* s, int K, int mode);
 size_t select2_ws_bytes(const kvb_store* s, int K);
 cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, cudaStream_t st,
                            int32_t** overflow_out);
+// Sorted token union from ascending chunk ids (K2b sorted output) and the
+// sorted resident ids: merge-path ranks, no bitmap pass.
+cudaError_t launch_union_sorted(const kvb_store* s, const int32_t* chunk_ids, int k,
+                                int32_t* token_ids, int32_t* n_tokens, int cap, cudaStream_t st);
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; it must griddepcontrol.wait before reading
+// the predecessor's output.
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       void** args);
 
 // Ascending list of the tokens of the selected chunks (Appendix-E stage 2).
 cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,
@@ -134,6 +167,34 @@ cudaError_t launch_attend_wh(const kvb_store* s, const float* q, int G, const in
                              const int32_t* ntok, int cap, const float* qt2, float* pm, float* pl,
                              float* po, int splits, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
+// bulk-copy pipelined attention (kvb_attend_bulk.cu). mode 0: explicit token
+// list (items = token ids, nitems = counts); mode 1: residents + the tokens of
+// `K` selected chunks per sequence (items = chunk ids, row stride cap).
+struct BulkLaunch {
+  int mode;
+  const int32_t* items;
+  const int32_t* nitems;
+  int cap, K, G;
+  const float* q;
+  const float* qt2;
+  float *pm, *pl, *po;
+  int* counters;
+  float* out;
+  float* lse;
+  int splits;
+  const uint32_t* sel_bm = nullptr;  // mode 1: selected-chunk bitmap [B][Wc] instead of items
+  int32_t* chunk_out = nullptr;      // mode 1 + sel_bm: ascending chunk ids out [B][K] (optional)
+  int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
+  int32_t* ntok_out = nullptr;  // [B]
+  int tcap = 0;
+};
+bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K = 0);
+int attend_bulk_splits(const kvb_store* s, int positions_cap);
+cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st);
+// decode-step attention over residents + selected chunks (chunk ids [B][K])
+cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
+                                 int K, cudaStream_t st, const uint32_t* sel_bm = nullptr,
+                                 int32_t* chunk_out = nullptr);
 // the two halves of launch_attend: per-step query prep, then the attention
 cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);

@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(256) k2a_split(const float* __restrict__ score
   __shared__ int s_tb, s_kb, s_nb;
   const int b = blockIdx.y, lane = threadIdx.x & 31;
   const int Kc = K < M ? K : M;
+  pdl_trigger();
+  pdl_wait();  // scores + histogram of the scan
   hist_threshold(hist + (size_t)b * kTopHistBins, Kc, red, &s_tb, &s_kb, &s_nb);
   const uint32_t tb = (uint32_t)s_tb;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -480,8 +482,20 @@ struct K2bParams {
   int cap;
   const uint32_t* res_bitmap;
   int n, cs, W, P;
-  int32_t* overflow;     // [B] set when K2a overflowed (caller falls back)
+  int32_t* overflow;     // [B] 1 when K2a overflowed (in-kernel radix fallback ran)
+  int sorted;            // out_ids in ascending id order (set semantics)
+  uint32_t* hist;        // [B][2048] store scratch: re-zeroed here after K2a consumed it
+  K2Meta* meta_rw;       // [B] store scratch: re-zeroed here after reading
 };
+
+// Rewrite row `ids` (K distinct ids < M, any order) in ascending order via a
+// bitmap over [0, M) in shared memory `bm` (>= ceil(M/32) words).
+__device__ __forceinline__ void sort_ids_bitmap(int32_t* ids, int K, int M, uint32_t* bm,
+                                                int* red, int* s_n) {
+  __syncthreads();
+  token_union(nullptr, 0, (M + 31) / 32, bm, [&](int r) { return (int)ids[r]; }, K, 0, 1, M,
+              nullptr, 0, M, ids, K, s_n, nullptr, red);
+}
 
 __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -490,8 +504,19 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
   __shared__ int s_gt, s_eq, s_cnt;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x;
+  pdl_trigger();
+  pdl_wait();  // K2a's split
   const K2Meta mt = p.meta[b];
   const int K = p.K < p.M ? p.K : p.M;
+  // self-cleaning scratch: K2a (complete) was the histogram's last reader and
+  // the meta counters are in registers now
+  if (p.hist)
+    for (int i = tid; i < kTopHistBins; i += nthr) p.hist[(size_t)b * kTopHistBins + i] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    p.meta_rw[b] = K2Meta{0, 0, 0, 0};
+    p.overflow[b] = mt.ncand > p.cand_cap ? 1 : 0;
+  }
   uint64_t* keys64 = reinterpret_cast<uint64_t*>(smem_raw);                 // [P] rank sort
   const size_t selb = std::max((size_t)p.P * 8, (size_t)((p.K + 3) & ~3) * 4);
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + selb);              // [W]
@@ -499,7 +524,6 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
   if (mt.ncand > p.cand_cap) {
     // pathological ties (> cand_cap keys share the top 11 bits): exact 4-pass
     // radix select over every key of this sequence, in this CTA
-    if (tid == 0) p.overflow[b] = 1;
     SelParams q{};
     q.scores = p.scores;
     q.M_stride = p.M;
@@ -521,6 +545,10 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     q.id_offset = 0;
     q.sel_scores = nullptr;
     select_body(q, smem_raw);
+    if (p.sorted && !p.rank_order) {
+      __shared__ int s_n;
+      sort_ids_bitmap(p.out_ids + (size_t)b * p.K, K, p.M, bm, red, &s_n);
+    }
     return;
   }
   const uint64_t* cd = p.cand + (size_t)b * p.cand_cap;
@@ -606,6 +634,13 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
       }
     for (int r = tid; r < p.K; r += nthr)
       p.out_ids[(size_t)b * p.K + r] = r < K ? (int32_t)(0xffffffffu - (uint32_t)keys64[r]) : -1;
+  } else if (p.sorted) {
+    for (int r = K + tid; r < p.K; r += nthr) p.out_ids[(size_t)b * p.K + r] = -1;
+    __syncthreads();
+    // ascending chunk ids straight from the bitmap (token_union with cs = 1)
+    __shared__ int s_n;
+    token_union(nullptr, 0, (p.M + 31) / 32, bm, [&](int r) { return (int)ids[r]; }, K, 0, 1, p.M,
+                nullptr, 0, p.M, p.out_ids + (size_t)b * p.K, K, &s_n, nullptr, red);
   } else if (p.out_ids != p.sel) {
     for (int r = tid; r < p.K; r += nthr)
       p.out_ids[(size_t)b * p.K + r] = r < K ? ids[r] : -1;
@@ -641,19 +676,26 @@ cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, 
                            int32_t** overflow_out) {
   const int B = s->d.batch;
   char* w = static_cast<char*>(ws);
-  K2Meta* meta = reinterpret_cast<K2Meta*>(w);
+  // (meta + overflow live in the store's self-cleaning scratch; the workspace
+  // layout keeps their former slots so its size is unchanged)
   w += ((B * sizeof(K2Meta) + 255) & ~size_t(255));
-  int32_t* overflow = reinterpret_cast<int32_t*>(w);
   w += ((B * 4 + 255) & ~size_t(255));
+  K2Meta* meta = reinterpret_cast<K2Meta*>(s->k2_meta);
+  int32_t* overflow = s->k2_overflow;
   int32_t* sel = reinterpret_cast<int32_t*>(w);
   w += (((size_t)B * a.K * 4 + 255) & ~size_t(255));
   uint64_t* cand = reinterpret_cast<uint64_t*>(w);
-  cudaMemsetAsync(meta, 0, B * sizeof(K2Meta), st);
-  cudaMemsetAsync(overflow, 0, B * 4, st);
   const int per_seq = std::max(1, sm_count() * 2 / B);
   count_launch(2);
-  k2a_split<<<dim3(per_seq, B), 256, 0, st>>>(a.scores, a.M_stride, a.K, a.hist, meta, sel, a.K,
-                                              cand, kCandCap);
+  {
+    const float* sc = a.scores;
+    int M = a.M_stride, K = a.K, cap = kCandCap, stride = a.K;
+    const uint32_t* hist = a.hist;
+    void* args[] = {(void*)&sc, (void*)&M, (void*)&K, (void*)&hist, (void*)&meta, (void*)&sel,
+                    (void*)&stride, (void*)&cand, (void*)&cap};
+    cudaError_t e = launch_pdl((const void*)k2a_split, dim3(per_seq, B), dim3(256), 0, st, args);
+    if (e != cudaSuccess) return e;
+  }
   K2bParams p{};
   p.meta = meta;
   p.sel = sel;
@@ -673,13 +715,112 @@ cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, 
   p.W = s->W;
   p.P = a.rank_order ? next_pow2(a.K < 1 ? 1 : a.K) : 0;
   p.overflow = overflow;
+  p.sorted = a.sorted_ids;
+  p.hist = const_cast<uint32_t*>(a.hist);
+  p.meta_rw = meta;
   // room for the in-kernel radix fallback too: max(P*8, K*4) + bitmap
   const int Pf = next_pow2(a.K < 1 ? 1 : a.K);
   const size_t smem = std::max((size_t)(a.rank_order ? Pf : 0) * 8, (size_t)((a.K + 3) & ~3) * 4) +
                       (size_t)s->W * 4;
   ensure_smem((const void*)k2b_finish, smem);
-  k2b_finish<<<B, kSelThreads, smem, st>>>(p);
+  void* args[] = {(void*)&p};
+  cudaError_t e = launch_pdl((const void*)k2b_finish, dim3(B), dim3(kSelThreads), smem, st, args);
   if (overflow_out) *overflow_out = overflow;
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// Sorted token union by merge-path ranks (decode step, side stream). Inputs:
+// ascending chunk ids (-1 padded) and the ascending resident ids. A token of
+// a selected chunk at stream position idx = j*cs + o lands at
+// idx + #(residents < x) - #(residents < x that lie in selected chunks);
+// a resident r_i at i + #(chunk tokens < r_i) - #(residents before i in
+// selected chunks). Same output as the bitmap union (np.unique order).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lower_bound_i(const int32_t* a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k2_union_sorted(const int32_t* __restrict__ cid, int K,
+                                                       const int32_t* __restrict__ res_ids,
+                                                       const int32_t* __restrict__ res_count, int Rcap,
+                                                       const uint32_t* __restrict__ res_bm, int W, int n,
+                                                       int cs, int C, int32_t* __restrict__ tok,
+                                                       int32_t* __restrict__ ntok, int cap) {
+  extern __shared__ int32_t usm[];
+  __shared__ int red[33];
+  __shared__ int s_kb;
+  const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  int32_t* sc = usm;             // [K] chunk ids
+  int32_t* sr = sc + K;          // [Rcap] residents
+  int32_t* sd = sr + Rcap;       // [Rcap + 1] residents-in-selected-chunks prefix
+  const int R = res_count[b];
+  int kv = 0;
+  for (int i = tid; i < K; i += nthr) {
+    const int c = cid[(size_t)b * K + i];
+    sc[i] = c;
+    kv += c >= 0 ? 1 : 0;
+  }
+  for (int i = tid; i < R; i += nthr) sr[i] = res_ids[(size_t)b * Rcap + i];
+  int tot;
+  block_excl_scan(kv, red, &tot);
+  if (tid == 0) s_kb = tot;
+  __syncthreads();
+  const int Kb = s_kb;  // valid ids are the ascending prefix
+  int run = 0;
+  for (int base = 0; base < R; base += nthr) {
+    const int i = base + tid;
+    int f = 0;
+    if (i < R) {
+      const int c = sr[i] / cs;
+      const int lb = lower_bound_i(sc, Kb, c);
+      f = (lb < Kb && sc[lb] == c) ? 1 : 0;
+    }
+    const int ex = block_excl_scan(f, red, &tot);
+    if (i < R) sd[i] = run + ex;
+    run += tot;
+  }
+  if (tid == 0) sd[R] = run;
+  __syncthreads();
+  int32_t* out = tok + (size_t)b * cap;
+  for (int i = tid; i < R; i += nthr) {
+    const int r = sr[i], c = r / cs;
+    const int lb = lower_bound_i(sc, Kb, c);
+    const bool inA = lb < Kb && sc[lb] == c;
+    const int pos = i + lb * cs + (inA ? r - c * cs : 0) - sd[i];
+    if (pos < cap) out[pos] = r;
+  }
+  const uint32_t* bm = res_bm + (size_t)b * W;
+  for (int idx = tid; idx < Kb * cs; idx += nthr) {
+    const int x = sc[idx / cs] * cs + idx % cs;
+    if (x >= n || ((bm[x >> 5] >> (x & 31)) & 1u)) continue;
+    const int lo = lower_bound_i(sr, R, x);
+    const int pos = idx + lo - sd[lo];
+    if (pos < cap) out[pos] = x;
+  }
+  if (tid == 0) {
+    const int lastlen = n - (C - 1) * cs;
+    const int atot = Kb * cs - ((Kb > 0 && sc[Kb - 1] == C - 1) ? cs - lastlen : 0);
+    const int total = R + atot - sd[R];
+    ntok[b] = total < cap ? total : cap;
+  }
+}
+
+cudaError_t launch_union_sorted(const kvb_store* s, const int32_t* chunk_ids, int k,
+                                int32_t* token_ids, int32_t* n_tokens, int cap, cudaStream_t st) {
+  const int Rcap = s->d.max_resident;
+  const size_t smem = (size_t)(k + 2 * Rcap + 1) * 4;
+  ensure_smem((const void*)k2_union_sorted, smem);
+  count_launch();
+  k2_union_sorted<<<s->d.batch, 256, smem, st>>>(chunk_ids, k, s->res_ids, s->res_count, Rcap,
+                                                 s->res_bitmap, s->W, s->d.n_tokens,
+                                                 s->d.chunk_size, s->C, token_ids, n_tokens, cap);
   return cudaGetLastError();
 }
 
@@ -743,7 +884,10 @@ cudaError_t launch_tokens_from_chunks(const kvb_store* s, const int32_t* chunk_i
   const size_t smem = (size_t)s->W * 4;
   ensure_smem((const void*)k2_union_chunks, smem);
   count_launch();
-  k2_union_chunks<<<s->d.batch, kSelThreads, smem, st>>>(chunk_ids, k, chunk_offset, s->C,
+  // 128 threads x <= 32 registers: fits beside a k5_attend_bulk CTA (8 warps x
+  // 232 registers: 2 per SM sub-partition) on one SM, so the decode step's
+  // side-stream union never delays it
+  k2_union_chunks<<<s->d.batch, 128, smem, st>>>(chunk_ids, k, chunk_offset, s->C,
                                                           s->res_bitmap, s->W, s->d.chunk_size,
                                                           s->d.n_tokens, token_ids, n_tokens, cap);
   return cudaGetLastError();

@@ -161,7 +161,11 @@ def test_decode_step_matches_select_then_attend():
     _, _, tok, ntok = dev.select(q, K)
     o_ref, _ = dev.attend(q, tok, ntok)
     assert torch.equal(plan.ntok, ntok)
-    assert torch.allclose(o_step, o_ref, rtol=0, atol=0)
+    for b in range(B):
+        assert torch.equal(plan.tok[b, : int(ntok[b])], tok[b, : int(ntok[b])])
+    # same token set; the decode step walks residents + selected chunks, the
+    # token-list attention walks the sorted union: fp32 reassociation only
+    assert float((o_step - o_ref).norm() / o_ref.norm()) < 1e-5
 
 
 @pytest.mark.parametrize("seed", [0, 1])

@@ -11,7 +11,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1
 echo "tests rc=$?" >> $O/gpu_tests.log
 timeout 900 python bench.py --steps 30 --warmup 3 ${BENCH_ARGS:-} > $O/bench.json 2> $O/bench.err
 echo "bench rc=$?" >> $O/bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k1|k2|k5|prep|merge|kvb" -c 400 --csv \
   --log-file $O/launches.csv python bench.py --profile-steps 2 --layers 4 > $O/launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"${NCU_KERNELS:-k1_dense_sum|k5_attend_wh|k2b_finish|k2a_split}" -s 8 -c 4 \

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Quick GPU iteration: build, smoke, GPU tests, one bench line. Usage: bash tools/gpu_quick.sh TAG [pytest -k expr]
+set -u
+TAG=${1:-quick}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1
+echo "smoke rc=$?" >> $O/smoke.log
+if [ -n "${2:-}" ]; then K="-k $2"; else K=""; fi
+timeout 900 python -m pytest tests -m gpu -x -q $K > $O/gpu_tests.log 2>&1
+echo "tests rc=$?" >> $O/gpu_tests.log
+timeout 900 python bench.py --steps 20 --warmup 3 ${BENCH_ARGS:-} > $O/bench.json 2> $O/bench.err
+echo "bench rc=$?" >> $O/bench.err
+tail -3 $O/smoke.log $O/gpu_tests.log $O/bench.err
+cat $O/bench.json
