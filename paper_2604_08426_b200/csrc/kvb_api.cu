@@ -15,7 +15,6 @@
 #include <vector>
 
 #include "kvb_common.cuh"
-#include "kvb_fuse.cuh"
 #include "kvb_internal.h"
 
 namespace kvb {
@@ -210,10 +209,7 @@ void free_store(kvb_store* s) {
   cudaFree(s->res_ids);
   cudaFree(s->res_count);
   cudaFree(s->k2_hist);
-  cudaFree(s->sel_bm);
-  cudaFree(s->sel_ckey);
-  cudaFree(s->sel_cid);
-  cudaFree(s->sel_ctr);
+
   cudaFree(s->k2_meta);
   cudaFree(s->k2_overflow);
   cudaFree(s->res_bitmap);
@@ -334,11 +330,6 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
   s->Wc = (s->C + 31) / 32;
-  if ((st = dalloc(&s->sel_bm, B * s->Wc, "selection bitmap")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->sel_ckey, B * kFuseCap, "selection candidates")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->sel_cid, B * kFuseCap, "selection candidate ids")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->sel_ctr, B * 4, "selection counters")) != KVB_OK) return bail(st);
-  cudaMemset(s->sel_ctr, 0, B * 4 * sizeof(int32_t));
   cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
   cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
   cudaMemset(s->res_count, 0, B * sizeof(int32_t));
@@ -868,35 +859,31 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   const int K = sel->n_select;
   const bool chunk_path =
       attend_bulk_supported(s, L.G, s->d.max_resident + K * s->d.chunk_size, K);
-  if (chunk_path && sel->aggregation == KVB_AGG_SUM && s->d.landmark_kind == KVB_LM_DENSE) {
-    // scan + top-K in one kernel (kvb_fuse.cuh) -> attention over the bitmap
-    float* sc = static_cast<float*>(sws);  // select workspace starts with [B][C] scores
+  const bool tc_scan = !sel->exact_scores && higgs_tc_supported(s);
+  // attention-side top-K: every attention CTA streams the sequence's C scores
+  // once (L2), cheap for chunked landmarks; at chunk 1 (C = n) the whole-GPU
+  // K2a split + per-sequence K2b finish is used instead
+  if (chunk_path && sel->aggregation == KVB_AGG_SUM && s->C <= 32768 &&
+      (s->d.landmark_kind == KVB_LM_DENSE || tc_scan)) {
+    // scan (scores + top-11-bit key histogram) -> attention whose prologue
+    // runs the exact top-K (kvb_fuse.cuh); no separate selection kernels
+    Carve sv(sws, sb);
+    float* sc = sv.take<float>((size_t)s->d.batch * s->C);
+    (void)sv.take<int32_t>(1);
+    void* tcws = sv.take<char>(higgs_tc_ws_bytes(s));
     if (s->k2_dirty) {
       KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
-      KVB_CUDA(cudaMemsetAsync(s->sel_ctr, 0, sizeof(int32_t) * s->d.batch * 4, st), "ctr reset");
       s->k2_dirty = false;
     }
-    FuseSel fz{};
-    fz.bm = s->sel_bm;
-    fz.ckey = s->sel_ckey;
-    fz.cid = s->sel_cid;
-    fz.ctr = s->sel_ctr;
-    fz.Wc = s->Wc;
-    fz.cap = kFuseCap;
-    fz.K = K < s->C ? K : s->C;
-    fz.on = 1;
-    fz.trace = trace_buffer() ? trace_buffer() + kTraceWords / 2 : nullptr;  // profiling hook
     s->k2_dirty = true;
-    cudaError_t fe = launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, &fz);
-    if (fe == cudaSuccess) {
-      s->k2_dirty = false;
-      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
-      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, s->sel_bm, chunk_ids), "sparse attention");
-      return KVB_OK;
-    }
-    if (fe != cudaErrorNotSupported) KVB_CUDA(fe, "fused landmark scan + top-K");
-    (void)cudaGetLastError();
+    if (tc_scan)
+      KVB_CUDA(launch_score_higgs_tc(s, q, L.G, sc, tcws, s->k2_hist, st), "HIGGS tensor-core scoring");
+    else
+      KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st), "landmark scoring");
+    KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+    KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
     s->k2_dirty = false;
+    return KVB_OK;
   }
   bool sorted = false;
   if ((ks = select_impl(s, q, &a2, cid, nullptr, chunk_path ? nullptr : token_ids,

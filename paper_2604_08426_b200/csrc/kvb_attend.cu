@@ -838,7 +838,8 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
 }
 
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
-                                 int K, cudaStream_t st, const uint32_t* sel_bm, int32_t* chunk_out) {
+                                 int K, cudaStream_t st, const float* sel_scores,
+                                 uint32_t* sel_hist, int32_t* chunk_out) {
   const int G = a.G;
   const int pos_cap = s->d.max_resident + K * s->d.chunk_size;
   if (!attend_bulk_supported(s, G, pos_cap, K)) return cudaErrorNotSupported;
@@ -863,7 +864,8 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
   bl.tok_out = const_cast<int32_t*>(a.token_ids);  // decode step: an output here
   bl.ntok_out = const_cast<int32_t*>(a.n_tokens);
   bl.tcap = a.cap;
-  bl.sel_bm = sel_bm;
+  bl.sel_scores = sel_scores;
+  bl.sel_hist = sel_hist;
   bl.chunk_out = chunk_out;
   return launch_attend_bulk(s, bl, st);
 }

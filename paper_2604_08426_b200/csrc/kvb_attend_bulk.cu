@@ -37,6 +37,7 @@
 #include <cstdlib>
 
 #include "kvb_common.cuh"
+#include "kvb_fuse.cuh"
 #include "kvb_internal.h"
 
 namespace kvb {
@@ -78,9 +79,10 @@ struct BulkParams {
   uint64_t* trace;            // profiling: [B][S][8] phase stamps or null
   // chunk mode: the sorted token union (the reference's token_ids) is emitted
   // here, each CTA writing its own share at merge-path ranks
-  const uint32_t* sel_bm;     // chunk mode: selected-chunk bitmap [B][Wc] (fused top-K) or null
+  const float* sel_scores;    // chunk mode: scan scores [B][C] -> top-K here (kvb_fuse.cuh)
+  const uint32_t* sel_hist;   // [B][2048] top-11-bit key histogram of those scores
   int Wc;
-  int32_t* chunk_out;         // with sel_bm: ascending chunk ids [B][K] (optional)
+  int32_t* chunk_out;         // with sel_scores: ascending chunk ids [B][K] (optional)
   int32_t* tok_out;           // [B][tcap] or null
   int32_t* ntok_out;          // [B]
   int tcap, Kb, C;
@@ -279,23 +281,34 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
   }
   const uint32_t* bm = p.res_bm + (size_t)b * p.W;
   const int32_t* pre = p.res_prefix + (size_t)b * p.W;
-  pdl_wait();  // the selection (token / chunk list) of the previous kernel
   // chunk mode: selected chunks (ascending), residents (ascending) and the
   // prefix count of residents lying in selected chunks, in shared memory
   int32_t* uc = reinterpret_cast<int32_t*>(sm + p.off_uni);  // [K]
   int32_t* ur = uc + p.K;                                    // [Rcap]
   int32_t* ud = ur + p.Rcap;                                 // [Rcap + 1]
-  if (p.mode == 1 && p.sel_bm) {
-    // ascending ids from the bitmap: each thread owns a run of words, one scan
-    const uint32_t* wb = p.sel_bm + (size_t)b * p.Wc;
+  if (p.mode == 1)  // residents are store state: load them before waiting on the scan
+    for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
+  pdl_wait();  // the selection (token / chunk list) of the previous kernel
+  KVB_STAMP(6);
+  if (p.mode == 1 && p.sel_scores) {
+    // top-K from the scan's scores + histogram into a bitmap in the (not yet
+    // used) ring, then ascending ids: each thread owns a run of words, one scan
+    uint32_t* wb = reinterpret_cast<uint32_t*>(ring);
+    uint32_t* sk = wb + ((p.Wc + 3) & ~3);
+    const int cap = (int)(((size_t)nst * p.stage_bytes - (size_t)((p.Wc + 3) & ~3) * 4) / 8);
+    select_topk_shared(p.sel_scores + (size_t)b * p.C, p.C, p.sel_hist + (size_t)b * kFuseHistBins,
+                       p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
+                       p.trace ? p.trace + (size_t)gridDim.y * gridDim.x * 8 + 64 +
+                                     ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8
+                               : nullptr);
     const int per = (p.Wc + nthr - 1) / nthr;
     const int w0 = min(p.Wc, tid * per), w1 = min(p.Wc, w0 + per);
     int cnt = 0;
-    for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(wb + w));
+    for (int w = w0; w < w1; ++w) cnt += __popc(wb[w]);
     int tot;
     int pos = block_excl_scan(cnt, red, &tot);
     for (int w = w0; w < w1; ++w) {
-      uint32_t bits = __ldcg(wb + w);
+      uint32_t bits = wb[w];
       while (bits) {
         const int bit = __ffs(bits) - 1;
         bits &= bits - 1u;
@@ -307,11 +320,13 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     __syncthreads();
     if (p.chunk_out && split == 0)
       for (int i = tid; i < p.K; i += nthr) p.chunk_out[(size_t)b * p.K + i] = uc[i];
+    if (p.trace)
+      sel_stamp(p.trace + (size_t)gridDim.y * gridDim.x * 8 + 64 +
+                    ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8, 4);
   } else if (p.mode == 1) {
     for (int i = tid; i < p.K; i += nthr) uc[i] = p.items[(size_t)b * p.cap + i];
   }
   if (p.mode == 1) {
-    for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
     __syncthreads();
     int run = 0;
     for (int base = 0; base < nres; base += nthr) {
@@ -329,6 +344,9 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     }
     if (tid == 0) ud[nres] = run;
     __syncthreads();
+    if (p.trace)
+      sel_stamp(p.trace + (size_t)gridDim.y * gridDim.x * 8 + 64 +
+                    ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8, 5);
     if (p.tok_out && split == 0 && tid == 0) {
       const int lastlen = p.n - (p.C - 1) * p.cs;
       const int atot = p.Kb * p.cs - ((p.Kb > 0 && uc[p.Kb - 1] == p.C - 1) ? p.cs - lastlen : 0);
@@ -739,9 +757,13 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
 __global__ void __launch_bounds__(128, 8) k5_merge_rows(const float* __restrict__ pm,
                                                      const float* __restrict__ pl,
                                                      const float* __restrict__ po, int S, int HG,
-                                                     float* __restrict__ out, float* __restrict__ lse) {
+                                                     float* __restrict__ out, float* __restrict__ lse,
+                                                     uint32_t* __restrict__ hist_clear) {
   const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // the attention (complete) was the last reader of the scan's histogram
+  if (hist_clear && row == 0)
+    for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
   const size_t base = (size_t)b * S * HG + row;
   float m = -INFINITY, acc = 0.f, L = 0.f;
   constexpr int CH = 8;  // splits per round: every load of a round in flight
@@ -893,7 +915,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.off_stage = g.off_stage;
   p.off_uni = g.off_uni;
   p.tok_out = a.mode == 1 ? a.tok_out : nullptr;
-  p.sel_bm = a.mode == 1 ? a.sel_bm : nullptr;
+  p.sel_scores = a.mode == 1 ? a.sel_scores : nullptr;
+  p.sel_hist = a.sel_hist;
   p.Wc = s->Wc;
   p.chunk_out = a.chunk_out;
   p.ntok_out = a.ntok_out;
@@ -941,7 +964,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
-                            (const float*)p.po, g.splits, H * a.G, p.out, p.lse);
+                            (const float*)p.po, g.splits, H * a.G, p.out, p.lse,
+                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr);
   return cudaGetLastError();
 }
 

@@ -1,24 +1,22 @@
-// Top-K fused into the tail of a landmark scan (decode step).
+// Exact top-K (selection.py:55-57) computed inside the attention prologue.
 //
-// The scan grid is one resident wave, G CTAs per sequence, each of which has
-// scored its share of the sequence's items and added a 2048-bin histogram of
-// the top 11 key bits into hist[b] (first radix level). The tail then:
-//   1. per-sequence arrival barrier (all G CTAs are co-resident);
-//   2. every CTA derives the threshold bin tb and the count kb to take inside
-//      it from the full histogram (bins scanned from the top);
-//   3. every CTA marks its items with bin > tb in the selected-item bitmap
-//      and appends its bin == tb items (key, id) to the candidate list;
-//   4. the last CTA to finish (ticket) resolves the exact K-th key inside
-//      the bin (single-warp bisection over the low 21 bits, candidates staged
-//      in shared memory) and marks the winners: keys above it, then the
-//      lowest ids among the ties -- the set of np.argsort(-s, kind="stable")[:K]
-//      (selection.py:55-57); with more candidates than fit, the same
-//      bisection runs over every item of the sequence (slow, exact);
-//   5. the resolver re-zeroes the histogram and the counters (self-cleaning
-//      store scratch: no memset nodes); scan kernels zero their slice of the
-//      bitmap before step 1.
-// The consumer (the attention prologue) turns the bitmap into the ascending
-// id list.
+// The landmark scan (K1) leaves per sequence the scores [C] and a 2048-bin
+// histogram of the top 11 bits of their order-preserving keys (first radix
+// level). Every attention CTA of the sequence then, redundantly and without
+// any inter-CTA communication:
+//   1. derives the threshold bin tb and the count kb to take inside it from
+//      the histogram (bins scanned from the top);
+//   2. streams the sequence's scores once (L2-resident, 64 KiB at C2):
+//      keys with bin > tb go straight into a shared-memory bitmap, keys in the
+//      threshold bin are appended to a shared candidate list;
+//   3. one warp bisects the candidates' low 21 bits for the K-th key T and
+//      marks the winners: keys above T, then the lowest ids among the ties --
+//      exactly the set of np.argsort(-s, kind="stable")[:K] (ties to the
+//      lowest id, -0 == +0 through score_key). With more candidates than the
+//      shared list holds, the same bisection runs block-wide over all scores
+//      (slow, exact; pathological ties only).
+// The bitmap then yields the ascending id list by one block scan. The merge
+// kernel that follows the attention re-zeroes the histogram.
 
 #pragma once
 
@@ -26,52 +24,30 @@
 
 namespace kvb {
 
-struct FuseSel {
-  uint32_t* bm;    // [B][Wc]  selected items (output)
-  uint32_t* ckey;  // [B][cap] candidate keys
-  int32_t* cid;    // [B][cap] candidate ids
-  int32_t* ctr;    // [B][4]   arrivals (barrier), arrivals (ticket), candidates
-  int Wc, cap, K;  // K <= items per sequence
-  int on;
-  uint64_t* trace;  // profiling: [B][G][8] %globaltimer phase stamps or null
-};
-
-__device__ __forceinline__ void fuse_stamp(const FuseSel& f, int b, int ph) {
-  if (f.trace && threadIdx.x == 0) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    f.trace[((size_t)b * gridDim.x + blockIdx.x) * 8 + ph] = t;
-  }
-}
-
 constexpr int kFuseHistBins = 2048;
 
-__device__ __forceinline__ void fuse_zero_bitmap(const FuseSel& f, int b) {
-  const int n = gridDim.x;
-  const int w0 = (int)(((long long)f.Wc * blockIdx.x) / n);
-  const int w1 = (int)(((long long)f.Wc * (blockIdx.x + 1)) / n);
-  for (int w = w0 + threadIdx.x; w < w1; w += blockDim.x) f.bm[(size_t)b * f.Wc + w] = 0u;
-}
-
-__device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Threshold bin: bins in descending order, blockDim.x divides 2048.
+// Threshold bin: bins in descending order; blockDim.x must divide 2048.
 __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
                                                int* s_kb) {
   const int tid = threadIdx.x;
+  constexpr int kMaxPer = 64;  // blockDim.x >= 32
   const int per = kFuseHistBins / blockDim.x;
+  int hv[kMaxPer];
   int loc = 0;
-  for (int j = 0; j < per; ++j) loc += (int)__ldcg(hb + kFuseHistBins - 1 - (tid * per + j));
+#pragma unroll
+  for (int j = 0; j < kMaxPer; ++j)
+    if (j < per) {
+      hv[j] = (int)__ldcg(hb + kFuseHistBins - 1 - (tid * per + j));
+      loc += hv[j];
+    }
   int tot;
   int above = block_excl_scan(loc, red, &tot);
   if (above < K && K <= above + loc) {
-    for (int j = 0; j < per; ++j) {
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+      if (j >= per) break;
       const int bin = kFuseHistBins - 1 - (tid * per + j);
-      const int c = (int)__ldcg(hb + bin);
+      const int c = hv[j];
       if (above + c >= K) {
         *s_tb = bin;
         *s_kb = K - above;
@@ -83,79 +59,101 @@ __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* r
   __syncthreads();
 }
 
-// items(fn): calls fn(id, score) for every item this CTA scored.
-// sk / si: shared memory for f.cap candidates. M: items per sequence;
-// scores_b: this sequence's scores (overflow path).
-template <typename Items>
-__device__ void fused_select_tail(const FuseSel& f, uint32_t* hist, const float* scores_b, int M,
-                                  int b, Items items, uint32_t* sk, int32_t* si) {
-  __shared__ int red[33];
-  __shared__ int s_tb, s_kb, s_last, s_gt, s_eq;
+// Top-K set of one sequence into the shared bitmap sbm[ceil(M/32)] (zeroed
+// here). sk/si: shared candidate storage for `cap` entries. All threads call.
+__device__ __forceinline__ void sel_stamp(uint64_t* tr, int k) {
+  if (tr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    tr[k] = t;
+  }
+}
+
+__device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
+                                   uint32_t* sbm, uint32_t* sk, int32_t* si, int cap, int* red,
+                                   uint64_t* tr = nullptr) {
+  __shared__ int s_tb, s_kb, s_nc, s_gt, s_eq;
   __shared__ uint32_t s_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
-  int32_t* ctr = f.ctr + (size_t)b * 4;
-  uint32_t* bm = f.bm + (size_t)b * f.Wc;
-  uint32_t* hb = hist + (size_t)b * kFuseHistBins;
-  // 1. every CTA of the sequence has flushed its histogram
-  __syncthreads();
-  fuse_stamp(f, b, 1);
-  if (tid == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1);
-    while (ld_acquire_s32(ctr) < (int)gridDim.x) {
-    }
-  }
-  __syncthreads();
-  fuse_stamp(f, b, 2);
-  // 2. threshold bin
+  const int W = (M + 31) >> 5;
+  for (int w = tid; w < W; w += nthr) sbm[w] = 0u;
   if (tid == 0) {
     s_tb = 0;
     s_kb = 0;
+    s_nc = 0;
   }
   __syncthreads();
-  fuse_threshold(hb, f.K, red, &s_tb, &s_kb);
+  fuse_threshold(hb, K, red, &s_tb, &s_kb);
   const uint32_t tb = (uint32_t)s_tb;
-  fuse_stamp(f, b, 3);
-  // 3. certain winners -> bitmap, threshold-bin items -> candidates
-  items([&](int id, float sc) {
-    const uint32_t key = score_key(sc), bin = key >> 21;
+  sel_stamp(tr, 0);
+  auto visit = [&](int i, float v) {
+    const uint32_t key = score_key(v), bin = key >> 21;
     if (bin > tb) {
-      atomicOr(bm + (id >> 5), 1u << (id & 31));
+      atomicOr(sbm + (i >> 5), 1u << (i & 31));
     } else if (bin == tb) {
-      const int pos = atomicAdd(ctr + 2, 1);
-      if (pos < f.cap) {
-        f.ckey[(size_t)b * f.cap + pos] = key;
-        f.cid[(size_t)b * f.cap + pos] = id;
+      const int pos = atomicAdd(&s_nc, 1);
+      if (pos < cap) {
+        sk[pos] = key;
+        si[pos] = i;
       }
     }
-  });
-  // 4. ticket: the last CTA resolves the threshold bin
-  __syncthreads();
-  fuse_stamp(f, b, 4);
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1;
+  };
+  if ((M & 3) == 0 && ((reinterpret_cast<uintptr_t>(sc) & 15) == 0)) {
+    // U float4 loads in flight per thread per round (the shared-memory atomics
+    // in visit() would otherwise serialise one L2 round trip per load)
+    constexpr int U = 16;
+    const float4* s4 = reinterpret_cast<const float4*>(sc);
+    const int M4 = M >> 2;
+    for (int i0 = tid; i0 < M4; i0 += nthr * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nthr;
+        v[u] = i < M4 ? __ldcg(s4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < M4) {
+          visit(4 * i, v[u].x);
+          visit(4 * i + 1, v[u].y);
+          visit(4 * i + 2, v[u].z);
+          visit(4 * i + 3, v[u].w);
+        }
+      }
+    }
+  } else {
+    for (int i = tid; i < M; i += nthr) visit(i, __ldcg(sc + i));
   }
   __syncthreads();
-  fuse_stamp(f, b, 5);
-  if (!s_last) return;
-  __threadfence();
-  const int nc = __ldcg(ctr + 2), kb = s_kb;
-  if (nc <= f.cap) {
-    for (int i = tid; i < nc; i += nthr) {
-      sk[i] = __ldcg(f.ckey + (size_t)b * f.cap + i);
-      si[i] = __ldcg(f.cid + (size_t)b * f.cap + i);
-    }
-    __syncthreads();
+  sel_stamp(tr, 1);
+  const int nc = s_nc, kb = s_kb;
+  if (nc <= cap) {
     if (warp == 0) {
       uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
-      while (lo < hi) {  // largest T with #(key >= T) >= kb
-        const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-        int c = 0;
-        for (int i = lane; i < nc; i += 32) c += sk[i] >= mid ? 1 : 0;
-        c = __reduce_add_sync(FULL, c);
-        if (c >= kb) lo = mid;
-        else hi = mid - 1u;
+      constexpr int RK = 16;  // candidates per lane held in registers
+      if (nc <= 32 * RK) {
+        uint32_t rk[RK];
+#pragma unroll
+        for (int j = 0; j < RK; ++j) rk[j] = (lane + 32 * j < nc) ? sk[lane + 32 * j] : 0u;
+        while (lo < hi) {  // largest T with #(key >= T) >= kb (keys outside the bin are 0)
+          const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+          int c = 0;
+#pragma unroll
+          for (int j = 0; j < RK; ++j) c += rk[j] >= mid ? 1 : 0;
+          c = __reduce_add_sync(FULL, c);
+          if (c >= kb) lo = mid;
+          else hi = mid - 1u;
+        }
+      } else {
+        while (lo < hi) {
+          const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+          int c = 0;
+          for (int i = lane; i < nc; i += 32) c += sk[i] >= mid ? 1 : 0;
+          c = __reduce_add_sync(FULL, c);
+          if (c >= kb) lo = mid;
+          else hi = mid - 1u;
+        }
       }
       int gt = 0, eq = 0;
       for (int i = lane; i < nc; i += 32) {
@@ -171,6 +169,7 @@ __device__ void fused_select_tail(const FuseSel& f, uint32_t* hist, const float*
       }
     }
     __syncthreads();
+    sel_stamp(tr, 2);
     const uint32_t T = s_T;
     const int need = kb - s_gt;
     const bool all_ties = need == s_eq;
@@ -182,18 +181,17 @@ __device__ void fused_select_tail(const FuseSel& f, uint32_t* hist, const float*
         for (int j = 0; j < nc; ++j) rank += (sk[j] == T && si[j] < si[i]) ? 1 : 0;
         take = rank < need;
       }
-      if (take) atomicOr(bm + (si[i] >> 5), 1u << (si[i] & 31));
+      if (take) atomicOr(sbm + (si[i] >> 5), 1u << (si[i] & 31));
     }
   } else {
-    // overflow (pathological ties): the same search over every item of the
-    // sequence, block-wide, reading the scores back
+    // overflow: the same bisection block-wide over every score of the bin
     uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
     while (lo < hi) {
       const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
       int c = 0;
       for (int i = tid; i < M; i += nthr) {
-        const uint32_t k = score_key(__ldcg(scores_b + i));
-        c += (k >> 21) == tb && k >= mid ? 1 : 0;
+        const uint32_t k = score_key(__ldcg(sc + i));
+        c += ((k >> 21) == tb && k >= mid) ? 1 : 0;
       }
       int tot;
       block_excl_scan(c, red, &tot);
@@ -203,34 +201,27 @@ __device__ void fused_select_tail(const FuseSel& f, uint32_t* hist, const float*
     const uint32_t T = lo;
     int gt = 0;
     for (int i = tid; i < M; i += nthr) {
-      const uint32_t k = score_key(__ldcg(scores_b + i));
+      const uint32_t k = score_key(__ldcg(sc + i));
       if ((k >> 21) == tb && k > T) {
         ++gt;
-        atomicOr(bm + (i >> 5), 1u << (i & 31));
+        atomicOr(sbm + (i >> 5), 1u << (i & 31));
       }
     }
     int gtot;
     block_excl_scan(gt, red, &gtot);
-    int need = kb - gtot, taken = 0;
+    const int need = kb - gtot;
+    int taken = 0;
     for (int base = 0; base < M && taken < need; base += nthr) {  // ascending ids
       const int i = base + tid;
-      const bool eq = i < M && score_key(__ldcg(scores_b + i)) == T;
+      const bool eq = i < M && score_key(__ldcg(sc + i)) == T;
       int tot;
       const int ex = block_excl_scan(eq ? 1 : 0, red, &tot);
-      if (eq && taken + ex < need) atomicOr(bm + (i >> 5), 1u << (i & 31));
+      if (eq && taken + ex < need) atomicOr(sbm + (i >> 5), 1u << (i & 31));
       taken += tot;
     }
   }
-  // 5. self-cleaning scratch for the next step
   __syncthreads();
-  fuse_stamp(f, b, 6);
-  for (int i = tid; i < kFuseHistBins; i += nthr) hb[i] = 0u;
-  if (tid == 0) {
-    ctr[0] = 0;
-    ctr[1] = 0;
-    ctr[2] = 0;
-  }
-  fuse_stamp(f, b, 7);
+  sel_stamp(tr, 3);
 }
 
 }  // namespace kvb

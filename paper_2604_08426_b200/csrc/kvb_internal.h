@@ -40,13 +40,7 @@ struct kvb_store {
   int32_t* k2_meta = nullptr;      // [B][4] threshold bin / counts
   int32_t* k2_overflow = nullptr;  // [B]
   bool k2_dirty = false;           // a failed launch may have left scratch dirty
-  // fused scan + top-K (kvb_fuse.cuh): selected-chunk bitmap, threshold-bin
-  // candidates and counters, same self-cleaning discipline
-  uint32_t* sel_bm = nullptr;      // [B][Wc]
-  uint32_t* sel_ckey = nullptr;    // [B][kFuseCap]
-  int32_t* sel_cid = nullptr;      // [B][kFuseCap]
-  int32_t* sel_ctr = nullptr;      // [B][4]
-  int Wc = 0;                      // ceil(C / 32)
+  int Wc = 0;                      // ceil(C / 32): words of a per-sequence chunk bitmap
   int32_t* res_prefix = nullptr;   // [B][W] residents before word w
   void* res_k = nullptr;         // [B][max_resident][E]
   void* res_v = nullptr;
@@ -73,7 +67,7 @@ bool trace_enable(int on);
 uint64_t* trace_buffer();  // null when disabled
 int64_t trace_read(uint64_t* host, int64_t max_words);
 constexpr int64_t kTraceWords = 1 << 16;
-constexpr int kFuseCap = 8192;  // threshold-bin candidates staged by the fused top-K
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
 cudaError_t ensure_smem(const void* func, size_t bytes);
 // Number of SMs of the current device and resident CTAs/SM for a kernel.
@@ -83,11 +77,8 @@ int resident_ctas(const void* func, int threads, size_t smem);
 // ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
 // hist (may be null): [B][2048] uint32, zeroed by the caller; receives the
 // histogram of the top 11 bits of the score keys (sum aggregation only).
-struct FuseSel;
-// fuse (optional): top-K fused into the scan tail (kvb_fuse.cuh); sum only
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st,
-                               const FuseSel* fuse = nullptr);
+                               float* scores, uint32_t* hist, cudaStream_t st);
 constexpr int kTopHistBins = 2048;
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);
@@ -182,8 +173,11 @@ struct BulkLaunch {
   float* out;
   float* lse;
   int splits;
-  const uint32_t* sel_bm = nullptr;  // mode 1: selected-chunk bitmap [B][Wc] instead of items
-  int32_t* chunk_out = nullptr;      // mode 1 + sel_bm: ascending chunk ids out [B][K] (optional)
+  // mode 1 with sel_scores: the top-K itself runs in the attention prologue
+  // (kvb_fuse.cuh) from the scan's scores [B][C] and key histogram [B][2048]
+  const float* sel_scores = nullptr;
+  uint32_t* sel_hist = nullptr;      // re-zeroed by the merge kernel
+  int32_t* chunk_out = nullptr;      // ascending selected chunk ids out [B][K] (optional)
   int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
   int32_t* ntok_out = nullptr;  // [B]
   int tcap = 0;
@@ -193,8 +187,8 @@ int attend_bulk_splits(const kvb_store* s, int positions_cap);
 cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st);
 // decode-step attention over residents + selected chunks (chunk ids [B][K])
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
-                                 int K, cudaStream_t st, const uint32_t* sel_bm = nullptr,
-                                 int32_t* chunk_out = nullptr);
+                                 int K, cudaStream_t st, const float* sel_scores = nullptr,
+                                 uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr);
 // the two halves of launch_attend: per-step query prep, then the attention
 cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);

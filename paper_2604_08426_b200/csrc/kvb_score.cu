@@ -18,7 +18,6 @@
 // oracle/exact_order.c, so GPU scores are bit-identical to that restatement.
 
 #include "kvb_common.cuh"
-#include "kvb_fuse.cuh"
 #include "kvb_internal.h"
 
 namespace kvb {
@@ -52,16 +51,12 @@ constexpr int kHistBins = 2048;
 template <typename T, int VW, int NV>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
-             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist, FuseSel fz) {
+             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist) {
   extern __shared__ float qbar[];
   __shared__ uint32_t shist[kHistBins];
   const int E = Hkv * D;
   const int b = blockIdx.y;
   pdl_trigger();  // the next kernel may launch now; it waits for this grid
-  if (fz.on) {
-    fuse_stamp(fz, b, 0);
-    fuse_zero_bitmap(fz, b);
-  }
   load_qbar(q + (size_t)b * Hkv * G * D, Hkv, G, D, qbar);
   if (hist)
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) shist[i] = 0u;
@@ -140,27 +135,13 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
       if (shist[i]) atomicAdd(gh + i, shist[i]);
   }
-  if (fz.on) {
-    // top-K fused into the scan tail (kvb_fuse.cuh); lane l re-reads the
-    // scores of its warp's rows c = gw*2 + k*nw*2 + (l & 1), k = l/2 mod 16
-    auto items = [&](auto fn) {
-      for (int c0 = gw * 2 + (lane >> 1) * nw * 2; c0 < C; c0 += 16 * nw * 2) {
-        const int c = c0 + (lane & 1);
-        if (c < C) fn(c, out[c]);
-      }
-    };
-    uint32_t* sk = reinterpret_cast<uint32_t*>(qbar + ((E + 3) & ~3));
-    fused_select_tail(fz, hist, out, C, b, items, sk, reinterpret_cast<int32_t*>(sk + fz.cap));
-  }
 }
 
 // Generic fallback for very wide rows: identical order, q_bar read from smem.
 template <typename T, int VW>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
-                  float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist,
-                  FuseSel fz) {
-  (void)fz;  // never fused (dense_sum_dispatch)
+                  float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist) {
   extern __shared__ float qbar[];
   const int E = Hkv * D;
   const int b = blockIdx.y;
@@ -401,19 +382,13 @@ int score_grid_x(int C, int B, const void* func, size_t smem) {
 
 template <typename T>
 cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, int G,
-                               float* scores, uint32_t* hist, cudaStream_t st,
-                               const FuseSel* fuse) {
+                               float* scores, uint32_t* hist, cudaStream_t st) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim, E = s->E;
   constexpr int VWv = 16 / sizeof(T);
   const bool vec = (E % VWv) == 0;
   const int VW = vec ? VWv : 1;
   const int nvl = (E / VW + 31) / 32;
-  FuseSel fz{};
-  if (fuse) {
-    if (!vec || nvl > 8 || !hist) return cudaErrorNotSupported;
-    fz = *fuse;
-  }
-  const size_t smem = (size_t)((E + 3) & ~3) * sizeof(float) + (fuse ? (size_t)fz.cap * 8 : 0);
+  const size_t smem = (size_t)E * sizeof(float);
   const void* fn;
   if (vec) {
     if (nvl <= 1) fn = (const void*)k1_dense_sum<T, VWv, 1>;
@@ -428,7 +403,7 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   dim3 grid(score_grid_x(C, B, fn, smem), B);
   count_launch();
   void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D,
-                  (void*)&hist, (void*)&fz};
+                  (void*)&hist};
   return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
 }
@@ -436,14 +411,13 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
 }  // namespace
 
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st, const FuseSel* fuse) {
+                               float* scores, uint32_t* hist, cudaStream_t st) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim;
   if (agg == KVB_AGG_SUM) {
     if (s->d.kv_dtype == KVB_BF16)
-      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st, fuse);
-    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st, fuse);
+      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st);
+    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st);
   }
-  if (fuse) return cudaErrorNotSupported;
   const size_t smem = (size_t)H * G * D * sizeof(float);
   const void* fmax_fn = s->d.kv_dtype == KVB_BF16 ? (const void*)k1_dense_max<__nv_bfloat16>
                                                   : (const void*)k1_dense_max<float>;

@@ -20,16 +20,16 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_2604_08426_b200 import _lib  # noqa: E402
 
-PH = ["start", "setup", "prologue", "first_tile", "loop_end", "end"]
+PH = ["start", "setup", "prologue", "first_tile", "loop_end", "end", "pdl_waited"]
 
 
 def report(tag, lib, B, S):
-    buf = np.zeros(B * S * 8 + B * 4, dtype=np.uint64)
+    buf = np.zeros(2 * B * S * 8 + 64, dtype=np.uint64)
     n = lib.kvb_trace_read(buf.ctypes.data, buf.size)
     t = buf[: B * S * 8].reshape(B * S, 8).astype(np.int64)
     smid = (t[:, 7] >> 32).astype(np.int64)
     work = (t[:, 7] & 0xffffffff).astype(np.int64)
-    ph = t[:, :6].astype(np.float64)
+    ph = t[:, :7].astype(np.float64)
     t0 = ph[:, 0].min()
     rel = (ph - t0) / 1e3
     print(f"== {tag}: {B * S} CTAs ({n} words), entries/CTA min {work.min()} max {work.max()}, "
@@ -39,6 +39,17 @@ def report(tag, lib, B, S):
         col = col[ph[:, i] > 0]
         if len(col):
             print(f"  {name:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")
+    base = B * S * 8 + 64
+    if n >= base + B * S * 8:
+        sub = buf[base: base + B * S * 8].reshape(B * S, 8).astype(np.float64)
+        names = ["threshold", "scan", "bisect", "winners", "id list", "union prefix"]
+        w = ph[:, 6]
+        for i, nm in enumerate(names):
+            col = sub[:, i]
+            ok = col > 0
+            if ok.any():
+                r = (col[ok] - w[ok]) / 1e3
+                print(f"    sel {nm:13s} (after pdl wait) min {r.min():7.2f} med {np.median(r):7.2f} max {r.max():7.2f}")
     d = (ph[:, 4] - ph[:, 3]) / 1e3
     print(f"  tile loop   min {d.min():7.2f}  med {np.median(d):7.2f}  max {d.max():7.2f} us")
     d = (ph[:, 3] - ph[:, 2]) / 1e3
