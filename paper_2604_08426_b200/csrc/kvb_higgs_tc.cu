@@ -37,7 +37,7 @@ constexpr int kTPI = 4;      // tiles per iteration (64 landmark rows)
 
 __device__ __forceinline__ void mma_f16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
@@ -74,14 +74,29 @@ __global__ void k1h_prep(const float* __restrict__ q, const float* __restrict__ 
 
 // One CTA per (slab of row tiles, sequence); warp w = head w. Codes are
 // packed 4-bit pairs: row r of head h = 32 bytes at codes[(b,h)][r*32].
+//
+// Codeword lookup: a pair LUT keyed by (code of row g4, code of row g4+8)
+// returns the fp16 parts of both rows' codewords -- exactly the consecutive
+// A-fragment registers {a0, a1} (or {a2, a3}) of m16n8k16 -- so one LDS.64
+// feeds two fragment registers, with the pair index taken from both rows'
+// nibble-packed code words by two logic ops per four k-steps. The tables are
+// replicated 16x (copy = lane & 15) so a half-warp's 16 lookups always hit
+// 16 distinct bank pairs. The three split products accumulate in separate
+// chains (fp32-class; summed hi.hi + hi.lo, then + lo.hi).
+constexpr int kPairEntries = 256;
+constexpr int kPairCopies = 16;
+constexpr int kLutBytes = kPairEntries * kPairCopies * 8;  // one table (hi or lo)
+
+__device__ __forceinline__ void lds64(uint32_t& x, uint32_t& y, uint32_t addr) {
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(x), "=r"(y) : "r"(addr));
+}
+
 template <int HMAX>
 __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     const uint8_t* __restrict__ codes, const float* __restrict__ factors,
     const float* __restrict__ W, const float* __restrict__ cb, float* __restrict__ scores,
     int rows, int H, int ngroups, int gbytes, int tiles_per_cta, uint32_t* __restrict__ hist) {
-  // code -> (hi half2, lo half2): 16 entries x 8 B span the 32 banks exactly,
-  // so any lane->entry pattern is conflict-free
-  __shared__ uint2 lut[16];
+  extern __shared__ __align__(16) unsigned char lut_raw[];  // [hi table][lo table]
   __shared__ float part[HMAX][kTPI * kTileRows];
   __shared__ uint32_t shist[kTopHistBins];   // first radix level of K2 (see k1_dense_sum)
   if (hist)
@@ -90,16 +105,25 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y;
   pdl_trigger();
-  if (threadIdx.x < 16) {
-    const float x = cb[2 * threadIdx.x], y = cb[2 * threadIdx.x + 1];
-    const __half2 hh = __floats2half2_rn(x, y);
-    const float2 f = __half22float2(hh);
-    lut[threadIdx.x] = make_uint2(h2u(hh), h2u(__floats2half2_rn(x - f.x, y - f.y)));
+  // pair tables: entry e = x + 16 y, copy c at byte (e * 16 + c) * 8
+  {
+    uint2* hi_t = reinterpret_cast<uint2*>(lut_raw);
+    uint2* lo_t = reinterpret_cast<uint2*>(lut_raw + kLutBytes);
+    for (int i = threadIdx.x; i < kPairEntries * kPairCopies; i += blockDim.x) {
+      const int e = i / kPairCopies, x = e & 15, y = e >> 4;
+      const __half2 hx = __floats2half2_rn(cb[2 * x], cb[2 * x + 1]);
+      const __half2 hy = __floats2half2_rn(cb[2 * y], cb[2 * y + 1]);
+      const float2 fx = __half22float2(hx), fy = __half22float2(hy);
+      hi_t[i] = make_uint2(h2u(hx), h2u(hy));
+      lo_t[i] = make_uint2(h2u(__floats2half2_rn(cb[2 * x] - fx.x, cb[2 * x + 1] - fx.y)),
+                           h2u(__floats2half2_rn(cb[2 * y] - fy.x, cb[2 * y + 1] - fy.y)));
+    }
   }
+  const uint32_t lane8 = (uint32_t)(lane & 15) * 8u;  // this lane's table copy
   // B fragments: thread (g4, tig) owns w_{g4}[32*tig + 4*ks + 0..3], ks = 0..7
   uint32_t bhi[8][2], blo[8][2];
   const int h = warp;
-  if (h < H) {
+  {
     const float* w = W + (((size_t)b * H + h) * kR + g4) * kD + 32 * tig;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
@@ -116,8 +140,8 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   const int ntiles = (rows + kTileRows - 1) / kTileRows;
   const int t_begin = blockIdx.x * tiles_per_cta;
   const int t_end = min(ntiles, t_begin + tiles_per_cta);
-  const uint8_t* cbase = codes + ((size_t)b * H + (h < H ? h : 0)) * (size_t)ngroups * gbytes;
-  const float* fbase = factors + ((size_t)b * H + (h < H ? h : 0)) * ngroups;
+  const uint8_t* cbase = codes + ((size_t)b * H + h) * (size_t)ngroups * gbytes;
+  const float* fbase = factors + ((size_t)b * H + h) * ngroups;
   // sign of H_8[k][a] for this lane's rows a = g4 and columns k = 2tig, 2tig+1
   const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
   const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
@@ -128,10 +152,10 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     for (int u = 0; u < kTPI; ++u) {
       const int row0 = (t0 + u) * kTileRows + g4;
       const int row1 = row0 + 8;
-      nxt[u][0] = (h < H && t0 + u < t_end && row0 < rows)
+      nxt[u][0] = (t0 + u < t_end && row0 < rows)
                       ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row0 * 32 + 8 * tig))
                       : make_uint2(0, 0);
-      nxt[u][1] = (h < H && t0 + u < t_end && row1 < rows)
+      nxt[u][1] = (t0 + u < t_end && row1 < rows)
                       ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row1 * 32 + 8 * tig))
                       : make_uint2(0, 0);
     }
@@ -147,21 +171,35 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     load(t + kTPI);
 #pragma unroll
     for (int u = 0; u < kTPI; ++u) {
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
-      if (h < H) {
+      // three independent accumulator chains (hi.hi, hi.lo, lo.hi): mma latency
+      float c[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
+      {
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint32_t w0 = ks < 4 ? cur[u][0].x : cur[u][0].y;
-          const uint32_t w1 = ks < 4 ? cur[u][1].x : cur[u][1].y;
-          const uint32_t sh = 8 * (ks & 3);
-          // a0 (row g4, code 16tig+2ks = low nibble), a2 (code +1 = high nibble);
-          // a1/a3: the same for row g4 + 8
-          const uint2 l0 = lut[(w0 >> sh) & 15u], h0 = lut[(w0 >> (sh + 4)) & 15u];
-          const uint2 l1 = lut[(w1 >> sh) & 15u], h1 = lut[(w1 >> (sh + 4)) & 15u];
-          mma_f16(c, l0.x, l1.x, h0.x, h1.x, bhi[ks][0], bhi[ks][1]);
-          mma_f16(c, l0.x, l1.x, h0.x, h1.x, blo[ks][0], blo[ks][1]);
-          mma_f16(c, l0.y, l1.y, h0.y, h1.y, bhi[ks][0], bhi[ks][1]);
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t w0 = half ? cur[u][0].y : cur[u][0].x;  // row g4, 4 bytes = 4 k-steps
+          const uint32_t w1 = half ? cur[u][1].y : cur[u][1].x;  // row g4 + 8
+          // byte k of pl / ph = pair index x + 16 y of the low / high nibbles
+          const uint32_t pl = (w0 & 0x0F0F0F0Fu) | ((w1 & 0x0F0F0F0Fu) << 4);
+          const uint32_t ph = ((w0 >> 4) & 0x0F0F0F0Fu) | (w1 & 0xF0F0F0F0u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int ks = half * 4 + k;
+            // byte offset entry * 128 | copy * 8 (16 copies x 8 B), one LOP3 each
+            const uint32_t ol = ((k == 0 ? (pl << 7) : (pl >> (8 * k - 7))) & 0x7F80u) | lane8;
+            const uint32_t oh = ((k == 0 ? (ph << 7) : (ph >> (8 * k - 7))) & 0x7F80u) | lane8;
+            const uint2 A01 = *reinterpret_cast<const uint2*>(lut_raw + ol);
+            const uint2 A23 = *reinterpret_cast<const uint2*>(lut_raw + oh);
+            const uint2 L01 = *reinterpret_cast<const uint2*>(lut_raw + kLutBytes + ol);
+            const uint2 L23 = *reinterpret_cast<const uint2*>(lut_raw + kLutBytes + oh);
+            const uint32_t a0 = A01.x, a1 = A01.y, a2 = A23.x, a3 = A23.y;
+            const uint32_t l0 = L01.x, l1 = L01.y, l2 = L23.x, l3 = L23.y;
+            mma_f16(c, a0, a1, a2, a3, bhi[ks][0], bhi[ks][1]);
+            mma_f16(c2, a0, a1, a2, a3, blo[ks][0], blo[ks][1]);
+            mma_f16(c3, l0, l1, l2, l3, bhi[ks][0], bhi[ks][1]);
+          }
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[i] = (c[i] + c2[i]) + c3[i];
       }
       // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)
       float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
@@ -171,7 +209,7 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
         v[i] += __shfl_xor_sync(FULL, v[i], 8);
         v[i] += __shfl_xor_sync(FULL, v[i], 16);
       }
-      if (h < H && g4 == 0) {
+      if (g4 == 0) {
         const int gam0 = (t + u) * 2, gam1 = gam0 + 1;  // groups of this tile
         const float f0 = gam0 < ngroups ? __ldg(fbase + gam0) * (1.0f / 32.0f) : 0.f;
         const float f1 = gam1 < ngroups ? __ldg(fbase + gam1) * (1.0f / 32.0f) : 0.f;
@@ -183,11 +221,11 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
       }
     }
     __syncthreads();
-    if (threadIdx.x < kTPI * kTileRows) {
-      const int row = t * kTileRows + threadIdx.x;
-      if (row < rows && t * kTileRows + threadIdx.x < t_end * kTileRows) {
-        float s = part[0][threadIdx.x];
-        for (int hh = 1; hh < H; ++hh) s = s + part[hh][threadIdx.x];
+    for (int i = threadIdx.x; i < kTPI * kTileRows; i += blockDim.x) {
+      const int row = t * kTileRows + i;
+      if (row < rows && row < t_end * kTileRows) {
+        float s = part[0][i];
+        for (int hh = 1; hh < H; ++hh) s = s + part[hh][i];
         scores[(size_t)b * rows + row] = s;
         if (hist) atomicAdd(&shist[score_key(s) >> 21], 1u);
       }
@@ -222,12 +260,15 @@ cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, flo
   k1h_prep<<<dim3(H, B), kR * 32, 0, st>>>(q, hd.signs, W, H, G);
   const int rows = s->C;
   const int ntiles = (rows + kTileRows - 1) / kTileRows;
-  const int slots = sm_count() * resident_ctas((const void*)k1h_score<8>, 256, 0);
+  const size_t smem = 2 * (size_t)kLutBytes;
+  ensure_smem((const void*)k1h_score<8>, smem);
+  const int slots = sm_count() * resident_ctas((const void*)k1h_score<8>, H * 32, smem);
   int ctas = slots / B;
   if (ctas < 1) ctas = 1;
   if (ctas > ntiles) ctas = ntiles;
   const int per = (ntiles + ctas - 1) / ctas;
-  k1h_score<8><<<dim3((ntiles + per - 1) / per, B), 256, 0, st>>>(
+  // one warp per KV head (every warp valid: no divergent guards around the mma)
+  k1h_score<8><<<dim3((ntiles + per - 1) / per, B), H * 32, smem, st>>>(
       hd.codes, hd.factor, W, hd.codebook, scores, rows, H, hd.groups, hd.group_bytes, per, hist);
   return cudaGetLastError();
 }
