@@ -112,6 +112,67 @@ __device__ __forceinline__ int block_excl_scan(int v, int* red, int* total) {
   return ex;
 }
 
+// Block-wide exact k-th largest key (1-based k) among n keys key_at(i) that
+// all share the bits above bit 20 with `prefix` (the threshold bin of an
+// 11-bit first radix level): three 7-bit radix rounds over the low 21 bits
+// with shared-memory histograms (all threads), then the counts strictly above
+// / equal to it. `hist` needs 128 ints of shared memory. All threads call;
+// results are valid in every thread on return.
+template <typename KeyAt>
+__device__ __forceinline__ void block_kth_key(KeyAt key_at, int n, uint32_t prefix, int k, int* hist,
+                                              int* red, uint32_t* out_T, int* out_gt, int* out_eq) {
+  __shared__ int s_d, s_k;
+  const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+  for (int shift = 14; shift >= 0; shift -= 7) {
+    for (int i = tid; i < 128; i += nthr) hist[i] = 0;
+    __syncthreads();
+    const uint32_t fixed = ~((1u << (shift + 7)) - 1u);
+    for (int i = tid; i < n; i += nthr) {
+      const uint32_t u = key_at(i);
+      if ((u & fixed) == prefix) atomicAdd(&hist[(u >> shift) & 127], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // lane l owns bins 127-4l .. 124-4l (descending)
+      int c[4], loc = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        c[j] = hist[127 - 4 * lane - j];
+        loc += c[j];
+      }
+      const int inc = warp_incl_scan(loc, lane);
+      int above = inc - loc;
+      if (above < k && k <= inc) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (above + c[j] >= k) {
+            s_d = 127 - 4 * lane - j;
+            s_k = k - above;
+            break;
+          }
+          above += c[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)s_d << shift;
+    k = s_k;
+    __syncthreads();
+  }
+  int gt = 0, eq = 0;
+  for (int i = tid; i < n; i += nthr) {
+    const uint32_t u = key_at(i);
+    gt += u > prefix ? 1 : 0;
+    eq += u == prefix ? 1 : 0;
+  }
+  int tg, te;
+  block_excl_scan(gt, red, &tg);
+  block_excl_scan(eq, red, &te);
+  *out_T = prefix;
+  *out_gt = tg;
+  *out_eq = te;
+}
+
 // Programmatic dependent launch (sm_90+): let the next kernel in the stream
 // launch now / wait until the previous kernel's grid completed and flushed.
 // Both are no-ops when the launch carried no programmatic dependency.

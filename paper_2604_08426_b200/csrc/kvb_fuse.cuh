@@ -129,41 +129,13 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
   sel_stamp(tr, 1);
   const int nc = s_nc, kb = s_kb;
   if (nc <= cap) {
-    if (warp == 0) {
-      uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
-      constexpr int RK = 16;  // candidates per lane held in registers
-      if (nc <= 32 * RK) {
-        uint32_t rk[RK];
-#pragma unroll
-        for (int j = 0; j < RK; ++j) rk[j] = (lane + 32 * j < nc) ? sk[lane + 32 * j] : 0u;
-        while (lo < hi) {  // largest T with #(key >= T) >= kb (keys outside the bin are 0)
-          const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-          int c = 0;
-#pragma unroll
-          for (int j = 0; j < RK; ++j) c += rk[j] >= mid ? 1 : 0;
-          c = __reduce_add_sync(FULL, c);
-          if (c >= kb) lo = mid;
-          else hi = mid - 1u;
-        }
-      } else {
-        while (lo < hi) {
-          const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-          int c = 0;
-          for (int i = lane; i < nc; i += 32) c += sk[i] >= mid ? 1 : 0;
-          c = __reduce_add_sync(FULL, c);
-          if (c >= kb) lo = mid;
-          else hi = mid - 1u;
-        }
-      }
-      int gt = 0, eq = 0;
-      for (int i = lane; i < nc; i += 32) {
-        gt += sk[i] > lo ? 1 : 0;
-        eq += sk[i] == lo ? 1 : 0;
-      }
-      gt = __reduce_add_sync(FULL, gt);
-      eq = __reduce_add_sync(FULL, eq);
-      if (lane == 0) {
-        s_T = lo;
+    {
+      __shared__ int khist[128];
+      uint32_t T0;
+      int gt, eq;
+      block_kth_key([&](int i) { return sk[i]; }, nc, tb << 21, kb, khist, red, &T0, &gt, &eq);
+      if (tid == 0) {
+        s_T = T0;
         s_gt = gt;
         s_eq = eq;
       }

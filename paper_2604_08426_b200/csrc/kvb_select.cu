@@ -422,52 +422,58 @@ __global__ void __launch_bounds__(256) k2a_split(const float* __restrict__ score
                                                  K2Meta* __restrict__ meta,
                                                  int32_t* __restrict__ sel, int sel_stride,
                                                  uint64_t* __restrict__ cand, int cand_cap) {
+  // this CTA's winners / threshold-bin candidates are first gathered in shared
+  // memory (one batched round of score loads, shared atomics), then appended
+  // to the sequence's lists with ONE global atomic per list
+  extern __shared__ __align__(16) unsigned char k2a_sm[];
   __shared__ int red[33];
-  __shared__ int s_tb, s_kb, s_nb;
-  const int b = blockIdx.y, lane = threadIdx.x & 31;
+  __shared__ int s_tb, s_kb, s_nb, s_ns, s_nc, s_bs, s_bc;
+  const int b = blockIdx.y, tid = threadIdx.x, nthr = blockDim.x;
   const int Kc = K < M ? K : M;
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  uint64_t* s_cand = reinterpret_cast<uint64_t*>(k2a_sm);        // [per]
+  int32_t* s_sel = reinterpret_cast<int32_t*>(s_cand + per);     // [per]
+  if (tid == 0) {
+    s_ns = 0;
+    s_nc = 0;
+  }
   pdl_trigger();
   pdl_wait();  // scores + histogram of the scan
   hist_threshold(hist + (size_t)b * kTopHistBins, Kc, red, &s_tb, &s_kb, &s_nb);
   const uint32_t tb = (uint32_t)s_tb;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     meta[b].tb = s_tb;
     meta[b].kb = s_kb;
   }
   const float* sc = scores + (size_t)b * M;
-  const int per = (M + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per, i1 = min(M, i0 + per);
-  for (int base = i0 + (threadIdx.x & ~31) * 4; base < i1; base += blockDim.x * 4) {
-    uint32_t u4[4];
+  constexpr int U = 16;
+  for (int base = i0 + tid; base < i1; base += nthr * U) {
+    float v[U];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = base + 32 * k + lane;
-      u4[k] = i < i1 ? score_key(__ldg(sc + i)) : 0u;
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nthr;
+      v[u] = i < i1 ? __ldcg(sc + i) : 0.f;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = base + 32 * k + lane;
-      const uint32_t bin = u4[k] >> 21;
-      const bool is_sel = i < i1 && bin > tb;
-      const bool is_cand = i < i1 && bin == tb;
-      unsigned m = __ballot_sync(FULL, is_sel);
-      if (m) {
-        int wb = 0;
-        if (lane == 0) wb = atomicAdd(&meta[b].nsel, __popc(m));
-        wb = __shfl_sync(FULL, wb, 0);
-        if (is_sel) sel[(size_t)b * sel_stride + wb + __popc(m & ((1u << lane) - 1u))] = i;
-      }
-      m = __ballot_sync(FULL, is_cand);
-      if (m) {
-        int wb = 0;
-        if (lane == 0) wb = atomicAdd(&meta[b].ncand, __popc(m));
-        wb = __shfl_sync(FULL, wb, 0);
-        const int pos = wb + __popc(m & ((1u << lane) - 1u));
-        if (is_cand && pos < cand_cap)
-          cand[(size_t)b * cand_cap + pos] = ((uint64_t)u4[k] << 32) | (uint32_t)i;
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nthr;
+      if (i < i1) {
+        const uint32_t key = score_key(v[u]), bin = key >> 21;
+        if (bin > tb) s_sel[atomicAdd(&s_ns, 1)] = i;
+        else if (bin == tb) s_cand[atomicAdd(&s_nc, 1)] = ((uint64_t)key << 32) | (uint32_t)i;
       }
     }
   }
+  __syncthreads();
+  if (tid == 0) {
+    s_bs = s_ns ? atomicAdd(&meta[b].nsel, s_ns) : 0;
+    s_bc = s_nc ? atomicAdd(&meta[b].ncand, s_nc) : 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < s_ns; i += nthr) sel[(size_t)b * sel_stride + s_bs + i] = s_sel[i];
+  for (int i = tid; i < s_nc; i += nthr)
+    if (s_bc + i < cand_cap) cand[(size_t)b * cand_cap + s_bc + i] = s_cand[i];
 }
 
 struct K2bParams {
@@ -486,7 +492,17 @@ struct K2bParams {
   int sorted;            // out_ids in ascending id order (set semantics)
   uint32_t* hist;        // [B][2048] store scratch: re-zeroed here after K2a consumed it
   K2Meta* meta_rw;       // [B] store scratch: re-zeroed here after reading
+  int stage_off, stage_cap;  // shared staging of the candidates
+  uint64_t* trace;           // profiling: [B][8] %globaltimer stamps or null
 };
+
+__device__ __forceinline__ void k2b_stamp(const K2bParams& p, int k) {
+  if (p.trace && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * 8 + k] = t;
+  }
+}
 
 // Rewrite row `ids` (K distinct ids < M, any order) in ascending order via a
 // bitmap over [0, M) in shared memory `bm` (>= ceil(M/32) words).
@@ -506,6 +522,7 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
   const int nthr = blockDim.x;
   pdl_trigger();
   pdl_wait();  // K2a's split
+  k2b_stamp(p, 0);
   const K2Meta mt = p.meta[b];
   const int K = p.K < p.M ? p.K : p.M;
   // self-cleaning scratch: K2a (complete) was the histogram's last reader and
@@ -553,31 +570,28 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
   }
   const uint64_t* cd = p.cand + (size_t)b * p.cand_cap;
   const int nc = mt.ncand, kb = mt.kb;
-  if (warp == 0) {
-    uint32_t lo = (uint32_t)mt.tb << 21, hi = lo | 0x1fffffu;
-    while (lo < hi) {
-      const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-      int c = 0;
-      for (int i = lane; i < nc; i += 32) c += (uint32_t)(cd[i] >> 32) >= mid ? 1 : 0;
-      c = __reduce_add_sync(FULL, c);
-      if (c >= kb) lo = mid; else hi = mid - 1u;
-    }
-    int gt = 0, eq = 0;
-    for (int i = lane; i < nc; i += 32) {
-      const uint32_t u = (uint32_t)(cd[i] >> 32);
-      gt += u > lo ? 1 : 0;
-      eq += u == lo ? 1 : 0;
-    }
-    gt = __reduce_add_sync(FULL, gt);
-    eq = __reduce_add_sync(FULL, eq);
-    if (lane == 0) {
-      s_T = lo;
+  if (nc <= p.stage_cap) {  // one batched round into shared memory
+    uint64_t* scd = reinterpret_cast<uint64_t*>(smem_raw + p.stage_off);
+    for (int i = tid; i < nc; i += nthr) scd[i] = __ldcg(cd + i);
+    __syncthreads();
+    cd = scd;
+  }
+  k2b_stamp(p, 1);
+  {
+    __shared__ int khist[128];
+    uint32_t T0;
+    int gt, eq;
+    block_kth_key([&](int i) { return (uint32_t)(cd[i] >> 32); }, nc, (uint32_t)mt.tb << 21, kb,
+                  khist, red, &T0, &gt, &eq);
+    if (tid == 0) {
+      s_T = T0;
       s_gt = gt;
       s_eq = eq;
       s_cnt = mt.nsel;
     }
   }
   __syncthreads();
+  k2b_stamp(p, 2);
   const uint32_t T = s_T;
   const int krem = kb - s_gt;
   const bool all_ties = krem == s_eq;
@@ -593,6 +607,7 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     if (take) ids[wb + __popc(m & ((1u << lane) - 1u))] = (int32_t)(uint32_t)cd[i];
   }
   __syncthreads();
+  k2b_stamp(p, 3);
   if (!all_ties) {
     // the krem lowest ids among the ties: rank ties by id (counting smaller ids)
     const int start = s_cnt;
@@ -606,6 +621,7 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     }
   }
   __syncthreads();
+  k2b_stamp(p, 4);
   // ids[0..K) now holds the top-K set; rank order on request
   if (p.rank_order) {
     const float* sc = p.scores + (size_t)b * p.M;
@@ -641,6 +657,7 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     __shared__ int s_n;
     token_union(nullptr, 0, (p.M + 31) / 32, bm, [&](int r) { return (int)ids[r]; }, K, 0, 1, p.M,
                 nullptr, 0, p.M, p.out_ids + (size_t)b * p.K, K, &s_n, nullptr, red);
+    k2b_stamp(p, 5);
   } else if (p.out_ids != p.sel) {
     for (int r = tid; r < p.K; r += nthr)
       p.out_ids[(size_t)b * p.K + r] = r < K ? ids[r] : -1;
@@ -693,7 +710,10 @@ cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, 
     const uint32_t* hist = a.hist;
     void* args[] = {(void*)&sc, (void*)&M, (void*)&K, (void*)&hist, (void*)&meta, (void*)&sel,
                     (void*)&stride, (void*)&cand, (void*)&cap};
-    cudaError_t e = launch_pdl((const void*)k2a_split, dim3(per_seq, B), dim3(256), 0, st, args);
+    const size_t per = (M + per_seq - 1) / per_seq;
+    const size_t asmem = per * 12;
+    ensure_smem((const void*)k2a_split, asmem);
+    cudaError_t e = launch_pdl((const void*)k2a_split, dim3(per_seq, B), dim3(256), asmem, st, args);
     if (e != cudaSuccess) return e;
   }
   K2bParams p{};
@@ -718,10 +738,15 @@ cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, 
   p.sorted = a.sorted_ids;
   p.hist = const_cast<uint32_t*>(a.hist);
   p.meta_rw = meta;
+  p.trace = trace_buffer() ? trace_buffer() + 49152 : nullptr;  // profiling hook
   // room for the in-kernel radix fallback too: max(P*8, K*4) + bitmap
   const int Pf = next_pow2(a.K < 1 ? 1 : a.K);
-  const size_t smem = std::max((size_t)(a.rank_order ? Pf : 0) * 8, (size_t)((a.K + 3) & ~3) * 4) +
-                      (size_t)s->W * 4;
+  size_t smem = std::max((size_t)(a.rank_order ? Pf : 0) * 8, (size_t)((a.K + 3) & ~3) * 4) +
+                (size_t)s->W * 4;
+  smem = (smem + 15) & ~size_t(15);
+  p.stage_off = (int)smem;
+  p.stage_cap = (int)std::min<size_t>(kCandCap, (188 * 1024 - smem) / 8);  // + ~34 KB static
+  smem += (size_t)p.stage_cap * 8;
   ensure_smem((const void*)k2b_finish, smem);
   void* args[] = {(void*)&p};
   cudaError_t e = launch_pdl((const void*)k2b_finish, dim3(B), dim3(kSelThreads), smem, st, args);
