@@ -849,9 +849,12 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
 }  // namespace
 
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) {
+  using kvb::env_int;
   if (s->d.kv_dtype != KVB_BF16 || s->d.head_dim != kBD || s->d.kv_heads > 8 || G > 8 || G < 1)
     return false;
-  if (s->off_host) return false;
+  // host-mapped offload tier: cp.async.bulk reads the pinned, device-mapped
+  // host pages directly (KVB_BULK_HOST=0 selects the cp.async kernel instead)
+  if (s->off_host && env_int("KVB_BULK_HOST", 1) == 0) return false;
   // SVD ranks: whole, even numbers of 16-wide k-steps up to 160 (compile-time k loop)
   if (s->d.slow_kind == KVB_SLOW_SVD &&
       (s->d.svd_rank % 32 != 0 || s->d.svd_rank > 16 * kBMaxKs ||
