@@ -909,7 +909,8 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
 
 int64_t kvb_select_candidates_workspace_bytes(const kvb_store* s, int32_t k) {
   if (!s) return -1;
-  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned((size_t)s->d.batch * 4) + 256);
+  return (int64_t)(aligned((size_t)s->d.batch * s->C * 4) + aligned((size_t)s->d.batch * 4) +
+                   aligned(select2_ws_bytes(s, k)) + 256);
 }
 
 kvb_status kvb_select_candidates(kvb_store* s, const float* q, int32_t G, int32_t k, int32_t agg,
@@ -925,7 +926,16 @@ kvb_status kvb_select_candidates(kvb_store* s, const float* q, int32_t G, int32_
   cudaStream_t st = as_stream(stream);
   Carve cv(ws, ws_bytes);
   float* sc = cv.take<float>((size_t)s->d.batch * s->C);
-  if ((ks = score_landmarks(s, q, G, agg, sc, st)) != KVB_OK) return ks;
+  (void)cv.take<int32_t>((size_t)s->d.batch);
+  // dense sum: histogram-carrying scan + whole-GPU K2a split + K2b finish
+  const bool use_hist = agg == KVB_AGG_SUM && s->d.landmark_kind == KVB_LM_DENSE;
+  if (use_hist && s->k2_dirty) {
+    KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+    KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * s->d.batch * 4, st), "meta reset");
+    s->k2_dirty = false;
+  }
+  if (use_hist) s->k2_dirty = true;
+  if ((ks = score_landmarks(s, q, G, agg, sc, st, use_hist ? s->k2_hist : nullptr)) != KVB_OK) return ks;
   SelectLaunch L{};
   L.scores = sc;
   L.M_stride = s->C;
@@ -935,6 +945,13 @@ kvb_status kvb_select_candidates(kvb_store* s, const float* q, int32_t G, int32_
   L.sel_ids = cand_ids;
   L.sel_scores = cand_scores;
   L.id_offset = chunk_offset;
+  if (use_hist) {
+    L.hist = s->k2_hist;
+    void* s2ws = cv.take<char>(select2_ws_bytes(s, k));
+    KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "local top-k");
+    s->k2_dirty = false;
+    return KVB_OK;
+  }
   KVB_CUDA(launch_select(s, L, st), "local top-k");
   return KVB_OK;
 }

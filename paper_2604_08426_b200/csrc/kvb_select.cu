@@ -493,6 +493,8 @@ struct K2bParams {
   uint32_t* hist;        // [B][2048] store scratch: re-zeroed here after K2a consumed it
   K2Meta* meta_rw;       // [B] store scratch: re-zeroed here after reading
   int stage_off, stage_cap;  // shared staging of the candidates
+  float* sel_scores;         // [B][K] scores of the selected ids (optional)
+  int id_offset;             // added to emitted ids (sharding)
   uint64_t* trace;           // profiling: [B][8] %globaltimer stamps or null
 };
 
@@ -560,7 +562,8 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     q.stage = 0;
     q.hist = nullptr;
     q.id_offset = 0;
-    q.sel_scores = nullptr;
+    q.sel_scores = p.sel_scores;
+    q.id_offset = p.id_offset;
     select_body(q, smem_raw);
     if (p.sorted && !p.rank_order) {
       __shared__ int s_n;
@@ -658,9 +661,13 @@ __global__ void __launch_bounds__(kSelThreads) k2b_finish(K2bParams p) {
     token_union(nullptr, 0, (p.M + 31) / 32, bm, [&](int r) { return (int)ids[r]; }, K, 0, 1, p.M,
                 nullptr, 0, p.M, p.out_ids + (size_t)b * p.K, K, &s_n, nullptr, red);
     k2b_stamp(p, 5);
-  } else if (p.out_ids != p.sel) {
-    for (int r = tid; r < p.K; r += nthr)
-      p.out_ids[(size_t)b * p.K + r] = r < K ? ids[r] : -1;
+  } else if (p.out_ids != p.sel || p.sel_scores || p.id_offset) {
+    for (int r = tid; r < p.K; r += nthr) {
+      const int id = r < K ? ids[r] : -1;
+      p.out_ids[(size_t)b * p.K + r] = id < 0 ? -1 : id + p.id_offset;
+      if (p.sel_scores)
+        p.sel_scores[(size_t)b * p.K + r] = id < 0 ? -INFINITY : p.scores[(size_t)b * p.M + id];
+    }
   }
   if (!p.token_ids) return;
   __syncthreads();
@@ -739,6 +746,8 @@ cudaError_t launch_select2(const kvb_store* s, const SelectLaunch& a, void* ws, 
   p.hist = const_cast<uint32_t*>(a.hist);
   p.meta_rw = meta;
   p.trace = trace_buffer() ? trace_buffer() + 49152 : nullptr;  // profiling hook
+  p.sel_scores = a.sel_scores;
+  p.id_offset = a.id_offset;
   // room for the in-kernel radix fallback too: max(P*8, K*4) + bitmap
   const int Pf = next_pow2(a.K < 1 ? 1 : a.K);
   size_t smem = std::max((size_t)(a.rank_order ? Pf : 0) * 8, (size_t)((a.K + 3) & ~3) * 4) +
