@@ -40,6 +40,7 @@ VARIANTS = {
     # name: (description, landmark, chunk, slow, budget tokens, outliers, local)
     "shadowkv": "C2 ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
     "higgs2c1": "C2 paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
+    "shadowkv_recon": "C2 ShadowKV, keys reconstructed on tcgen05 (K3: left.right in TMEM, q.k epilogue) instead of the q~ = right.q fold",
     "shadowkv_host": "C3 ShadowKV with V offloaded to pinned, device-mapped host memory (zero-copy gather over the host link)",
     "c4": "C4 Qwen2.5-7B-1M shape (28 q / 4 kv heads), 1M ctx, batch 1, ShadowKV r160/cs8, sequence-sharded over the GPUs: global top-K + LSE merge by NCCL all-gather",
 }
@@ -58,7 +59,7 @@ def parse():
     ap.add_argument("--budget", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--also", default="higgs2c1",
+    ap.add_argument("--also", default="higgs2c1,shadowkv_recon",
                     help="comma-separated secondary variants reported under 'variants'")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N eager steps after setup (for ncu) and exit")
@@ -157,7 +158,7 @@ def build_layers(a, rank):
         shape = (a.batch, a.ctx, H, D)
         k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
         v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
-        if a.variant in ("shadowkv", "shadowkv_host"):
+        if a.variant in ("shadowkv", "shadowkv_host", "shadowkv_recon"):
             st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
                              dtype=torch.bfloat16, landmark=S.scheme_none(),
                              slow=S.scheme_svd(160, H * D), svd_groups=1,
@@ -203,7 +204,7 @@ def algorithmic_bytes(a, st, G):
     S_tok = K * st.cs
     R = st.max_resident
     q = H * G * D * 4 + H * G * D * 4  # queries in, output out
-    if a.variant in ("shadowkv", "shadowkv_host"):
+    if a.variant in ("shadowkv", "shadowkv_host", "shadowkv_recon"):
         lm = st.C * E * 2
         r = st.slow.rank
         return {"landmarks": lm, "left_rows": S_tok * r * 2, "right": r * E * 2,
@@ -345,7 +346,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     L_ = a.layers
     B = a.batch
     K = stores[0].n_select(a.budget / a.ctx)
-    plans = [st.decode_plan(G, K) for st in stores]
+    plans = [st.decode_plan(G, K, k_path=2 if variant == "shadowkv_recon" else 0) for st in stores]
     qgen = torch.Generator(device="cuda").manual_seed(7 + rank)
     q_dev = torch.randn((L_, B, H, G, D), generator=qgen, device="cuda")
     out_dev = torch.empty_like(q_dev)
@@ -447,17 +448,23 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         torch.cuda.synchronize()
         return s0.elapsed_time(s1) / (reps * L_)
 
-    if variant in ("shadowkv", "shadowkv_host"):
+    if variant in ("shadowkv", "shadowkv_host", "shadowkv_recon"):
         g_score = stage_graph(lambda: [stores[l].score(q_dev[l], out=scores[l]) for l in range(L_)])
         k1_kernel = "k1_dense_sum (kvb_score_landmarks)"
     else:
         g_score = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
         k1_kernel = "k1h_score + k2_select (kvb_select, HIGGS tensor-core scan)"
     g_select = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
-    g_attend = stage_graph(lambda: [plans[l].attend_only(q_dev[l], out_dev[l]) for l in range(L_)])
     k1_ms = stage_ms(g_score)
     sel_ms = stage_ms(g_select)
-    att_ms = stage_ms(g_attend)
+    if variant == "shadowkv_recon":
+        # K3 consumes the decode step's chunk stream: no token-list attention
+        # entry point to time on its own -> attention = step - selection
+        g_attend = None
+        att_ms = ms_max / L_ - sel_ms
+    else:
+        g_attend = stage_graph(lambda: [plans[l].attend_only(q_dev[l], out_dev[l]) for l in range(L_)])
+        att_ms = stage_ms(g_attend)
     ab = algorithmic_bytes(a, st0, G)
     lm_key = "landmarks" if variant != "higgs2c1" else "landmark_codes"
     k1_bytes = B * (ab[lm_key] + H * G * D * 4)

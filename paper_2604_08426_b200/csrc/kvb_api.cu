@@ -218,6 +218,7 @@ void free_store(kvb_store* s) {
   cudaFree(s->res_v);
   cudaFree(s->svd_left);
   cudaFree(s->svd_right);
+  cudaFree(s->svd_rightT);
   if (s->off_host) {
     cudaFreeHost(s->off_k);
     cudaFreeHost(s->off_v);
@@ -361,6 +362,7 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
     const size_t r = d.svd_rank, g = d.svd_groups, Dg = E / g;
     if ((st = dalloc(&s->svd_left, B * n * g * r, "svd left")) != KVB_OK) return bail(st);
     if ((st = dalloc(&s->svd_right, B * g * r * Dg, "svd right")) != KVB_OK) return bail(st);
+    if (g == 1 && (st = dalloc(&s->svd_rightT, B * r * Dg, "svd right^T")) != KVB_OK) return bail(st);
   }
   *out = s;
   return KVB_OK;
@@ -540,6 +542,7 @@ kvb_status kvb_store_set_svd(kvb_store* s, const void* left16, const void* right
   cudaStream_t st = as_stream(stream);
   KVB_CUDA(cudaMemcpyAsync(s->svd_left, left16, B * n * g * r * 2, cudaMemcpyDefault, st), "svd left");
   KVB_CUDA(cudaMemcpyAsync(s->svd_right, right16, B * g * r * Dg * 2, cudaMemcpyDefault, st), "svd right");
+  if (s->svd_rightT) KVB_CUDA(launch_transpose_right(s, st), "svd right^T");
   return KVB_OK;
 }
 
@@ -801,9 +804,12 @@ kvb_status kvb_attend(kvb_store* s, const float* q, const kvb_attend_args* a,
 int64_t kvb_decode_workspace_bytes(const kvb_store* s, const kvb_select_args* sel,
                                    const kvb_attend_args* att) {
   if (!s || !sel || !att) return -1;
+  const size_t logits = att->k_path == 2 && s->d.slow_kind == KVB_SLOW_SVD
+                            ? recon_logits_bytes(s, att->queries_per_head, sel->n_select)
+                            : 0;
   return (int64_t)(aligned(kvb_select_workspace_bytes(s, sel)) +
                    aligned((size_t)s->d.batch * sel->n_select * 4) +
-                   aligned(kvb_attend_workspace_bytes(s, att)) + 512);
+                   aligned(kvb_attend_workspace_bytes(s, att)) + aligned(logits) + 512);
 }
 
 kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* sel,
@@ -826,8 +832,13 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   if ((ks = check_queries(s, att->queries_per_head)) != KVB_OK) return ks;
   if ((ks = check_attend_shape(s)) != KVB_OK) return ks;
   if (att->queries_per_head != sel->queries_per_head) KVB_FAIL(KVB_EINVAL, "G mismatch");
-  if (s->d.slow_kind == KVB_SLOW_SVD && att->k_path == 2)
-    KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction path not built in this version");
+  const bool recon = s->d.slow_kind == KVB_SLOW_SVD && att->k_path == 2;
+  if (recon && !recon_supported(s, att->queries_per_head))
+    KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction needs a head-concatenated SVD (groups 1), "
+                               "rank % 16 == 0, head_dim 128");
+  float* recon_logits = recon ? cv.take<float>(recon_logits_bytes(s, att->queries_per_head,
+                                                                   sel->n_select) / 4)
+                              : nullptr;
   // fork: per-step query prep (q transpose, q~ = right.q, split tickets) on
   // the side stream, overlapping the landmark scan and top-K on the caller's
   // stream; join before the attention. When the selected chunks come out
@@ -863,7 +874,7 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   // attention-side top-K: every attention CTA streams the sequence's C scores
   // once (L2), cheap for chunked landmarks; at chunk 1 (C = n) the whole-GPU
   // K2a split + per-sequence K2b finish is used instead
-  if (chunk_path && sel->aggregation == KVB_AGG_SUM && s->C <= 32768 &&
+  if (chunk_path && !recon && sel->aggregation == KVB_AGG_SUM && s->C <= 32768 &&
       (s->d.landmark_kind == KVB_LM_DENSE || tc_scan)) {
     // scan (scores + top-11-bit key histogram) -> attention whose prologue
     // runs the exact top-K (kvb_fuse.cuh); no separate selection kernels
@@ -898,10 +909,14 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   }
   if (chunk_path) {
     // the attention also emits the sorted token union (token_ids, n_tokens)
+    if (recon)  // K3: reconstructed-key logits on tcgen05 (kvb_recon.cu)
+      KVB_CUDA(launch_recon_logits(s, q, L.G, cid, K, recon_logits, st), "K3 reconstruction");
     KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
-    KVB_CUDA(launch_attend_chunks(s, L, cid, K, st), "sparse attention");
+    KVB_CUDA(launch_attend_chunks(s, L, cid, K, st, nullptr, nullptr, nullptr, recon_logits),
+             "sparse attention");
     return KVB_OK;
   }
+  if (recon) KVB_FAIL(KVB_EUNSUPPORTED, "tcgen05 reconstruction needs the chunk-stream attention");
   KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
   KVB_CUDA(launch_attend_main(s, L, st), "sparse attention");
   return KVB_OK;

@@ -79,6 +79,7 @@ struct BulkParams {
   uint64_t* trace;            // profiling: [B][S][8] phase stamps or null
   // chunk mode: the sorted token union (the reference's token_ids) is emitted
   // here, each CTA writing its own share at merge-path ranks
+  const float* svd_logits;    // chunk mode: K3 logits [B][K*cs][HG] (kvb_recon.cu) or null
   const float* sel_scores;    // chunk mode: scan scores [B][C] -> top-K here (kvb_fuse.cuh)
   const uint32_t* sel_hist;   // [B][2048] top-11-bit key histogram of those scores
   int Wc;
@@ -215,6 +216,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
   pdl_trigger();
   uint32_t* tab_ex = reinterpret_cast<uint32_t*>(sm + p.off_tab);
   uint32_t* tab_sv = tab_ex + p.maxper;
+  int32_t* tab_pos = reinterpret_cast<int32_t*>(tab_sv + p.maxper);  // svd_logits: stream index
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + p.off_bar);
   const int nst = p.nst, ett = p.ett;
   uint64_t* empty = full + nst;
@@ -358,6 +360,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     const int i = base + tid;
     uint32_t e = 0;
     int kind = -1;  // 0 exact, 1 svd
+    int spos = 0;   // chunk mode: stream index of an SVD entry (K3 logits row)
     if (i < i1) {
       if (p.mode == 0) {
         const int t = p.items[(size_t)b * p.cap + i];
@@ -389,6 +392,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
           if (!(lo < nres && ur[lo] == t)) {  // residents are served by the first part
             e = (uint32_t)t | ((p.svd ? 2u : 1u) << kTierShift);
             kind = p.svd ? 1 : 0;
+            spos = j;
             const int pos = j + lo - ud[lo];
             if (p.tok_out && pos < p.tcap) p.tok_out[(size_t)b * p.tcap + pos] = t;
           }
@@ -399,7 +403,10 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     const int v = (kind == 0 ? 1 : 0) | (kind == 1 ? 1 << 16 : 0);
     const int ex = block_excl_scan(v, red, &tot);
     if (kind == 0) tab_ex[s_cnt[0] + (ex & 0xffff)] = e;
-    if (kind == 1) tab_sv[s_cnt[1] + (ex >> 16)] = e;
+    if (kind == 1) {
+      tab_sv[s_cnt[1] + (ex >> 16)] = e;
+      tab_pos[s_cnt[1] + (ex >> 16)] = spos;
+    }
     __syncthreads();
     if (tid == 0) {
       s_cnt[0] += tot & 0xffff;
@@ -447,7 +454,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     const uint32_t e = j < cnt ? (sv ? tab_sv : tab_ex)[base + j] : 0u;
     const uint32_t tier = e >> kTierShift, idx = e & ((1u << kTierShift) - 1u);
     const int krow = sv ? p.krow_sv : p.krow_ex;
-    const int kb = sv ? lbytes : vbytes;
+    const int kb = sv ? (p.svd_logits ? HG * 4 : lbytes) : vbytes;
     uint32_t bytes = 0;
     if (lane < 16 && j < cnt) bytes = (uint32_t)(vbytes + kb);
     bytes = __reduce_add_sync(FULL, bytes);
@@ -473,7 +480,11 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
       } else {
         const size_t off = ((size_t)b * p.n + idx) * vbytes;
         vsrc = p.off_v + off;
-        ksrc = tier == 1 ? p.off_k + off : p.left + ((size_t)b * p.n + idx) * lbytes;
+        ksrc = tier == 1 ? p.off_k + off
+               : p.svd_logits
+                   ? reinterpret_cast<const unsigned char*>(
+                         p.svd_logits + ((size_t)b * p.K * p.cs + tab_pos[base + j]) * HG)
+                   : p.left + ((size_t)b * p.n + idx) * lbytes;
       }
       if (lane < 16) bulk_g2s(st + j * vrow, vsrc, vbytes, full + stg);
       else bulk_g2s(st + tt * vrow + j * krow, ksrc, kb, full + stg);
@@ -663,7 +674,30 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     }
   }
   // ---- SVD tiles: B = q~_h in fp16 hi | lo --------------------------------------------
-  if (NKS > 0 && t_sv > 0) {
+  if (NKS > 0 && t_sv > 0 && p.svd_logits) {
+    // K3 (kvb_recon.cu) already produced q.k of the reconstructed keys: the
+    // staged row of token j holds logits[(h, g)] for every head
+    for (int k = t_ex; k < ntiles; ++k) {
+      produce(k + nst - 1);
+      int stg, par;
+      next_slot(stg, par);
+      mbar_wait(full + stg, par);
+      const uint32_t st = ring_s + (uint32_t)(stg * p.stage_bytes);
+      const int cnt = min(kBT, n_sv - (k - t_ex) * kBT);
+      const float* lg = reinterpret_cast<const float*>(ring + (size_t)stg * p.stage_bytes +
+                                                       (size_t)kBT * vrow);
+      float sv[2][2];
+#pragma unroll
+      for (int th = 0; th < 2; ++th)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int row = g4 + 8 * th, qq = qa + jj;
+          sv[th][jj] = (qq < G) ? lg[(size_t)row * (p.krow_sv / 4) + h * G + qq] : 0.f;
+        }
+      softmax_pv(sv, cnt, st, kBT - 1);
+      release(stg);
+    }
+  } else if (NKS > 0 && t_sv > 0) {
     uint32_t bq[NKS > 0 ? NKS : 1][NTS][2];
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks)
@@ -835,7 +869,7 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
   }
   if (g.ett == kBT) g.stage_bytes = (kBT * (g.vrow + std::max(g.krow_ex, g.krow_sv)) + 127) & ~127;
   g.off_tab = 0;
-  g.off_uni = (2 * g.maxper * 4 + 127) & ~127;
+  g.off_uni = (3 * g.maxper * 4 + 127) & ~127;
   g.off_bar = (g.off_uni + (K + 2 * s->d.max_resident + 1) * 4 + 127) & ~127;
   g.off_stage = g.off_bar + 128;
   const size_t room = 227 * 1024 - g.off_stage - 2048;  // static smem + slack
@@ -919,6 +953,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.off_uni = g.off_uni;
   p.tok_out = a.mode == 1 ? a.tok_out : nullptr;
   p.sel_scores = a.mode == 1 ? a.sel_scores : nullptr;
+  p.svd_logits = a.mode == 1 ? a.svd_logits : nullptr;
   p.sel_hist = a.sel_hist;
   p.Wc = s->Wc;
   p.chunk_out = a.chunk_out;

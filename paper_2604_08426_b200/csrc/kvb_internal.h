@@ -46,6 +46,7 @@ struct kvb_store {
   void* res_v = nullptr;
   uint16_t* svd_left = nullptr;  // fp16 [B][n][groups][r]
   uint16_t* svd_right = nullptr; // fp16 [B][groups][r][Dg]
+  uint16_t* svd_rightT = nullptr; // fp16 [B][E][r] (groups == 1): K-major tcgen05 B operand
   // offload tier ------------------------------------------------------------
   void* off_k = nullptr;         // [B][n][E]  (slow_kind == NONE)
   void* off_v = nullptr;         // [B][n][E]
@@ -178,6 +179,7 @@ struct BulkLaunch {
   const float* sel_scores = nullptr;
   uint32_t* sel_hist = nullptr;      // re-zeroed by the merge kernel
   int32_t* chunk_out = nullptr;      // ascending selected chunk ids out [B][K] (optional)
+  const float* svd_logits = nullptr; // mode 1: K3 logits [B][K*cs][H*G] replace the q~.left fold
   int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
   int32_t* ntok_out = nullptr;  // [B]
   int tcap = 0;
@@ -188,7 +190,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
 // decode-step attention over residents + selected chunks (chunk ids [B][K])
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores = nullptr,
-                                 uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr);
+                                 uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr,
+                                 const float* svd_logits = nullptr);
 // the two halves of launch_attend: per-step query prep, then the attention
 cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
@@ -196,6 +199,14 @@ cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int p
                                    int D, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
                               int32_t* out, cudaStream_t st);
+
+// K3 reconstruction on tcgen05 (kvb_recon.cu): logits [B][K*cs][H*G] of the
+// selected SVD tokens, consumed by the bulk attention (svd_logits mode)
+bool recon_supported(const kvb_store* s, int G);
+size_t recon_logits_bytes(const kvb_store* s, int G, int K);
+cudaError_t launch_transpose_right(const kvb_store* s, cudaStream_t st);
+cudaError_t launch_recon_logits(const kvb_store* s, const float* q, int G, const int32_t* chunks,
+                                int K, float* logits, cudaStream_t st);
 
 // ---- build ---------------------------------------------------------------
 cudaError_t launch_chunk_means(const kvb_store* s, const void* keys, void* out_dense,
