@@ -202,7 +202,10 @@ __device__ __forceinline__ void bparts(float x, float y, uint32_t* o, int parts)
 // entry encoding: bits 0-29 index, bits 30-31 tier (0 resident slot, 1 offload token, 2 SVD token)
 constexpr uint32_t kTierShift = 30;
 
-template <int QW, int NKS>
+// VAR: 0 = plain (token or chunk list), 1 = K3 logits for SVD tokens,
+// 2 = top-K in the prologue (scores + histogram). Separate instances keep each
+// kernel's code small (instruction-cache misses dominated the prologue).
+template <int QW, int NKS, int VAR>
 __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ int red[33];
@@ -292,13 +295,15 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
   pdl_wait();  // the selection (token / chunk list) of the previous kernel
   KVB_STAMP(6);
-  if (p.mode == 1 && p.sel_scores) {
+  if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     // top-K from the scan's scores + histogram into a bitmap in the (not yet
     // used) ring, then ascending ids: each thread owns a run of words, one scan
     uint32_t* wb = reinterpret_cast<uint32_t*>(ring);
     uint32_t* sk = wb + ((p.Wc + 3) & ~3);
     const int cap = (int)(((size_t)nst * p.stage_bytes - (size_t)((p.Wc + 3) & ~3) * 4) / 8);
-    select_topk_shared(p.sel_scores + (size_t)b * p.C, p.C, p.sel_hist + (size_t)b * kFuseHistBins,
+    // (profiling: dbg & 4 -> only split 0 streams the scores, to isolate L2 contention)
+    select_topk_shared(p.sel_scores + (size_t)b * p.C, ((p.dbg & 4) && split) ? 0 : p.C,
+                       p.sel_hist + (size_t)b * kFuseHistBins,
                        p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
                        p.trace ? p.trace + (size_t)gridDim.y * gridDim.x * 8 + 64 +
                                      ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8
@@ -674,7 +679,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     }
   }
   // ---- SVD tiles: B = q~_h in fp16 hi | lo --------------------------------------------
-  if (NKS > 0 && t_sv > 0 && p.svd_logits) {
+  if (VAR == 1 && NKS > 0 && t_sv > 0) {
     // K3 (kvb_recon.cu) already produced q.k of the reconstructed keys: the
     // staged row of token j holds logits[(h, g)] for every head
     for (int k = t_ex; k < ntiles; ++k) {
@@ -697,7 +702,7 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
       softmax_pv(sv, cnt, st, kBT - 1);
       release(stg);
     }
-  } else if (NKS > 0 && t_sv > 0) {
+  } else if (VAR != 1 && NKS > 0 && t_sv > 0) {
     uint32_t bq[NKS > 0 ? NKS : 1][NTS][2];
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks)
@@ -968,15 +973,20 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.dbg = dbg;
   count_launch(2);
   const int nks = svd ? s->d.svd_rank / 16 : 0;
+  const int var = p.svd_logits ? 1 : (p.sel_scores ? 2 : 0);
   const void* fn = nullptr;
+#define KVB_BULK_VAR(Q, N)                                                     \
+  fn = var == 0 ? (const void*)k5_attend_bulk<Q, N, 0>                          \
+                : var == 2 ? (const void*)k5_attend_bulk<Q, N, 2>               \
+                           : (N > 0 ? (const void*)k5_attend_bulk<Q, (N > 0 ? N : 2), 1> : nullptr);
 #define KVB_BULK_PICK(Q)                                                       \
   switch (nks) {                                                               \
-    case 0: fn = (const void*)k5_attend_bulk<Q, 0>; break;                     \
-    case 2: fn = (const void*)k5_attend_bulk<Q, 2>; break;                     \
-    case 4: fn = (const void*)k5_attend_bulk<Q, 4>; break;                     \
-    case 6: fn = (const void*)k5_attend_bulk<Q, 6>; break;                     \
-    case 8: fn = (const void*)k5_attend_bulk<Q, 8>; break;                     \
-    case 10: fn = (const void*)k5_attend_bulk<Q, 10>; break;                   \
+    case 0: KVB_BULK_VAR(Q, 0) break;                                          \
+    case 2: KVB_BULK_VAR(Q, 2) break;                                          \
+    case 4: KVB_BULK_VAR(Q, 4) break;                                          \
+    case 6: KVB_BULK_VAR(Q, 6) break;                                          \
+    case 8: KVB_BULK_VAR(Q, 8) break;                                          \
+    case 10: KVB_BULK_VAR(Q, 10) break;                                        \
     default: return cudaErrorNotSupported;                                     \
   }
   if (a.G <= 4) {
@@ -985,6 +995,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
     KVB_BULK_PICK(8)
   }
 #undef KVB_BULK_PICK
+#undef KVB_BULK_VAR
+  if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
   cudaError_t le = launch_pdl(fn, dim3(g.splits, B), dim3(H * 32), g.smem, st, args);
