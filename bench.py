@@ -42,6 +42,7 @@ VARIANTS = {
     "higgs2c1": "C2 paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
     "shadowkv_recon": "C2 ShadowKV, keys reconstructed on tcgen05 (K3: left.right in TMEM, q.k epilogue) instead of the q~ = right.q fold",
     "shadowkv_host": "C3 ShadowKV with V offloaded to pinned, device-mapped host memory (zero-copy gather over the host link)",
+    "c5": "C5 paper's proposed selection (HIGGS 2-bit landmarks, exact K+V in HBM), token-budget x chunk-size sweep at 128K ctx, batch 32, one layer per point",
     "c4": "C4 Qwen2.5-7B-1M shape (28 q / 4 kv heads), 1M ctx, batch 1, ShadowKV r160/cs8, sequence-sharded over the GPUs: global top-K + LSE merge by NCCL all-gather",
 }
 
@@ -486,6 +487,68 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     return res
 
 
+def run_c5(a, rank, world, local):
+    """C5: budget 512-8192 x chunk 4-32 sweep of the proposed selection at 128K,
+    batch 32, one layer per point (the full 32-layer state does not
+    fit); every point is one decode step of B = 32 sequences in a CUDA graph."""
+    import torch
+
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    H, G, D = 8, 4, 128
+    n, B = a.ctx, 32 if a.batch == 8 else a.batch
+    hbm, kind = peaks()
+    rows = []
+    gen = torch.Generator(device="cuda")
+    for cs in (4, 8, 16, 32):
+        gen.manual_seed(100 + cs + rank)
+        k = torch.randn((B, n, H, D), generator=gen, device="cuda", dtype=torch.bfloat16)
+        v = torch.randn((B, n, H, D), generator=gen, device="cuda", dtype=torch.bfloat16)
+        st = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=cs,
+                         dtype=torch.bfloat16, landmark=S.scheme_higgs(2), outlier_tokens=384,
+                         local_window=32)
+        st.build(k, v)
+        del k, v
+        q = torch.randn((B, H, G, D), generator=gen, device="cuda")
+        for budget in (512, 1024, 2048, 4096, 8192):
+            K = st.n_select(budget / n)
+            plan = st.decode_plan(G, K)
+            out = torch.empty((B, H, G, D), device="cuda")
+            plan.run(q, out)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                plan.run(q, out)
+            for _ in range(max(3, a.warmup)):
+                g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(5, a.steps)
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            C = st.C
+            nbytes = B * (C * H * D // 4 + (C // 8) * H * 4 + (K * cs + st.max_resident) * H * D * 2 * 2)
+            rows.append({"chunk": cs, "budget_tokens": budget, "K": K, "ms_per_layer": round(ms, 4),
+                         "tok_s_per_layer": round(B / (ms / 1e3), 1),
+                         "frac_of_hbm": round(nbytes / (ms / 1e3) / 1e9 / hbm, 4)})
+            del plan, g
+        st.close()
+        del st
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    if rank == 0:
+        print(json.dumps({"metric": "C5 sweep: decode ms per layer (B=32, 128K) of the proposed selection",
+                          "impl": "kvb", "n_gpus": world, "unit": "ms/layer", "higher_is_better": False,
+                          "dtype": "bf16", "data": "synthetic (torch.randn K/V, random queries)",
+                          "config": {"workload": VARIANTS["c5"], "seq_len": n, "global_batch": B},
+                          "sweep": rows}), flush=True)
+
+
 def run_c4(a, rank, world, local):
     """C4: one 1M-token sequence sharded over `world` GPUs (strong scaling)."""
     import torch
@@ -595,6 +658,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     primary = a.variant
+    if primary == "c5":
+        run_c5(a, rank, world, local)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if primary == "c4":
         run_c4(a, rank, world, local)
         if world > 1:
