@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--also", default="higgs2c1,shadowkv_recon",
                     help="comma-separated secondary variants reported under 'variants'")
+    ap.add_argument("--microbatches", type=int, default=1,
+                    help="split the batch into this many stores per layer, each decode chain on its own stream")
+    ap.add_argument("--mb-offset", type=int, default=0,
+                    help="micro-batch m starts after micro-batch m-1 finished this many layers")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N eager steps after setup (for ncu) and exit")
     return ap.parse_args()
@@ -154,19 +158,21 @@ def build_layers(a, rank):
     H, G, D = 8, 4, 128
     stores = []
     gen = torch.Generator(device="cuda")
-    for layer in range(a.layers):
+    mb = getattr(a, "microbatches", 1)
+    bsz = a.batch // mb
+    for layer in range(a.layers * mb):
         gen.manual_seed(1000 * rank + layer)
-        shape = (a.batch, a.ctx, H, D)
+        shape = (bsz, a.ctx, H, D)
         k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
         v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
         if a.variant in ("shadowkv", "shadowkv_host", "shadowkv_recon"):
-            st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
+            st = DeviceStore(batch=bsz, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
                              dtype=torch.bfloat16, landmark=S.scheme_none(),
                              slow=S.scheme_svd(160, H * D), svd_groups=1,
                              outlier_tokens=384, local_window=32,
                              offload="host" if a.variant == "shadowkv_host" else "hbm")
         else:
-            st = DeviceStore(batch=a.batch, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=1,
+            st = DeviceStore(batch=bsz, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=1,
                              dtype=torch.bfloat16, landmark=S.scheme_higgs(2),
                              outlier_tokens=384, local_window=32)
         st.build(k, v)
@@ -354,10 +360,32 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     q_host = q_dev.cpu().pin_memory()
     out_host = torch.empty_like(q_host).pin_memory()
     stream = torch.cuda.current_stream()
+    mb = a.microbatches
+    Bm = B // mb
+    mstreams = [torch.cuda.Stream() for _ in range(mb)] if mb > 1 else []
 
     def step():
+        if mb == 1:
+            for l in range(L_):
+                plans[l].run(q_dev[l], out_dev[l])
+            return
+        # micro-batch m owns stores [l * mb + m]; each chain runs its layers in
+        # order on its own stream (two-batch overlap); chain m may start
+        # mb_offset layers behind chain m-1
+        cur = torch.cuda.current_stream()  # the capture stream inside torch.cuda.graph
+        evs = [[torch.cuda.Event() for _ in range(L_)] for _ in range(mb)]
+        for m, s_ in enumerate(mstreams):
+            s_.wait_stream(cur)
         for l in range(L_):
-            plans[l].run(q_dev[l], out_dev[l])
+            for m, s_ in enumerate(mstreams):
+                with torch.cuda.stream(s_):
+                    if m > 0 and a.mb_offset and l == 0:
+                        s_.wait_event(evs[m - 1][min(a.mb_offset, L_) - 1])
+                    sl = slice(m * Bm, (m + 1) * Bm)
+                    plans[l * mb + m].run(q_dev[l, sl], out_dev[l, sl])
+                    evs[m][l].record(s_)
+        for s_ in mstreams:
+            cur.wait_stream(s_)
 
     if a.profile_steps:
         for _ in range(a.profile_steps):
@@ -401,8 +429,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     # end to end through the public API with host buffers
     def e2e_step():
         q_dev.copy_(q_host, non_blocking=True)
-        for l in range(L_):
-            plans[l].run(q_dev[l], out_dev[l])
+        step()
         out_host.copy_(out_dev, non_blocking=True)
 
     for _ in range(max(2, a.warmup)):
@@ -426,7 +453,11 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
 
     # per-stage device time: one CUDA graph per stage over all layers
     st0 = stores[0]
-    scores = [torch.empty((B, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
+    scores = [torch.empty((Bm, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
+    qb = [q_dev[l, :Bm] for l in range(L_)]          # micro-batch 0 (all of it when mb = 1)
+    ob = [out_dev[l, :Bm] for l in range(L_)]
+    sp = [stores[l * mb] for l in range(L_)]
+    pp = [plans[l * mb] for l in range(L_)]
 
     def stage_graph(fn):
         fn()
@@ -450,12 +481,12 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         return s0.elapsed_time(s1) / (reps * L_)
 
     if variant in ("shadowkv", "shadowkv_host", "shadowkv_recon"):
-        g_score = stage_graph(lambda: [stores[l].score(q_dev[l], out=scores[l]) for l in range(L_)])
+        g_score = stage_graph(lambda: [sp[l].score(qb[l], out=scores[l]) for l in range(L_)])
         k1_kernel = "k1_dense_sum (kvb_score_landmarks)"
     else:
-        g_score = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
+        g_score = stage_graph(lambda: [pp[l].select_only(qb[l]) for l in range(L_)])
         k1_kernel = "k1h_score + k2_select (kvb_select, HIGGS tensor-core scan)"
-    g_select = stage_graph(lambda: [plans[l].select_only(q_dev[l]) for l in range(L_)])
+    g_select = stage_graph(lambda: [pp[l].select_only(qb[l]) for l in range(L_)])
     k1_ms = stage_ms(g_score)
     sel_ms = stage_ms(g_select)
     if variant == "shadowkv_recon":
@@ -464,7 +495,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         g_attend = None
         att_ms = ms_max / L_ - sel_ms
     else:
-        g_attend = stage_graph(lambda: [plans[l].attend_only(q_dev[l], out_dev[l]) for l in range(L_)])
+        g_attend = stage_graph(lambda: [pp[l].attend_only(qb[l], ob[l]) for l in range(L_)])
         att_ms = stage_ms(g_attend)
     ab = algorithmic_bytes(a, st0, G)
     lm_key = "landmarks" if variant != "higgs2c1" else "landmark_codes"
