@@ -793,43 +793,37 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
 // k5_attend_bulk (which triggers its dependents at entry), so its CTAs are
 // resident before the attention drains; griddepcontrol.wait then orders the
 // reads after the attention grid has completed and flushed.
-__global__ void __launch_bounds__(128, 8) k5_merge_rows(const float* __restrict__ pm,
+__global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict__ pm,
                                                      const float* __restrict__ pl,
                                                      const float* __restrict__ po, int S, int HG,
                                                      float* __restrict__ out, float* __restrict__ lse,
                                                      uint32_t* __restrict__ hist_clear) {
-  const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x, lane = d & 31;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // the attention (complete) was the last reader of the scan's histogram
   if (hist_clear && row == 0)
     for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
   const size_t base = (size_t)b * S * HG + row;
   float m = -INFINITY, acc = 0.f, L = 0.f;
-  constexpr int CH = 8;  // splits per round: every load of a round in flight
+  constexpr int CH = 32;  // splits per round: one round for S <= 32, every load in flight
   for (int s0 = 0; s0 < S; s0 += CH) {
-    float mv[CH], lv[CH], ov[CH];
+    // split (s0 + lane)'s (m, l) in lane registers; this thread's o column for all CH splits
+    const int sl = s0 + lane;
+    const float ml = sl < S ? __ldcg(pm + base + (size_t)sl * HG) : -INFINITY;
+    const float ll = sl < S ? __ldcg(pl + base + (size_t)sl * HG) : 0.f;
+    float ov[CH];
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
       const int s2 = s0 + k;
-      const size_t gi = base + (size_t)s2 * HG;
-      mv[k] = s2 < S ? __ldcg(pm + gi) : -INFINITY;
-      lv[k] = s2 < S ? __ldcg(pl + gi) : 0.f;
-      ov[k] = s2 < S ? __ldcg(po + gi * 128 + d) : 0.f;
+      ov[k] = s2 < S ? __ldcg(po + (base + (size_t)s2 * HG) * 128 + d) : 0.f;
     }
-    float mr = m;
-#pragma unroll
-    for (int k = 0; k < CH; ++k)
-      if (lv[k] > 0.f) mr = fmaxf(mr, mv[k]);
+    const float mr = fmaxf(m, warp_max(ll > 0.f ? ml : -INFINITY));
     const float al = (m == -INFINITY) ? 0.f : expf(m - mr);
+    const float wl = ll > 0.f ? expf(ml - mr) : 0.f;  // weight of split s0 + lane
     acc *= al;
-    L *= al;
+    L = L * al + warp_sum_butterfly(wl * ll);
 #pragma unroll
-    for (int k = 0; k < CH; ++k)
-      if (lv[k] > 0.f) {
-        const float w = expf(mv[k] - mr);
-        acc = fmaf(ov[k], w, acc);
-        L = fmaf(w, lv[k], L);
-      }
+    for (int k = 0; k < CH; ++k) acc = fmaf(ov[k], __shfl_sync(FULL, wl, k), acc);
     m = mr;
   }
   out[((size_t)b * HG + row) * 128 + d] = acc / L;
