@@ -40,6 +40,8 @@ VARIANTS = {
     # name: (description, landmark, chunk, slow, budget tokens, outliers, local)
     "shadowkv": "C2 ShadowKV baseline: bf16 chunk-8 landmarks, rank-160 SVD keys, V offloaded (HBM tier)",
     "higgs2c1": "C2 paper's proposed selection: HIGGS 2-bit landmarks at chunk 1, exact K+V offloaded (HBM tier)",
+    "higgs4c2": "C2 paper's proposed selection, equal-memory variant: HIGGS 4-bit landmarks at chunk 2, exact K+V offloaded (HBM tier)",
+    "proposed_b": "C2 paper's Appendix-E variant: HIGGS 4-bit@8 landmarks + 1-bit residuals, two-stage top-k (k 2048 tokens, candidate multiplier 8), exact K+V",
     "shadowkv_recon": "C2 ShadowKV, keys reconstructed on tcgen05 (K3: left.right in TMEM, q.k epilogue) instead of the q~ = right.q fold",
     "shadowkv_host": "C3 ShadowKV with V offloaded to pinned, device-mapped host memory (zero-copy gather over the host link)",
     "c5": "C5 paper's proposed selection (HIGGS 2-bit landmarks, exact K+V in HBM), token-budget x chunk-size sweep at 128K ctx, batch 32, one layer per point",
@@ -171,6 +173,14 @@ def build_layers(a, rank):
                              slow=S.scheme_svd(160, H * D), svd_groups=1,
                              outlier_tokens=384, local_window=32,
                              offload="host" if a.variant == "shadowkv_host" else "hbm")
+        elif a.variant == "higgs4c2":
+            st = DeviceStore(batch=bsz, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=2,
+                             dtype=torch.bfloat16, landmark=S.scheme_higgs(4),
+                             outlier_tokens=384, local_window=32)
+        elif a.variant == "proposed_b":
+            st = DeviceStore(batch=bsz, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=8,
+                             dtype=torch.bfloat16, landmark=S.scheme_higgs(4),
+                             residual=S.scheme_higgs(1), outlier_tokens=384, local_window=32)
         else:
             st = DeviceStore(batch=bsz, n_tokens=a.ctx, kv_heads=H, head_dim=D, chunk_size=1,
                              dtype=torch.bfloat16, landmark=S.scheme_higgs(2),
@@ -218,6 +228,11 @@ def algorithmic_bytes(a, st, G):
                 "values": S_tok * E * 2, "resident_kv": R * E * 2 * 2, "q_out": q}
     lm = st.info.n_groups_landmark * H * (st.landmark.group_size // st.landmark.d *
                                           (st.landmark.n.bit_length() - 1) // 8 + 4)
+    if a.variant == "proposed_b":
+        k_tok = a.budget
+        n_cand = min(st.C, 8 * -(-k_tok // st.cs))
+        return {"landmark_codes": lm, "residual_codes": n_cand * st.cs * E // 8,
+                "kv": k_tok * E * 2 * 2, "resident_kv": R * E * 2 * 2, "q_out": q}
     return {"landmark_codes": lm, "kv": S_tok * E * 2 * 2, "resident_kv": R * E * 2 * 2, "q_out": q}
 
 
@@ -365,6 +380,13 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     mstreams = [torch.cuda.Stream() for _ in range(mb)] if mb > 1 else []
 
     def step():
+        if variant == "proposed_b":
+            # Appendix E: two-stage residual top-k (kvb_select_residual) then
+            # the token-list attention (kvb_attend); k = budget tokens, mult 8
+            for l in range(L_):
+                _, _, tok, ntok = stores[l].select_residual(q_dev[l], a.budget, 8, want_scores=False)
+                out_dev[l].copy_(stores[l].attend(q_dev[l], tok, ntok)[0])
+            return
         if mb == 1:
             for l in range(L_):
                 plans[l].run(q_dev[l], out_dev[l])
@@ -487,9 +509,12 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         g_score = stage_graph(lambda: [pp[l].select_only(qb[l]) for l in range(L_)])
         k1_kernel = "k1h_score + k2_select (kvb_select, HIGGS tensor-core scan)"
     g_select = stage_graph(lambda: [pp[l].select_only(qb[l]) for l in range(L_)])
+    if variant == "proposed_b":
+        g_select = stage_graph(lambda: [sp[l].select_residual(qb[l], a.budget, 8, want_scores=False)
+                                        for l in range(L_)])
     k1_ms = stage_ms(g_score)
     sel_ms = stage_ms(g_select)
-    if variant == "shadowkv_recon":
+    if variant in ("shadowkv_recon", "proposed_b"):
         # K3 consumes the decode step's chunk stream: no token-list attention
         # entry point to time on its own -> attention = step - selection
         g_attend = None
@@ -498,7 +523,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         g_attend = stage_graph(lambda: [pp[l].attend_only(qb[l], ob[l]) for l in range(L_)])
         att_ms = stage_ms(g_attend)
     ab = algorithmic_bytes(a, st0, G)
-    lm_key = "landmarks" if variant != "higgs2c1" else "landmark_codes"
+    lm_key = "landmarks" if variant.startswith("shadowkv") else "landmark_codes"
     k1_bytes = B * (ab[lm_key] + H * G * D * 4)
     step_bytes = L_ * B * sum(ab.values())
     res = {
