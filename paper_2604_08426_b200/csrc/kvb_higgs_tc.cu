@@ -33,7 +33,7 @@ namespace {
 constexpr int kR = 8;      // rows per group
 constexpr int kD = 128;    // head dim
 constexpr int kTileRows = 16;
-constexpr int kTPI = 4;      // tiles per iteration (64 landmark rows)
+constexpr int kTPIMax = 4;   // tiles per iteration (2-bit; 4-bit uses 2: register budget)
 
 __device__ __forceinline__ void mma_f16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
                                         uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -91,11 +91,15 @@ __device__ __forceinline__ void lds64(uint32_t& x, uint32_t& y, uint32_t addr) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(x), "=r"(y) : "r"(addr));
 }
 
-template <int HMAX>
+// BITS = 2 (n = 16 codewords, 4-bit code per value pair, pair LUT) or
+// BITS = 4 (n = 256, one code byte per pair: single-code LUTs, 32 lane copies
+// of 4-byte entries, one LDS.32 per A-fragment register).
+template <int HMAX, int BITS>
 __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     const uint8_t* __restrict__ codes, const float* __restrict__ factors,
     const float* __restrict__ W, const float* __restrict__ cb, float* __restrict__ scores,
     int rows, int H, int ngroups, int gbytes, int tiles_per_cta, uint32_t* __restrict__ hist) {
+  constexpr int kTPI = BITS == 2 ? 4 : 2;
   extern __shared__ __align__(16) unsigned char lut_raw[];  // [hi table][lo table]
   __shared__ float part[HMAX][kTPI * kTileRows];
   __shared__ uint32_t shist[kTopHistBins];   // first radix level of K2 (see k1_dense_sum)
@@ -105,8 +109,8 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y;
   pdl_trigger();
-  // pair tables: entry e = x + 16 y, copy c at byte (e * 16 + c) * 8
-  {
+  if constexpr (BITS == 2) {
+    // pair tables: entry e = x + 16 y, copy c at byte (e * 16 + c) * 8
     uint2* hi_t = reinterpret_cast<uint2*>(lut_raw);
     uint2* lo_t = reinterpret_cast<uint2*>(lut_raw + kLutBytes);
     for (int i = threadIdx.x; i < kPairEntries * kPairCopies; i += blockDim.x) {
@@ -118,8 +122,20 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
       lo_t[i] = make_uint2(h2u(__floats2half2_rn(cb[2 * x] - fx.x, cb[2 * x + 1] - fx.y)),
                            h2u(__floats2half2_rn(cb[2 * y] - fy.x, cb[2 * y + 1] - fy.y)));
     }
+  } else {
+    // single-code tables: entry e (256), copy c (32) at byte (e * 32 + c) * 4
+    uint32_t* hi_t = reinterpret_cast<uint32_t*>(lut_raw);
+    uint32_t* lo_t = reinterpret_cast<uint32_t*>(lut_raw + kLutBytes);
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int e = i >> 5;
+      const __half2 hx = __floats2half2_rn(cb[2 * e], cb[2 * e + 1]);
+      const float2 fx = __half22float2(hx);
+      hi_t[i] = h2u(hx);
+      lo_t[i] = h2u(__floats2half2_rn(cb[2 * e] - fx.x, cb[2 * e + 1] - fx.y));
+    }
   }
-  const uint32_t lane8 = (uint32_t)(lane & 15) * 8u;  // this lane's table copy
+  const uint32_t lane8 = BITS == 2 ? (uint32_t)(lane & 15) * 8u   // this lane's table copy
+                                   : (uint32_t)lane * 4u;
   // B fragments: thread (g4, tig) owns w_{g4}[32*tig + 4*ks + 0..3], ks = 0..7
   uint32_t bhi[8][2], blo[8][2];
   const int h = warp;
@@ -145,24 +161,34 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   // sign of H_8[k][a] for this lane's rows a = g4 and columns k = 2tig, 2tig+1
   const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
   const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
-  // kTPI tiles per iteration, the next kTPI prefetched into registers
-  uint2 nxt[kTPI][2];
+  // kTPI tiles per iteration, the next kTPI prefetched into registers; lane
+  // tig owns values d = 32 tig .. 32 tig + 31 of its rows: 8 B (2-bit) or
+  // 16 B (4-bit) of each 32 / 64-byte code row
+  constexpr int kRowB = BITS == 2 ? 32 : 64;
+  uint4 nxt[kTPI][2];
   auto load = [&](int t0) {
 #pragma unroll
     for (int u = 0; u < kTPI; ++u) {
       const int row0 = (t0 + u) * kTileRows + g4;
       const int row1 = row0 + 8;
-      nxt[u][0] = (t0 + u < t_end && row0 < rows)
-                      ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row0 * 32 + 8 * tig))
-                      : make_uint2(0, 0);
-      nxt[u][1] = (t0 + u < t_end && row1 < rows)
-                      ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row1 * 32 + 8 * tig))
-                      : make_uint2(0, 0);
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int row = rr ? row1 : row0;
+        const bool ok = t0 + u < t_end && row < rows;
+        if constexpr (BITS == 2) {
+          const uint2 v = ok ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row * kRowB + 8 * tig))
+                             : make_uint2(0, 0);
+          nxt[u][rr] = make_uint4(v.x, v.y, 0u, 0u);
+        } else {
+          nxt[u][rr] = ok ? __ldg(reinterpret_cast<const uint4*>(cbase + (size_t)row * kRowB + 16 * tig))
+                          : make_uint4(0, 0, 0, 0);
+        }
+      }
     }
   };
   load(t_begin);
   for (int t = t_begin; t < t_end; t += kTPI) {
-    uint2 cur[kTPI][2];
+    uint4 cur[kTPI][2];
 #pragma unroll
     for (int u = 0; u < kTPI; ++u) {
       cur[u][0] = nxt[u][0];
@@ -173,7 +199,7 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
     for (int u = 0; u < kTPI; ++u) {
       // three independent accumulator chains (hi.hi, hi.lo, lo.hi): mma latency
       float c[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
-      {
+      if constexpr (BITS == 2) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           const uint32_t w0 = half ? cur[u][0].y : cur[u][0].x;  // row g4, 4 bytes = 4 k-steps
@@ -191,16 +217,37 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
             const uint2 A23 = *reinterpret_cast<const uint2*>(lut_raw + oh);
             const uint2 L01 = *reinterpret_cast<const uint2*>(lut_raw + kLutBytes + ol);
             const uint2 L23 = *reinterpret_cast<const uint2*>(lut_raw + kLutBytes + oh);
-            const uint32_t a0 = A01.x, a1 = A01.y, a2 = A23.x, a3 = A23.y;
-            const uint32_t l0 = L01.x, l1 = L01.y, l2 = L23.x, l3 = L23.y;
-            mma_f16(c, a0, a1, a2, a3, bhi[ks][0], bhi[ks][1]);
-            mma_f16(c2, a0, a1, a2, a3, blo[ks][0], blo[ks][1]);
-            mma_f16(c3, l0, l1, l2, l3, bhi[ks][0], bhi[ks][1]);
+            mma_f16(c, A01.x, A01.y, A23.x, A23.y, bhi[ks][0], bhi[ks][1]);
+            mma_f16(c2, A01.x, A01.y, A23.x, A23.y, blo[ks][0], blo[ks][1]);
+            mma_f16(c3, L01.x, L01.y, L23.x, L23.y, bhi[ks][0], bhi[ks][1]);
           }
         }
+      } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) c[i] = (c[i] + c2[i]) + c3[i];
+        for (int ks = 0; ks < 8; ++ks) {
+          // k-step ks: code bytes 2 ks (a0 / a1) and 2 ks + 1 (a2 / a3) of the
+          // lane's 16 bytes, rows g4 / g4 + 8
+          const uint32_t wa = (&cur[u][0].x)[ks >> 1], wb = (&cur[u][1].x)[ks >> 1];
+          const int sh = 16 * (ks & 1);  // byte 2ks % 4 at bit sh, 2ks+1 at sh + 8
+          auto off = [&](uint32_t w, int s8) {
+            return ((s8 >= 7 ? (w >> (s8 - 7)) : (w << (7 - s8))) & 0x7F80u) | lane8;
+          };
+          const uint32_t o0 = off(wa, sh), o1 = off(wb, sh), o2 = off(wa, sh + 8), o3 = off(wb, sh + 8);
+          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(lut_raw + o0);
+          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(lut_raw + o1);
+          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(lut_raw + o2);
+          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(lut_raw + o3);
+          const uint32_t l0 = *reinterpret_cast<const uint32_t*>(lut_raw + kLutBytes + o0);
+          const uint32_t l1 = *reinterpret_cast<const uint32_t*>(lut_raw + kLutBytes + o1);
+          const uint32_t l2 = *reinterpret_cast<const uint32_t*>(lut_raw + kLutBytes + o2);
+          const uint32_t l3 = *reinterpret_cast<const uint32_t*>(lut_raw + kLutBytes + o3);
+          mma_f16(c, a0, a1, a2, a3, bhi[ks][0], bhi[ks][1]);
+          mma_f16(c2, a0, a1, a2, a3, blo[ks][0], blo[ks][1]);
+          mma_f16(c3, l0, l1, l2, l3, bhi[ks][0], bhi[ks][1]);
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = (c[i] + c2[i]) + c3[i];
       // s_k = c_gamma/32 * sum_a H8[k,a] P[a,k]: butterfly over g4 (lane bits 2..4)
       float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
 #pragma unroll
@@ -243,7 +290,8 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
 
 bool higgs_tc_supported(const kvb_store* s) {
   const kvb_higgs_dev& h = s->lm_h;
-  return s->d.landmark_kind == KVB_LM_HIGGS && h.d == 2 && h.n == 16 && h.group == 1024 &&
+  return s->d.landmark_kind == KVB_LM_HIGGS && h.d == 2 && (h.n == 16 || h.n == 256) &&
+         h.group == 1024 &&
          s->d.head_dim == kD && s->d.kv_heads <= 8;
 }
 
@@ -261,15 +309,21 @@ cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, flo
   const int rows = s->C;
   const int ntiles = (rows + kTileRows - 1) / kTileRows;
   const size_t smem = 2 * (size_t)kLutBytes;
-  ensure_smem((const void*)k1h_score<8>, smem);
-  const int slots = sm_count() * resident_ctas((const void*)k1h_score<8>, H * 32, smem);
+  const void* fn = hd.n == 16 ? (const void*)k1h_score<8, 2> : (const void*)k1h_score<8, 4>;
+  ensure_smem(fn, smem);
+  const int slots = sm_count() * resident_ctas(fn, H * 32, smem);
   int ctas = slots / B;
   if (ctas < 1) ctas = 1;
   if (ctas > ntiles) ctas = ntiles;
   const int per = (ntiles + ctas - 1) / ctas;
   // one warp per KV head (every warp valid: no divergent guards around the mma)
-  k1h_score<8><<<dim3((ntiles + per - 1) / per, B), H * 32, smem, st>>>(
-      hd.codes, hd.factor, W, hd.codebook, scores, rows, H, hd.groups, hd.group_bytes, per, hist);
+  const uint8_t* codes = hd.codes;
+  const float* fac = hd.factor;
+  const float* cbk = hd.codebook;
+  int rows_ = rows, Hh = H, ng = hd.groups, gb = hd.group_bytes;
+  void* args[] = {(void*)&codes, (void*)&fac, (void*)&W, (void*)&cbk, (void*)&scores, (void*)&rows_,
+                  (void*)&Hh, (void*)&ng, (void*)&gb, (void*)&per, (void*)&hist};
+  return cudaLaunchKernel(fn, dim3((ntiles + per - 1) / per, B), dim3(H * 32), args, smem, st);
   return cudaGetLastError();
 }
 

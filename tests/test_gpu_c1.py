@@ -168,9 +168,9 @@ def test_decode_step_matches_select_then_attend():
     assert float((o_step - o_ref).norm() / o_ref.norm()) < 1e-5
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_higgs2_tensor_core_scores(seed):
-    """HIGGS 2-bit landmarks at chunk 1 (the paper's proposed selection):
+@pytest.mark.parametrize("seed,bits,cs", [(0, 2, 1), (1, 2, 1), (0, 4, 2), (1, 4, 8)])
+def test_higgs2_tensor_core_scores(seed, bits, cs):
+    """HIGGS 2-bit landmarks at chunk 1 and 4-bit at chunks 2 / 8 (the paper's proposed selection):
     the rotated-domain tensor-core scan (fast path, used by decode) agrees
     with the bit-exact CUDA-core scan to fp32 accuracy, and selects the same
     chunks up to exact near-ties."""
@@ -182,8 +182,8 @@ def test_higgs2_tensor_core_scores(seed):
     k = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
     v = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
     q = torch.from_numpy(rng.standard_normal((B, H, G, D)).astype(np.float32)).cuda()
-    dev = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=1,
-                      dtype=torch.bfloat16, landmark=S.scheme_higgs(2), outlier_tokens=64,
+    dev = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=cs,
+                      dtype=torch.bfloat16, landmark=S.scheme_higgs(bits), outlier_tokens=64,
                       local_window=32)
     dev.build(k, v)
     K = dev.n_select(256 / n)
