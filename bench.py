@@ -384,7 +384,8 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
             # Appendix E: two-stage residual top-k (kvb_select_residual) then
             # the token-list attention (kvb_attend); k = budget tokens, mult 8
             for l in range(L_):
-                _, _, tok, ntok = stores[l].select_residual(q_dev[l], a.budget, 8, want_scores=False)
+                _, _, tok, ntok = stores[l].select_residual(q_dev[l], a.budget, 8, want_scores=False,
+                                                            exact=False)
                 out_dev[l].copy_(stores[l].attend(q_dev[l], tok, ntok)[0])
             return
         if mb == 1:
@@ -510,7 +511,7 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         k1_kernel = "k1h_score + k2_select (kvb_select, HIGGS tensor-core scan)"
     g_select = stage_graph(lambda: [pp[l].select_only(qb[l]) for l in range(L_)])
     if variant == "proposed_b":
-        g_select = stage_graph(lambda: [sp[l].select_residual(qb[l], a.budget, 8, want_scores=False)
+        g_select = stage_graph(lambda: [sp[l].select_residual(qb[l], a.budget, 8, want_scores=False, exact=False)
                                         for l in range(L_)])
     k1_ms = stage_ms(g_score)
     sel_ms = stage_ms(g_select)

@@ -214,6 +214,8 @@ typedef struct kvb_residual_args {
   int32_t k_tokens;
   int32_t n_candidates;     /* min(C, mult*ceil(k/cs))                       */
   int32_t token_capacity;
+  int32_t exact_scores;     /* 1: bit-reproducible stage-1 scoring; 0: fastest
+                               (HIGGS tensor-core scan + K2a/K2b candidates)  */
 } kvb_residual_args;
 kvb_status kvb_select_residual(kvb_store* store, const float* queries,
                                const kvb_residual_args* args, int32_t* chunk_ids,

@@ -45,7 +45,8 @@ class SelectArgs(C.Structure):
 
 class ResidualArgs(C.Structure):
     _fields_ = [("queries_per_head", C.c_int32), ("k_tokens", C.c_int32),
-                ("n_candidates", C.c_int32), ("token_capacity", C.c_int32)]
+                ("n_candidates", C.c_int32), ("token_capacity", C.c_int32),
+                ("exact_scores", C.c_int32)]
 
 
 class AttendArgs(C.Structure):

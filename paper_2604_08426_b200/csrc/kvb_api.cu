@@ -704,7 +704,8 @@ int64_t kvb_select_residual_workspace_bytes(const kvb_store* s, const kvb_residu
   const size_t B = s->d.batch, nc = a->n_candidates, cs = s->d.chunk_size;
   return (int64_t)(aligned(B * s->C * 4) + aligned(B * nc * 4) + aligned(B * nc * 4) +
                    aligned(B * nc * cs * 4) * 2 + aligned(B * 4) + aligned(B * a->k_tokens * 4) +
-                   aligned(B * 4) + 2048);
+                   aligned(B * 4) + aligned(higgs_tc_ws_bytes(s)) +
+                   aligned(select2_ws_bytes(s, (int)nc)) + 2048);
 }
 
 kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_args* a,
@@ -732,8 +733,9 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
   float* tok_s = cv.take<float>(B * nc * cs);
   int32_t* cand_count = cv.take<int32_t>(B);
   int32_t* sel_pos = cv.take<int32_t>(B * a->k_tokens);
+  void* tcws = cv.take<char>(higgs_tc_ws_bytes(s));
+  void* s2ws = cv.take<char>(select2_ws_bytes(s, (int)nc));
   // stage 1: chunk scores (selection.py:150) and candidate shortlist (:151-152)
-  if ((ks = score_landmarks(s, q, a->queries_per_head, KVB_AGG_SUM, chunk_s, st)) != KVB_OK) return ks;
   SelectLaunch L{};
   L.scores = chunk_s;
   L.M_stride = s->C;
@@ -743,7 +745,24 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
   L.sel_ids = chunk_ids;
   L.token_ids = nullptr;
   L.n_tokens = nullptr;
-  KVB_CUDA(launch_select(s, L, st), "candidate chunks");
+  if (!a->exact_scores && higgs_tc_supported(s)) {
+    // tensor-core scan + key histogram, whole-GPU split (K2a) + per-sequence
+    // finish with the rank-order sort (K2b); store-owned self-cleaning scratch
+    if (s->k2_dirty) {
+      KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * B * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * B * 4, st), "meta reset");
+    }
+    s->k2_dirty = true;
+    KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, chunk_s, tcws, s->k2_hist, st),
+             "HIGGS tensor-core scoring");
+    L.hist = s->k2_hist;
+    KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "candidate chunks");
+    s->k2_dirty = false;
+  } else {
+    if ((ks = score_landmarks(s, q, a->queries_per_head, KVB_AGG_SUM, chunk_s, st)) != KVB_OK)
+      return ks;
+    KVB_CUDA(launch_select(s, L, st), "candidate chunks");
+  }
   // stage 2: candidate tokens (:153), residual-refined scores (:155-158)
   KVB_CUDA(launch_candidate_tokens(s, chunk_ids, (int)nc, cand_tok, cand_count, cand_sorted, st),
            "candidate tokens");

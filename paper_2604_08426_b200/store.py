@@ -331,8 +331,9 @@ class DeviceStore:
         return chunk_ids, scores, tok, ntok
 
     def select_residual(self, q: torch.Tensor, k: int, candidate_multiplier: int = 4,
-                        want_scores: bool = True):
-        """approx_topk_residual (selection.py:132-171), batched."""
+                        want_scores: bool = True, exact: bool = True):
+        """approx_topk_residual (selection.py:132-171), batched. exact=False uses
+        the fastest stage-1 scan (HIGGS tensor cores, fp32-class scores)."""
         G = self._check_q(q)
         if candidate_multiplier < 1:
             raise ValueError("candidate_multiplier must be >= 1")
@@ -340,7 +341,7 @@ class DeviceStore:
             raise ValueError(f"k {k} out of range [1, {self.n}]")
         n_cand = min(self.C, candidate_multiplier * math.ceil(k / self.cs))
         cap = min(self.n, k + self.max_resident)
-        a = L.ResidualArgs(G, k, n_cand, cap)
+        a = L.ResidualArgs(G, k, n_cand, cap, 1 if exact else 0)
         cand = torch.empty((self.batch, n_cand), dtype=torch.int32, device="cuda")
         scores = torch.empty((self.batch, self.n), dtype=torch.float32, device="cuda") if want_scores else None
         tok = torch.empty((self.batch, cap), dtype=torch.int32, device="cuda")
