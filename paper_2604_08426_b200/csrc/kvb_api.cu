@@ -704,7 +704,7 @@ int64_t kvb_select_residual_workspace_bytes(const kvb_store* s, const kvb_residu
   const size_t B = s->d.batch, nc = a->n_candidates, cs = s->d.chunk_size;
   return (int64_t)(aligned(B * s->C * 4) + aligned(B * nc * 4) + aligned(B * nc * 4) +
                    aligned(B * nc * cs * 4) * 2 + aligned(B * 4) + aligned(B * a->k_tokens * 4) +
-                   aligned(B * 4) + aligned(higgs_tc_ws_bytes(s)) +
+                   aligned(B * 4) + 2 * aligned(higgs_tc_ws_bytes(s)) +
                    aligned(select2_ws_bytes(s, (int)nc)) + 2048);
 }
 
@@ -735,6 +735,7 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
   int32_t* sel_pos = cv.take<int32_t>(B * a->k_tokens);
   void* tcws = cv.take<char>(higgs_tc_ws_bytes(s));
   void* s2ws = cv.take<char>(select2_ws_bytes(s, (int)nc));
+  void* rtws = cv.take<char>(higgs_tc_ws_bytes(s));
   // stage 1: chunk scores (selection.py:150) and candidate shortlist (:151-152)
   SelectLaunch L{};
   L.scores = chunk_s;
@@ -766,8 +767,14 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
   // stage 2: candidate tokens (:153), residual-refined scores (:155-158)
   KVB_CUDA(launch_candidate_tokens(s, chunk_ids, (int)nc, cand_tok, cand_count, cand_sorted, st),
            "candidate tokens");
-  KVB_CUDA(launch_residual_scores(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc, tok_s, st),
-           "residual scores");
+  if (!a->exact_scores && resid_tc_supported(s))
+    KVB_CUDA(launch_residual_scores_tc(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc,
+                                       tok_s, rtws, st),
+             "residual scores (tensor cores)");
+  else
+    KVB_CUDA(launch_residual_scores(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc, tok_s,
+                                    st),
+             "residual scores");
   // token top-k inside the candidates (:160-161) and union with residents (:162)
   SelectLaunch T{};
   T.scores = tok_s;

@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int row = rr ? row1 : row0;
-        const bool ok = t0 + u < t_end && row < rows;
+        // whole groups: a partial last group's padding rows still carry codes
+        // (quantization.py:434-437) and enter every row's H_8 combine
+        const bool ok = t0 + u < t_end && row < ngroups * kR;
         if constexpr (BITS == 2) {
           const uint2 v = ok ? __ldg(reinterpret_cast<const uint2*>(cbase + (size_t)row * kRowB + 8 * tig))
                              : make_uint2(0, 0);
@@ -286,6 +288,137 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_score(
   }
 }
 
+
+// Appendix-E stage 2 on tensor cores (selection.py:155-158): residual scores
+// of every token of the candidate chunks, gathered through the ascending
+// candidate list. Residual codec: d = 2, n = 4 (1 bit per value, 2-bit code
+// per pair), group 1024 = one chunk of cs = 8 tokens, so a 16-row tile is two
+// candidate chunks and its rows are tok_s[b][16 t .. 16 t + 15] (the padded
+// layout of k_residual_scores). Same rotated-domain GEMM as k1h_score with W
+// built from the residual signs; single-code LUT of 4 entries x 32 lane
+// copies. Output: chunk score + sum over heads (head order).
+template <int HMAX>
+__global__ void __launch_bounds__(HMAX * 32) k1h_resid(
+    const uint8_t* __restrict__ codes, const float* __restrict__ factors,
+    const float* __restrict__ W, const float* __restrict__ cb, const float* __restrict__ chunk_s,
+    const int32_t* __restrict__ cand, int nc, int C, int n, float* __restrict__ tok_s, int H,
+    int ngroups, int gbytes, int tiles_per_cta) {
+  constexpr int kTPI = 8;
+  __shared__ uint32_t lut[2][4 * 32];
+  __shared__ float part[HMAX][kTPI * kTileRows];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g4 = lane >> 2, tig = lane & 3;
+  const int b = blockIdx.y, h = warp;
+  for (int i = threadIdx.x; i < 4 * 32; i += blockDim.x) {
+    const int e = i >> 5;
+    const __half2 hx = __floats2half2_rn(cb[2 * e], cb[2 * e + 1]);
+    const float2 fx = __half22float2(hx);
+    lut[0][i] = h2u(hx);
+    lut[1][i] = h2u(__floats2half2_rn(cb[2 * e] - fx.x, cb[2 * e + 1] - fx.y));
+  }
+  uint32_t bhi[8][2], blo[8][2];
+  {
+    const float* w = W + (((size_t)b * H + h) * kR + g4) * kD + 32 * tig;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const float4 v = *reinterpret_cast<const float4*>(w + 4 * ks);
+      const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      bhi[ks][0] = h2u(h01);
+      bhi[ks][1] = h2u(h23);
+      blo[ks][0] = h2u(__floats2half2_rn(v.x - f01.x, v.y - f01.y));
+      blo[ks][1] = h2u(__floats2half2_rn(v.z - f23.x, v.w - f23.y));
+    }
+  }
+  __syncthreads();
+  const unsigned char* lraw = reinterpret_cast<const unsigned char*>(&lut[0][0]);
+  const uint32_t lane4 = (uint32_t)lane * 4u;
+  const int ntiles = (nc + 1) >> 1;
+  const int t_begin = blockIdx.x * tiles_per_cta;
+  const int t_end = min(ntiles, t_begin + tiles_per_cta);
+  const int32_t* cl = cand + (size_t)b * nc;
+  const uint8_t* cbase = codes + ((size_t)b * H + h) * (size_t)ngroups * gbytes;
+  const float* fbase = factors + ((size_t)b * H + h) * ngroups;
+  const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
+  const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
+  for (int t = t_begin; t < t_end; t += kTPI) {
+    // lane tig owns codes 16 tig .. 16 tig + 15 (4 bytes) of rows g4 of both
+    // chunks of each tile
+    int gid[kTPI][2];
+    uint32_t wv[kTPI][2];
+#pragma unroll
+    for (int u = 0; u < kTPI; ++u)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int p = 2 * (t + u) + rr;
+        gid[u][rr] = (t + u < t_end && p < nc) ? __ldg(cl + p) : -1;
+      }
+#pragma unroll
+    for (int u = 0; u < kTPI; ++u)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+        wv[u][rr] = gid[u][rr] >= 0
+                        ? __ldg(reinterpret_cast<const uint32_t*>(cbase + (size_t)gid[u][rr] * gbytes +
+                                                                  g4 * 16 + 4 * tig))
+                        : 0u;
+#pragma unroll
+    for (int u = 0; u < kTPI; ++u) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        // k-step ks: codes 2 ks (a0 / a1) and 2 ks + 1 (a2 / a3), rows g4 / g4 + 8
+        auto off = [&](uint32_t w, int s) {
+          return ((s >= 7 ? (w >> (s - 7)) : (w << (7 - s))) & 0x180u) | lane4;
+        };
+        const int s0 = 4 * ks, s1 = 4 * ks + 2;
+        const uint32_t o0 = off(wv[u][0], s0), o1 = off(wv[u][1], s0);
+        const uint32_t o2 = off(wv[u][0], s1), o3 = off(wv[u][1], s1);
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(lraw + o0);
+        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(lraw + o1);
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(lraw + o2);
+        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(lraw + o3);
+        const uint32_t l0 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o0);
+        const uint32_t l1 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o1);
+        const uint32_t l2 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o2);
+        const uint32_t l3 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o3);
+        mma_f16(c, a0, a1, a2, a3, bhi[ks][0], bhi[ks][1]);
+        mma_f16(c2, a0, a1, a2, a3, blo[ks][0], blo[ks][1]);
+        mma_f16(c3, l0, l1, l2, l3, bhi[ks][0], bhi[ks][1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = (c[i] + c2[i]) + c3[i];
+      float v[4] = {c[0] * sg0, c[1] * sg1, c[2] * sg0, c[3] * sg1};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] += __shfl_xor_sync(FULL, v[i], 4);
+        v[i] += __shfl_xor_sync(FULL, v[i], 8);
+        v[i] += __shfl_xor_sync(FULL, v[i], 16);
+      }
+      if (g4 == 0) {
+        const float f0 = gid[u][0] >= 0 ? __ldg(fbase + gid[u][0]) * (1.0f / 32.0f) : 0.f;
+        const float f1 = gid[u][1] >= 0 ? __ldg(fbase + gid[u][1]) * (1.0f / 32.0f) : 0.f;
+        float* pr = part[h] + u * kTileRows;
+        pr[2 * tig] = v[0] * f0;
+        pr[2 * tig + 1] = v[1] * f0;
+        pr[8 + 2 * tig] = v[2] * f1;
+        pr[8 + 2 * tig + 1] = v[3] * f1;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTPI * kTileRows; i += blockDim.x) {
+      const int p = 2 * t + (i >> 3);  // candidate position
+      if (t + (i >> 4) < t_end && p < nc) {
+        const int c = __ldg(cl + p), k = i & 7;
+        if (c * kR + k < n) {
+          float r = part[0][i];
+          for (int hh = 1; hh < H; ++hh) r = r + part[hh][i];
+          tok_s[(size_t)b * nc * kR + (size_t)p * kR + k] = __ldg(chunk_s + (size_t)b * C + c) + r;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
 }  // namespace
 
 bool higgs_tc_supported(const kvb_store* s) {
@@ -325,6 +458,37 @@ cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, flo
                   (void*)&Hh, (void*)&ng, (void*)&gb, (void*)&per, (void*)&hist};
   return cudaLaunchKernel(fn, dim3((ntiles + per - 1) / per, B), dim3(H * 32), args, smem, st);
   return cudaGetLastError();
+}
+
+bool resid_tc_supported(const kvb_store* s) {
+  const kvb_higgs_dev& h = s->res_h;
+  return s->d.has_residual && h.d == 2 && h.n == 4 && h.group == 1024 && s->d.head_dim == kD &&
+         s->d.kv_heads <= 8 && s->d.chunk_size == kR;
+}
+
+cudaError_t launch_residual_scores_tc(const kvb_store* s, const float* q, int G,
+                                      const float* chunk_s, const int32_t* cand_sorted, int nc,
+                                      float* tok_s, void* ws, cudaStream_t st) {
+  const kvb_higgs_dev& hd = s->res_h;
+  const int B = s->d.batch, H = s->d.kv_heads;
+  float* W = static_cast<float*>(ws);
+  count_launch(2);
+  k1h_prep<<<dim3(H, B), kR * 32, 0, st>>>(q, hd.signs, W, H, G);
+  const int ntiles = (nc + 1) / 2;
+  const void* fn = (const void*)k1h_resid<8>;
+  const int slots = sm_count() * resident_ctas(fn, H * 32, 0);
+  int ctas = slots / B;
+  if (ctas < 1) ctas = 1;
+  if (ctas > ntiles) ctas = ntiles;
+  const int per = (ntiles + ctas - 1) / ctas;
+  const uint8_t* codes = hd.codes;
+  const float* fac = hd.factor;
+  const float* cbk = hd.codebook;
+  int C = s->C, n = s->d.n_tokens, Hh = H, ng = hd.groups, gb = hd.group_bytes;
+  void* args[] = {(void*)&codes, (void*)&fac, (void*)&W, (void*)&cbk, (void*)&chunk_s,
+                  (void*)&cand_sorted, (void*)&nc, (void*)&C, (void*)&n, (void*)&tok_s,
+                  (void*)&Hh, (void*)&ng, (void*)&gb, (void*)&per};
+  return cudaLaunchKernel(fn, dim3((ntiles + per - 1) / per, B), dim3(H * 32), args, 0, st);
 }
 
 }  // namespace kvb

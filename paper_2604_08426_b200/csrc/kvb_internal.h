@@ -85,6 +85,10 @@ cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int ag
                                float* scores, cudaStream_t st);
 bool higgs_tc_supported(const kvb_store* s);
 size_t higgs_tc_ws_bytes(const kvb_store* s);
+bool resid_tc_supported(const kvb_store* s);
+cudaError_t launch_residual_scores_tc(const kvb_store* s, const float* q, int G,
+                                      const float* chunk_s, const int32_t* cand_sorted, int nc,
+                                      float* tok_s, void* ws, cudaStream_t st);
 cudaError_t launch_score_higgs_tc(const kvb_store* s, const float* q, int G, float* scores,
                                   void* ws, uint32_t* hist, cudaStream_t st);
 // Top-K + token union. mode 0: items are chunks (M = C); mode 1: items are

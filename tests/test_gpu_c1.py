@@ -168,8 +168,9 @@ def test_decode_step_matches_select_then_attend():
     assert float((o_step - o_ref).norm() / o_ref.norm()) < 1e-5
 
 
-@pytest.mark.parametrize("seed,bits,cs", [(0, 2, 1), (1, 2, 1), (0, 4, 2), (1, 4, 8)])
-def test_higgs2_tensor_core_scores(seed, bits, cs):
+@pytest.mark.parametrize("seed,bits,cs,n", [(0, 2, 1, 16384), (1, 2, 1, 16384), (0, 4, 2, 16384),
+                                          (1, 4, 8, 16384), (2, 4, 8, 8195), (3, 2, 1, 16381)])
+def test_higgs2_tensor_core_scores(seed, bits, cs, n):
     """HIGGS 2-bit landmarks at chunk 1 and 4-bit at chunks 2 / 8 (the paper's proposed selection):
     the rotated-domain tensor-core scan (fast path, used by decode) agrees
     with the bit-exact CUDA-core scan to fp32 accuracy, and selects the same
@@ -177,7 +178,9 @@ def test_higgs2_tensor_core_scores(seed, bits, cs):
     from paper_2604_08426_b200 import schemes as S
     from paper_2604_08426_b200.store import DeviceStore
 
-    B, n = 2, 16384
+    # ragged n: a partial last landmark group (its padding rows' codes enter
+    # every row's H_8 combine)
+    B = 2
     rng = np.random.default_rng(100 + seed)
     k = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
     v = torch.from_numpy(rng.standard_normal((B, n, H, D)).astype(np.float32)).cuda().bfloat16()
