@@ -699,6 +699,17 @@ kvb_status kvb_select(kvb_store* s, const float* q, const kvb_select_args* a, in
                      as_stream(stream), false, nullptr);
 }
 
+// Store-owned side stream + fork/join events (created on first use).
+static cudaError_t ensure_side(kvb_store* s) {
+  if (s->side) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  cudaEvent_t* evs[] = {&s->ev_fork, &s->ev_join, &s->ev_sel, &s->ev_union};
+  for (cudaEvent_t* ev : evs)
+    if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
 int64_t kvb_select_residual_workspace_bytes(const kvb_store* s, const kvb_residual_args* a) {
   if (!s || !a) return -1;
   const size_t B = s->d.batch, nc = a->n_candidates, cs = s->d.chunk_size;
@@ -746,6 +757,7 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
   L.sel_ids = chunk_ids;
   L.token_ids = nullptr;
   L.n_tokens = nullptr;
+  bool joined = false;
   if (!a->exact_scores && higgs_tc_supported(s)) {
     // tensor-core scan + key histogram, whole-GPU split (K2a) + per-sequence
     // finish with the rank-order sort (K2b); store-owned self-cleaning scratch
@@ -757,7 +769,26 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     KVB_CUDA(launch_score_higgs_tc(s, q, a->queries_per_head, chunk_s, tcws, s->k2_hist, st),
              "HIGGS tensor-core scoring");
     L.hist = s->k2_hist;
-    KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "candidate chunks");
+    size_t pw = 1;
+    while (pw < nc) pw <<= 1;
+    if (pw * 8 <= 227 * 1024) {
+      // the candidate SET in ascending order feeds stage 2 directly; kvlab's
+      // rank order of chunk_ids (a result, not an input of stage 2) is sorted
+      // on the side stream, overlapping stage 2
+      L.rank_order = 0;
+      L.sorted_ids = 1;
+      L.sel_ids = cand_sorted;
+      KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "candidate chunks");
+      KVB_CUDA(ensure_side(s), "side stream");
+      KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
+      KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
+      KVB_CUDA(launch_merge_topk(chunk_s, cand_sorted, 1, (int)B, (int)nc, chunk_ids, s->side, s->C),
+               "candidate rank order");
+      KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
+      joined = true;
+    } else {
+      KVB_CUDA(launch_select2(s, L, s2ws, st, nullptr), "candidate chunks");
+    }
     s->k2_dirty = false;
   } else {
     if ((ks = score_landmarks(s, q, a->queries_per_head, KVB_AGG_SUM, chunk_s, st)) != KVB_OK)
@@ -765,7 +796,8 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     KVB_CUDA(launch_select(s, L, st), "candidate chunks");
   }
   // stage 2: candidate tokens (:153), residual-refined scores (:155-158)
-  KVB_CUDA(launch_candidate_tokens(s, chunk_ids, (int)nc, cand_tok, cand_count, cand_sorted, st),
+  KVB_CUDA(launch_candidate_tokens(s, joined ? cand_sorted : chunk_ids, (int)nc, cand_tok, cand_count,
+                                   cand_sorted, st),
            "candidate tokens");
   if (!a->exact_scores && resid_tc_supported(s))
     KVB_CUDA(launch_residual_scores_tc(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc,
@@ -794,6 +826,7 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     KVB_CUDA(launch_residual_full_scores(s, chunk_s, cand_tok, cand_count, (int)(nc * cs), tok_s,
                                          scores, st),
              "full scores");
+  if (joined) KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
   return KVB_OK;
 }
 
@@ -872,13 +905,7 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   // selected chunks) and also writes the sorted token union the API returns.
   // Capturable into CUDA graphs.
   cudaStream_t st = as_stream(stream);
-  if (!s->side) {
-    KVB_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "side stream");
-    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming), "fork event");
-    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming), "join event");
-    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_sel, cudaEventDisableTiming), "select event");
-    KVB_CUDA(cudaEventCreateWithFlags(&s->ev_union, cudaEventDisableTiming), "union event");
-  }
+  KVB_CUDA(ensure_side(s), "side stream");
   AttendLaunch L{};
   L.q = q;
   L.G = att->queries_per_head;

@@ -303,12 +303,24 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
     const float* __restrict__ W, const float* __restrict__ cb, const float* __restrict__ chunk_s,
     const int32_t* __restrict__ cand, int nc, int C, int n, float* __restrict__ tok_s, int H,
     int ngroups, int gbytes, int tiles_per_cta) {
-  constexpr int kTPI = 8;
+  constexpr int kTPI = 4;
   __shared__ uint32_t lut[2][4 * 32];
-  __shared__ float part[HMAX][kTPI * kTileRows];
+  __shared__ float part[2][HMAX][kTPI * kTileRows];  // double-buffered: one barrier per iteration
+  extern __shared__ int32_t s_cand[];               // [2 per] candidate ids, then [2 per] base scores
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g4 = lane >> 2, tig = lane & 3;
   const int b = blockIdx.y, h = warp;
+  const int ntiles = (nc + 1) >> 1;
+  const int t_begin = blockIdx.x * tiles_per_cta;
+  const int t_end = min(ntiles, t_begin + tiles_per_cta);
+  const int p_begin = 2 * t_begin, np_ = min(nc, 2 * t_end) - p_begin;
+  float* s_base = reinterpret_cast<float*>(s_cand + 2 * tiles_per_cta);
+  // the CTA's candidate range and their chunk scores, staged once
+  for (int i = threadIdx.x; i < np_; i += blockDim.x) {
+    const int c = __ldg(cand + (size_t)b * nc + p_begin + i);
+    s_cand[i] = c;
+    s_base[i] = __ldg(chunk_s + (size_t)b * C + c);
+  }
   for (int i = threadIdx.x; i < 4 * 32; i += blockDim.x) {
     const int e = i >> 5;
     const __half2 hx = __floats2half2_rn(cb[2 * e], cb[2 * e + 1]);
@@ -333,34 +345,39 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
   __syncthreads();
   const unsigned char* lraw = reinterpret_cast<const unsigned char*>(&lut[0][0]);
   const uint32_t lane4 = (uint32_t)lane * 4u;
-  const int ntiles = (nc + 1) >> 1;
-  const int t_begin = blockIdx.x * tiles_per_cta;
-  const int t_end = min(ntiles, t_begin + tiles_per_cta);
-  const int32_t* cl = cand + (size_t)b * nc;
-  const uint8_t* cbase = codes + ((size_t)b * H + h) * (size_t)ngroups * gbytes;
+  const uint8_t* cbase = codes + ((size_t)b * H + h) * (size_t)ngroups * gbytes + g4 * 16 + 4 * tig;
   const float* fbase = factors + ((size_t)b * H + h) * ngroups;
   const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
   const float sg1 = (__popc((2 * tig + 1) & g4) & 1) ? -1.f : 1.f;
-  for (int t = t_begin; t < t_end; t += kTPI) {
-    // lane tig owns codes 16 tig .. 16 tig + 15 (4 bytes) of rows g4 of both
-    // chunks of each tile
-    int gid[kTPI][2];
-    uint32_t wv[kTPI][2];
+  // lane tig owns codes 16 tig .. 16 tig + 15 (4 bytes) of row g4 of both
+  // chunks of each tile; the next kTPI tiles' words (+ factors) are prefetched
+  uint32_t nw[kTPI][2];
+  float nf[kTPI][2];
+  auto load = [&](int t0) {
 #pragma unroll
     for (int u = 0; u < kTPI; ++u)
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
-        const int p = 2 * (t + u) + rr;
-        gid[u][rr] = (t + u < t_end && p < nc) ? __ldg(cl + p) : -1;
+        const int i = 2 * (t0 + u - t_begin) + rr;
+        const bool ok = i < np_;
+        const int g = ok ? s_cand[i] : 0;
+        nw[u][rr] = ok ? __ldg(reinterpret_cast<const uint32_t*>(cbase + (size_t)g * gbytes)) : 0u;
+        nf[u][rr] = ok ? __ldg(fbase + g) * (1.0f / 32.0f) : 0.f;
       }
+  };
+  load(t_begin);
+  int buf = 0;
+  for (int t = t_begin; t < t_end; t += kTPI, buf ^= 1) {
+    uint32_t wv[kTPI][2];
+    float fv[kTPI][2];
 #pragma unroll
     for (int u = 0; u < kTPI; ++u)
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-        wv[u][rr] = gid[u][rr] >= 0
-                        ? __ldg(reinterpret_cast<const uint32_t*>(cbase + (size_t)gid[u][rr] * gbytes +
-                                                                  g4 * 16 + 4 * tig))
-                        : 0u;
+      for (int rr = 0; rr < 2; ++rr) {
+        wv[u][rr] = nw[u][rr];
+        fv[u][rr] = nf[u][rr];
+      }
+    load(t + kTPI);
 #pragma unroll
     for (int u = 0; u < kTPI; ++u) {
       float c[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
@@ -395,30 +412,28 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
         v[i] += __shfl_xor_sync(FULL, v[i], 16);
       }
       if (g4 == 0) {
-        const float f0 = gid[u][0] >= 0 ? __ldg(fbase + gid[u][0]) * (1.0f / 32.0f) : 0.f;
-        const float f1 = gid[u][1] >= 0 ? __ldg(fbase + gid[u][1]) * (1.0f / 32.0f) : 0.f;
-        float* pr = part[h] + u * kTileRows;
-        pr[2 * tig] = v[0] * f0;
-        pr[2 * tig + 1] = v[1] * f0;
-        pr[8 + 2 * tig] = v[2] * f1;
-        pr[8 + 2 * tig + 1] = v[3] * f1;
+        float* pr = part[buf][h] + u * kTileRows;
+        pr[2 * tig] = v[0] * fv[u][0];
+        pr[2 * tig + 1] = v[1] * fv[u][0];
+        pr[8 + 2 * tig] = v[2] * fv[u][1];
+        pr[8 + 2 * tig + 1] = v[3] * fv[u][1];
       }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kTPI * kTileRows; i += blockDim.x) {
-      const int p = 2 * t + (i >> 3);  // candidate position
-      if (t + (i >> 4) < t_end && p < nc) {
-        const int c = __ldg(cl + p), k = i & 7;
+      const int j = 2 * (t - t_begin) + (i >> 3);  // candidate index within the CTA
+      if (j < np_) {
+        const int c = s_cand[j], k = i & 7;
         if (c * kR + k < n) {
-          float r = part[0][i];
-          for (int hh = 1; hh < H; ++hh) r = r + part[hh][i];
-          tok_s[(size_t)b * nc * kR + (size_t)p * kR + k] = __ldg(chunk_s + (size_t)b * C + c) + r;
+          float r = part[buf][0][i];
+          for (int hh = 1; hh < H; ++hh) r = r + part[buf][hh][i];
+          tok_s[(size_t)b * nc * kR + (size_t)(p_begin + j) * kR + k] = s_base[j] + r;
         }
       }
     }
-    __syncthreads();
   }
 }
+
 }  // namespace
 
 bool higgs_tc_supported(const kvb_store* s) {
@@ -476,11 +491,12 @@ cudaError_t launch_residual_scores_tc(const kvb_store* s, const float* q, int G,
   k1h_prep<<<dim3(H, B), kR * 32, 0, st>>>(q, hd.signs, W, H, G);
   const int ntiles = (nc + 1) / 2;
   const void* fn = (const void*)k1h_resid<8>;
-  const int slots = sm_count() * resident_ctas(fn, H * 32, 0);
-  int ctas = slots / B;
+  int ctas = sm_count() * resident_ctas(fn, H * 32, 4096) / B;
   if (ctas < 1) ctas = 1;
   if (ctas > ntiles) ctas = ntiles;
-  const int per = (ntiles + ctas - 1) / ctas;
+  int per = (ntiles + ctas - 1) / ctas;
+  if (per > 1024) per = 1024;  // staged candidate range <= 16 KB
+  const size_t smem = (size_t)per * 2 * 8;
   const uint8_t* codes = hd.codes;
   const float* fac = hd.factor;
   const float* cbk = hd.codebook;
@@ -488,7 +504,7 @@ cudaError_t launch_residual_scores_tc(const kvb_store* s, const float* q, int G,
   void* args[] = {(void*)&codes, (void*)&fac, (void*)&W, (void*)&cbk, (void*)&chunk_s,
                   (void*)&cand_sorted, (void*)&nc, (void*)&C, (void*)&n, (void*)&tok_s,
                   (void*)&Hh, (void*)&ng, (void*)&gb, (void*)&per};
-  return cudaLaunchKernel(fn, dim3((ntiles + per - 1) / per, B), dim3(H * 32), args, 0, st);
+  return cudaLaunchKernel(fn, dim3((ntiles + per - 1) / per, B), dim3(H * 32), args, smem, st);
 }
 
 }  // namespace kvb

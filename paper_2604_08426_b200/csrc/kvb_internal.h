@@ -202,7 +202,7 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
                                    int D, float* out, float* lse, cudaStream_t st);
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
-                              int32_t* out, cudaStream_t st);
+                              int32_t* out, cudaStream_t st, int by_id_M = 0);
 
 // K3 reconstruction on tcgen05 (kvb_recon.cu): logits [B][K*cs][H*G] of the
 // selected SVD tokens, consumed by the bulk attention (svd_logits mode)

@@ -989,7 +989,7 @@ cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chun
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024)
 k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int parts, int batch,
-             int k, int P, int32_t* __restrict__ out) {
+             int k, int P, int32_t* __restrict__ out, int by_id_M) {
   extern __shared__ uint64_t mk[];
   const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
   const int tot = parts * k;
@@ -999,7 +999,11 @@ k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int 
       const int pp = i / k, j = i - pp * k;
       const size_t off = ((size_t)pp * batch + b) * k + j;
       const int id = gid[off];
-      if (id >= 0) v = ((uint64_t)score_key(sc[off]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)id);
+      // scores listed beside the ids, or (by_id_M > 0) indexed by id in [B][M]
+      if (id >= 0) {
+        const float x = by_id_M > 0 ? sc[(size_t)b * by_id_M + id] : sc[off];
+        v = ((uint64_t)score_key(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)id);
+      }
     }
     mk[i] = v;
   }
@@ -1023,13 +1027,13 @@ k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int 
 }
 
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
-                              int32_t* out, cudaStream_t st) {
+                              int32_t* out, cudaStream_t st, int by_id_M) {
   const int P = next_pow2(parts * k);
   const size_t smem = (size_t)P * 8;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   ensure_smem((const void*)k_merge_topk, smem);
   count_launch();
-  k_merge_topk<<<batch, 1024, smem, st>>>(sc, ids, parts, batch, k, P, out);
+  k_merge_topk<<<batch, 1024, smem, st>>>(sc, ids, parts, batch, k, P, out, by_id_M);
   return cudaGetLastError();
 }
 
