@@ -66,6 +66,9 @@ def parse():
                     help="comma-separated secondary variants reported under 'variants'")
     ap.add_argument("--microbatches", type=int, default=1,
                     help="split the batch into this many stores per layer, each decode chain on its own stream")
+    ap.add_argument("--overlap-sms", type=int, default=0,
+                    help="with --microbatches > 1: attention on per-micro-batch high-priority streams, "
+                         "grid sized for this many SMs (kvb_store_set_overlap)")
     ap.add_argument("--mb-offset", type=int, default=0,
                     help="micro-batch m starts after micro-batch m-1 finished this many layers")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -378,6 +381,13 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     mb = a.microbatches
     Bm = B // mb
     mstreams = [torch.cuda.Stream() for _ in range(mb)] if mb > 1 else []
+    if mb > 1 and a.overlap_sms:
+        # two-batch overlap: each micro-batch's attention on its own
+        # high-priority stream, sized for overlap_sms SMs
+        astreams = [torch.cuda.Stream(priority=-1) for _ in range(mb)]
+        for l in range(L_):
+            for m in range(mb):
+                stores[l * mb + m].set_overlap(astreams[m], a.overlap_sms)
 
     def step():
         if variant == "proposed_b":

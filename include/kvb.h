@@ -157,6 +157,14 @@ kvb_status kvb_store_set_offload(kvb_store* store, const void* keys, const void*
 /* SVD slow tier (quantization.py:490-513): device fp16 factors
  * left [batch][n_tokens][svd_groups][r], right [batch][svd_groups][r][Dg],
  * Dg = kv_heads*head_dim/svd_groups.                                        */
+/* Two-batch overlap (serving extension, no kvlab counterpart): when
+ * attention_stream is non-NULL, kvb_decode_step runs the attention + merge of
+ * the fused path on that stream (ordered after the scan by events; the
+ * caller's stream waits for it), and the attention grid is sized for
+ * attention_sms SMs (0 = all). Two micro-batches on two caller streams then
+ * overlap one's latency-bound attention with the other's HBM-bound scan.
+ * The streams are the caller's and must outlive the store's use of them. */
+kvb_status kvb_store_set_overlap(kvb_store* store, void* attention_stream, int32_t attention_sms);
 kvb_status kvb_store_set_svd(kvb_store* store, const void* left16, const void* right16,
                              void* stream);
 /* Import precomputed landmark state (identical codes for parity runs).

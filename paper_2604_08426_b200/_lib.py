@@ -76,6 +76,7 @@ SIGNATURES = [
     ("kvb_store_set_residency", _I32, [_P, _P, _P, _P, _P, _P]),
     ("kvb_store_set_offload", _I32, [_P, _P, _P, _P]),
     ("kvb_store_set_svd", _I32, [_P, _P, _P, _P]),
+    ("kvb_store_set_overlap", _I32, [_P, _P, _I32]),
     ("kvb_store_set_landmarks_dense", _I32, [_P, _P, _P]),
     ("kvb_store_set_landmarks_higgs", _I32, [_P, _P, _P, _P]),
     ("kvb_store_set_residuals_higgs", _I32, [_P, _P, _P, _P]),

@@ -71,6 +71,8 @@ int64_t trace_read(uint64_t* host, int64_t max_words) {
   return n;
 }
 
+bool pdl_enabled();
+
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        void** args) {
   cudaLaunchConfig_t cfg{};
@@ -82,8 +84,19 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+// PDL on by default; KVB_PDL=0 launches every chained kernel fully
+// serialised (experiments: PDL-resident waiting CTAs hold their SMs)
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KVB_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int sm_count() {
@@ -534,6 +547,17 @@ kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* val
   return KVB_OK;
 }
 
+kvb_status kvb_store_set_overlap(kvb_store* s, void* attention_stream, int32_t attention_sms) {
+  if (!s) KVB_FAIL(KVB_EINVAL, "null store");
+  if (attention_sms < 0) KVB_FAIL(KVB_EINVAL, "attention_sms must be >= 0");
+  if (attention_sms > 0 && attention_sms < s->d.batch)
+    KVB_FAIL(KVB_EINVAL, "attention_sms must be 0 or >= batch");
+  if (attention_sms > sm_count()) KVB_FAIL(KVB_EINVAL, "attention_sms exceeds the device's SM count");
+  s->att_stream = static_cast<cudaStream_t>(attention_stream);
+  s->att_sms = attention_sms;
+  return KVB_OK;
+}
+
 kvb_status kvb_store_set_svd(kvb_store* s, const void* left16, const void* right16, void* stream) {
   if (!s || !left16 || !right16) KVB_FAIL(KVB_EINVAL, "null argument");
   if (s->d.slow_kind != KVB_SLOW_SVD) KVB_FAIL(KVB_EINVAL, "store slow tier is not svd");
@@ -944,8 +968,20 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
       KVB_CUDA(launch_score_higgs_tc(s, q, L.G, sc, tcws, s->k2_hist, st), "HIGGS tensor-core scoring");
     else
       KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st), "landmark scoring");
-    KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
-    KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
+    if (s->att_stream) {
+      // two-batch overlap: attention on the (high-priority) attention stream,
+      // event-ordered after the scan; the caller's stream resumes after it
+      KVB_CUDA(cudaEventRecord(s->ev_sel, st), "scan done");
+      KVB_CUDA(cudaStreamWaitEvent(s->att_stream, s->ev_sel, 0), "scan wait");
+      KVB_CUDA(cudaStreamWaitEvent(s->att_stream, s->ev_join, 0), "join wait");
+      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, s->att_stream, sc, s->k2_hist, chunk_ids),
+               "sparse attention");
+      KVB_CUDA(cudaEventRecord(s->ev_union, s->att_stream), "attention done");
+      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_union, 0), "attention wait");
+    } else {
+      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
+    }
     s->k2_dirty = false;
     return KVB_OK;
   }

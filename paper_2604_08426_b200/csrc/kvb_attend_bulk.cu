@@ -844,7 +844,7 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
   BulkGeom g{};
   const int B = s->d.batch, H = s->d.kv_heads;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
-  int splits = sm_count() / B;
+  int splits = (s->att_sms > 0 ? s->att_sms : sm_count()) / B;
   const int tiles = (positions_cap + kBT - 1) / kBT;
   if (splits > tiles) splits = tiles;
   if (splits < 1) splits = 1;
@@ -1006,7 +1006,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
                             (const float*)p.po, g.splits, H * a.G, p.out, p.lse,
                             p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr);

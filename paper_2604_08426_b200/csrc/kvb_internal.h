@@ -55,6 +55,10 @@ struct kvb_store {
   bool off_host = false;
   // side stream + events for the fork/join of decode-step work (prep || scan)
   cudaStream_t side = nullptr;
+  // two-batch overlap (kvb_store_set_overlap): the decode step's attention +
+  // merge go to att_stream (event-ordered after the scan) on att_sms SMs
+  cudaStream_t att_stream = nullptr;
+  int att_sms = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sel = nullptr, ev_union = nullptr;
 };
 
@@ -130,6 +134,7 @@ cudaError_t launch_union_sorted(const kvb_store* s, const int32_t* chunk_ids, in
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while its predecessor drains; it must griddepcontrol.wait before reading
 // the predecessor's output.
+bool pdl_enabled();
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        void** args);
 

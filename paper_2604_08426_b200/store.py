@@ -371,6 +371,14 @@ class DeviceStore:
                                     _stream()), "kvb_attend")
         return out, lse
 
+    def set_overlap(self, attention_stream=None, attention_sms: int = 0):
+        """Two-batch overlap (kvb_store_set_overlap): decode-step attention on
+        `attention_stream` (a torch.cuda.Stream, None = the caller's stream),
+        its grid sized for `attention_sms` SMs (0 = all)."""
+        self._att_stream = attention_stream  # keep the stream alive
+        ptr = C.c_void_p(attention_stream.cuda_stream) if attention_stream is not None else None
+        L.check(self.lib.kvb_store_set_overlap(self.h, ptr, int(attention_sms)), "kvb_store_set_overlap")
+
     def decode_plan(self, G: int, n_select: int, k_path: int = 0):
         """Pre-sized arguments + buffers for repeated decode steps (graph-capturable)."""
         cap = self.token_capacity(n_select)
