@@ -91,7 +91,8 @@ struct BulkParams {
   int off_uni;
   int nst;                    // ring slots (stages)
   int ett;                    // tokens per exact-key tile (8 in SVD stores: compact slots)
-  int dbg;                    // profiling: 1 skip the math, 2 skip the copies
+  int dbg;                    // profiling: 1 skip the math, 2 skip the copies, 4 one scanning
+                              // split, 8 staging copy only (empty selection)
   // geometry
   int maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_bar, off_stage;
 };
@@ -300,14 +301,34 @@ __global__ void __maxnreg__(232) k5_attend_bulk(BulkParams p) {
     // used) ring, then ascending ids: each thread owns a run of words, one scan
     uint32_t* wb = reinterpret_cast<uint32_t*>(ring);
     uint32_t* sk = wb + ((p.Wc + 3) & ~3);
-    const int cap = (int)(((size_t)nst * p.stage_bytes - (size_t)((p.Wc + 3) & ~3) * 4) / 8);
+    const size_t ring_bytes = (size_t)nst * p.stage_bytes;
+    const size_t used = (size_t)((p.Wc + 3) & ~3) * 4;
+    const float* scs = p.sel_scores + (size_t)b * p.C;
+    // stage the sequence's scores in the ring's tail by bulk copies (overlaps
+    // the threshold search) when they fit beside >= 4096 candidate slots
+    const size_t sbytes = (size_t)p.C * 4;
+    const bool staged = (sbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(scs) & 15) == 0) &&
+                        used + sbytes + 4096 * 8 <= ring_bytes && !(p.dbg & 4);
+    __shared__ __align__(8) uint64_t stage_bar;
+    float* stage = staged ? reinterpret_cast<float*>(ring + ring_bytes - sbytes) : nullptr;
+    if (staged && tid == 0) {
+      mbar_init(&stage_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_arrive_tx(&stage_bar, (uint32_t)sbytes);
+      constexpr uint32_t kPiece = 32768;
+      for (size_t o = 0; o < sbytes; o += kPiece)
+        bulk_g2s(reinterpret_cast<unsigned char*>(stage) + o, reinterpret_cast<const unsigned char*>(scs) + o,
+                 (uint32_t)min((size_t)kPiece, sbytes - o), &stage_bar);
+    }
+    const int cap = (int)((ring_bytes - used - (staged ? sbytes : 0)) / 8);
     // (profiling: dbg & 4 -> only split 0 streams the scores, to isolate L2 contention)
-    select_topk_shared(p.sel_scores + (size_t)b * p.C, ((p.dbg & 4) && split) ? 0 : p.C,
+    select_topk_shared(scs, ((p.dbg & 4) && split) ? 0 : p.C,
                        p.sel_hist + (size_t)b * kFuseHistBins,
                        p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
                        p.trace ? p.trace + (size_t)gridDim.y * gridDim.x * 8 + 64 +
                                      ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8
-                               : nullptr);
+                               : nullptr,
+                       stage, staged ? &stage_bar : nullptr, p.dbg & 8);
     const int per = (p.Wc + nthr - 1) / nthr;
     const int w0 = min(p.Wc, tid * per), w1 = min(p.Wc, w0 + per);
     int cnt = 0;

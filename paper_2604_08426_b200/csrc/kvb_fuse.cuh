@@ -69,9 +69,22 @@ __device__ __forceinline__ void sel_stamp(uint64_t* tr, int k) {
   }
 }
 
+// stage / stage_bar (optional): the caller has issued bulk copies of sc[0, M)
+// into shared memory `stage` completing on mbarrier stage_bar (phase 0); the
+// score stream then reads shared memory with a compact loop -- the unrolled
+// global-load stream executes once per CTA and is instruction-fetch bound.
+__device__ __forceinline__ void fuse_mbar_wait0(uint64_t* b) {
+  asm volatile(
+      "{\n .reg .pred p;\n FW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra FW_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(b))
+      : "memory");
+}
+
 __device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
                                    uint32_t* sbm, uint32_t* sk, int32_t* si, int cap, int* red,
-                                   uint64_t* tr = nullptr) {
+                                   uint64_t* tr = nullptr, const float* stage = nullptr,
+                                   uint64_t* stage_bar = nullptr, int dbg_copy_only = 0) {
   __shared__ int s_tb, s_kb, s_nc, s_gt, s_eq;
   __shared__ uint32_t s_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
@@ -98,7 +111,42 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
       }
     }
   };
-  if ((M & 3) == 0 && ((reinterpret_cast<uintptr_t>(sc) & 15) == 0)) {
+  if (stage) {
+    fuse_mbar_wait0(stage_bar);
+    if (dbg_copy_only) {  // profiling: the staging copy alone (empty selection)
+      __syncthreads();
+      sel_stamp(tr, 1);
+      return;
+    }
+    // 4 scores per LDS.128 and 4 independent loads per iteration: at 8 warps
+    // per SM a serial per-score chain is latency-bound (~10 us at C2); keys at
+    // or above the threshold bin (~3% of them) take the rare branch
+    const float4* s4 = reinterpret_cast<const float4*>(stage);
+    const int M4 = M >> 2;  // staged => M % 4 == 0
+#pragma unroll 4
+    for (int j = tid; j < M4; j += nthr) {
+      const float4 v = s4[j];
+      const uint32_t k0 = score_key(v.x), k1 = score_key(v.y), k2 = score_key(v.z), k3 = score_key(v.w);
+      const uint32_t kmax = max(max(k0, k1), max(k2, k3));
+      if ((kmax >> 21) >= tb) {
+        const uint32_t kk[4] = {k0, k1, k2, k3};
+        uint32_t wm = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t bin = kk[e] >> 21;
+          if (bin > tb) wm |= 1u << e;
+          if (bin == tb) {
+            const int pos = atomicAdd(&s_nc, 1);
+            if (pos < cap) {
+              sk[pos] = kk[e];
+              si[pos] = 4 * j + e;
+            }
+          }
+        }
+        if (wm) atomicOr(sbm + ((4 * j) >> 5), wm << ((4 * j) & 31));
+      }
+    }
+  } else if ((M & 3) == 0 && ((reinterpret_cast<uintptr_t>(sc) & 15) == 0)) {
     // U float4 loads in flight per thread per round (the shared-memory atomics
     // in visit() would otherwise serialise one L2 round trip per load)
     constexpr int U = 16;
@@ -194,6 +242,7 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
   }
   __syncthreads();
   sel_stamp(tr, 3);
+  if (tr && threadIdx.x == 0) tr[7] = (uint64_t)s_nc;  // candidates in the threshold bin
 }
 
 }  // namespace kvb

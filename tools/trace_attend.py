@@ -42,6 +42,9 @@ def report(tag, lib, B, S):
     base = B * S * 8 + 64
     if n >= base + B * S * 8:
         sub = buf[base: base + B * S * 8].reshape(B * S, 8).astype(np.float64)
+        ncand = sub[:, 7]
+        if (ncand > 0).any():
+            print(f"    threshold-bin candidates per CTA: min {ncand.min():.0f} med {np.median(ncand):.0f} max {ncand.max():.0f}")
         names = ["threshold", "scan", "bisect", "winners", "id list", "union prefix"]
         w = ph[:, 6]
         for i, nm in enumerate(names):
