@@ -73,6 +73,11 @@ int64_t trace_read(uint64_t* host, int64_t max_words) {
 
 bool pdl_enabled();
 
+static int env_int_api(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        void** args) {
   cudaLaunchConfig_t cfg{};
@@ -225,6 +230,7 @@ void free_store(kvb_store* s) {
 
   cudaFree(s->k2_meta);
   cudaFree(s->k2_overflow);
+  cudaFree(s->fused_ctr);
   cudaFree(s->res_bitmap);
   cudaFree(s->res_prefix);
   cudaFree(s->res_k);
@@ -343,6 +349,8 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc(&s->k2_hist, B * kTopHistBins, "K2 histogram")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->fused_ctr, 1 + 2 * B, "fused layer counters")) != KVB_OK) return bail(st);
+  cudaMemset(s->fused_ctr, 0, (1 + 2 * B) * sizeof(int));
   s->Wc = (s->C + 31) / 32;
   cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
   cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
@@ -940,14 +948,35 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   L.lse = lse;
   L.k_path = att->k_path;
   L.ws = aws;
-  KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
-  KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
-  KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
-  KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
   const int K = sel->n_select;
   const bool chunk_path =
       attend_bulk_supported(s, L.G, s->d.max_resident + K * s->d.chunk_size, K);
   const bool tc_scan = !sel->exact_scores && higgs_tc_supported(s);
+  // fused layer kernel (scan + q~ fold + attention items in one persistent
+  // launch, kvb_attend_bulk.cu k5_fused_layer): experimental, opt-in with
+  // KVB_FUSED=1 -- measured slower at C2 (1524 vs 2740 tok/s): its register-fed
+  // scan items reach ~25 GB/s per SM and the last sequence's attention stays
+  // serial behind the whole scan
+  const bool fused = env_int_api("KVB_FUSED", 0) && chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
+                     !s->att_stream && fused_layer_supported(s, L.G, K);
+  if (fused) {
+    Carve sv(sws, sb);
+    float* sc = sv.take<float>((size_t)s->d.batch * s->C);
+    if (s->k2_dirty) {
+      KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->fused_ctr, 0, sizeof(int) * (1 + 2 * s->d.batch), st), "counter reset");
+      s->k2_dirty = false;
+    }
+    s->k2_dirty = true;
+    KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids, nullptr, 1),
+             "fused decode layer");
+    s->k2_dirty = false;
+    return KVB_OK;
+  }
+  KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
+  KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
+  KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
+  KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
   // attention-side top-K: every attention CTA streams the sequence's C scores
   // once (L2), cheap for chunked landmarks; at chunk 1 (C = n) the whole-GPU
   // K2a split + per-sequence K2b finish is used instead

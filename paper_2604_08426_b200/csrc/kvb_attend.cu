@@ -839,7 +839,8 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
 
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores,
-                                 uint32_t* sel_hist, int32_t* chunk_out, const float* svd_logits) {
+                                 uint32_t* sel_hist, int32_t* chunk_out, const float* svd_logits,
+                                 int fused) {
   const int G = a.G;
   const int pos_cap = s->d.max_resident + K * s->d.chunk_size;
   if (!attend_bulk_supported(s, G, pos_cap, K)) return cudaErrorNotSupported;
@@ -868,6 +869,7 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
   bl.sel_hist = sel_hist;
   bl.chunk_out = chunk_out;
   bl.svd_logits = svd_logits;
+  bl.fused = fused;
   return launch_attend_bulk(s, bl, st);
 }
 

@@ -58,6 +58,7 @@ struct kvb_store {
   // two-batch overlap (kvb_store_set_overlap): the decode step's attention +
   // merge go to att_stream (event-ordered after the scan) on att_sms SMs
   cudaStream_t att_stream = nullptr;
+  int* fused_ctr = nullptr;  // [1 + 2B] k5_fused_layer queue / done counters (self-cleaning)
   int att_sms = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sel = nullptr, ev_union = nullptr;
 };
@@ -192,15 +193,19 @@ struct BulkLaunch {
   int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
   int32_t* ntok_out = nullptr;  // [B]
   int tcap = 0;
+  // fused layer (k5_fused_layer): the dense landmark scan and the q~ fold run
+  // as items of the attention kernel itself (sel_scores / sel_hist written there)
+  int fused = 0;
 };
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K = 0);
+bool fused_layer_supported(const kvb_store* s, int G, int K);
 int attend_bulk_splits(const kvb_store* s, int positions_cap);
 cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st);
 // decode-step attention over residents + selected chunks (chunk ids [B][K])
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores = nullptr,
                                  uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr,
-                                 const float* svd_logits = nullptr);
+                                 const float* svd_logits = nullptr, int fused = 0);
 // the two halves of launch_attend: per-step query prep, then the attention
 cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
