@@ -16,4 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k3_
   -o $O/prof_recon python bench.py --variant shadowkv_recon --profile-steps 2 --layers 2 --also "" > $O/ncu_recon.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1h_score|k2b" -s 2 -c 2 \
   -o $O/prof_higgs python bench.py --variant higgs2c1 --profile-steps 2 --layers 2 --also "" > $O/ncu_higgs.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1h_resid|k2_select|k1h_score" -s 3 -c 3 \
+  -o $O/prof_pb python bench.py --variant proposed_b --profile-steps 2 --layers 2 --also "" > $O/ncu_pb.log 2>&1
+timeout 600 python bench.py --variant proposed_b --steps 10 --warmup 3 --also "" > $O/bench_pb.json 2>&1
 ls $O
