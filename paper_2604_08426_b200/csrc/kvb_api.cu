@@ -973,10 +973,21 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     s->k2_dirty = false;
     return KVB_OK;
   }
-  KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
-  KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
-  KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
-  KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
+  // dense scan + attention-side top-K on the caller's stream: prep (plain
+  // launch, triggers at entry) -> scan (PDL, overlaps the prep; waits for it
+  // at exit) -> attention -> merge, no side stream or events. Other paths
+  // fork the prep onto the side stream.
+  const bool inline_prep = chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
+                           s->C <= 32768 && s->d.landmark_kind == KVB_LM_DENSE && !s->att_stream &&
+                           env_int_api("KVB_INLINE_PREP", 1);
+  if (inline_prep) {
+    KVB_CUDA(launch_attend_prep(s, L, st), "attention prep");
+  } else {
+    KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
+    KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");
+    KVB_CUDA(launch_attend_prep(s, L, s->side), "attention prep");
+    KVB_CUDA(cudaEventRecord(s->ev_join, s->side), "join");
+  }
   // attention-side top-K: every attention CTA streams the sequence's C scores
   // once (L2), cheap for chunked landmarks; at chunk 1 (C = n) the whole-GPU
   // K2a split + per-sequence K2b finish is used instead
@@ -996,7 +1007,8 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     if (tc_scan)
       KVB_CUDA(launch_score_higgs_tc(s, q, L.G, sc, tcws, s->k2_hist, st), "HIGGS tensor-core scoring");
     else
-      KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st), "landmark scoring");
+      KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, inline_prep),
+               "landmark scoring");
     if (s->att_stream) {
       // two-batch overlap: attention on the (high-priority) attention stream,
       // event-ordered after the scan; the caller's stream resumes after it
@@ -1008,7 +1020,7 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
       KVB_CUDA(cudaEventRecord(s->ev_union, s->att_stream), "attention done");
       KVB_CUDA(cudaStreamWaitEvent(st, s->ev_union, 0), "attention wait");
     } else {
-      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+      if (!inline_prep) KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
       KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
     }
     s->k2_dirty = false;

@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                int* __restrict__ counters) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
+  pdl_trigger();  // decode step: the PDL-launched scan may start beside this kernel
   // split tickets of the attention that follows (self-resetting; zeroed here
   // so a fresh caller workspace needs no memset)
   if (counters && h == 0 && blockIdx.z == 0 && threadIdx.x == 0) counters[b] = 0;

@@ -84,7 +84,7 @@ int resident_ctas(const void* func, int threads, size_t smem);
 // hist (may be null): [B][2048] uint32, zeroed by the caller; receives the
 // histogram of the top 11 bits of the score keys (sum aggregation only).
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st);
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl = false);
 constexpr int kTopHistBins = 2048;
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);

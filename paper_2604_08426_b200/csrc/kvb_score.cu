@@ -135,6 +135,9 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
       if (shist[i]) atomicAdd(gh + i, shist[i]);
   }
+  // PDL-launched behind k5_prep (decode step): this grid's completion then
+  // implies the prep's, for the attention that waits on this grid
+  pdl_wait();
 }
 
 // Generic fallback for very wide rows: identical order, q_bar read from smem.
@@ -170,6 +173,7 @@ k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
       if (hist) atomicAdd(hist + (size_t)b * kHistBins + (score_key(a) >> 21), 1u);
     }
   }
+  pdl_wait();  // see k1_dense_sum
 }
 
 // ---------------------------------------------------------------------------
@@ -382,7 +386,7 @@ int score_grid_x(int C, int B, const void* func, size_t smem) {
 
 template <typename T>
 cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, int G,
-                               float* scores, uint32_t* hist, cudaStream_t st) {
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim, E = s->E;
   constexpr int VWv = 16 / sizeof(T);
   const bool vec = (E % VWv) == 0;
@@ -404,6 +408,7 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   count_launch();
   void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D,
                   (void*)&hist};
+  if (pdl) return launch_pdl(fn, grid, dim3(kScoreThreads), smem, st, args);
   return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
 }
@@ -411,13 +416,14 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
 }  // namespace
 
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st) {
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim;
   if (agg == KVB_AGG_SUM) {
     if (s->d.kv_dtype == KVB_BF16)
-      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st);
-    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st);
+      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st, pdl);
+    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st, pdl);
   }
+  if (pdl) return cudaErrorInvalidValue;  // the max scan is never PDL-chained
   const size_t smem = (size_t)H * G * D * sizeof(float);
   const void* fmax_fn = s->d.kv_dtype == KVB_BF16 ? (const void*)k1_dense_max<__nv_bfloat16>
                                                   : (const void*)k1_dense_max<float>;
