@@ -973,15 +973,15 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     s->k2_dirty = false;
     return KVB_OK;
   }
-  // dense scan + attention-side top-K on the caller's stream: prep (plain
-  // launch, triggers at entry) -> scan (PDL, overlaps the prep; waits for it
-  // at exit) -> attention -> merge, no side stream or events. Other paths
-  // fork the prep onto the side stream.
+  // dense scan + attention-side top-K on the caller's stream: prep (PDL: waits
+  // for the stream's previous work, then triggers) -> scan (PDL, overlaps the
+  // prep; waits for it at exit) -> attention -> merge, no side stream or
+  // events. Other paths fork the prep onto the side stream.
   const bool inline_prep = chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
                            s->C <= 32768 && s->d.landmark_kind == KVB_LM_DENSE && !s->att_stream &&
                            env_int_api("KVB_INLINE_PREP", 1);
   if (inline_prep) {
-    KVB_CUDA(launch_attend_prep(s, L, st), "attention prep");
+    KVB_CUDA(launch_attend_prep(s, L, st, true), "attention prep");
   } else {
     KVB_CUDA(cudaEventRecord(s->ev_fork, st), "fork");
     KVB_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0), "fork wait");

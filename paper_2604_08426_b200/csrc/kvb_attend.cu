@@ -603,7 +603,10 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                int* __restrict__ counters) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
-  pdl_trigger();  // decode step: the PDL-launched scan may start beside this kernel
+  // decode step: PDL-launched behind the previous layer -- wait for it before
+  // touching q, then let the PDL-launched scan start beside this kernel
+  pdl_wait();
+  pdl_trigger();
   // split tickets of the attention that follows (self-resetting; zeroed here
   // so a fresh caller workspace needs no memset)
   if (counters && h == 0 && blockIdx.z == 0 && threadIdx.x == 0) counters[b] = 0;
@@ -754,7 +757,7 @@ AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo
 
 }  // namespace
 
-cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl) {
   const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
   AttGeom geo = attend_geometry(s, G, a.cap);
   AttWs w = carve_att_ws(s, a, geo);
@@ -763,10 +766,17 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
   ensure_smem((const void*)k5_prep, fs);
   count_launch();
-  k5_prep<<<dim3(H, B, svd ? 4 : 1), 256, fs, st>>>(a.q, svd ? s->svd_right : nullptr, w.q2, w.qt2,
-                                                    H, G, D, r, svd ? s->d.svd_groups : 1,
-                                                    w.counters);
-  return cudaGetLastError();
+  const float* q = a.q;
+  const uint16_t* right = svd ? s->svd_right : nullptr;
+  float* q2 = w.q2;
+  float* qt2 = w.qt2;
+  int Hh = H, Gg = G, Dd = D, rr = r, sg = svd ? s->d.svd_groups : 1;
+  int* ctr = w.counters;
+  void* args[] = {(void*)&q, (void*)&right, (void*)&q2, (void*)&qt2, (void*)&Hh, (void*)&Gg,
+                  (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr};
+  const dim3 grid(H, B, svd ? 4 : 1);
+  if (pdl) return launch_pdl((const void*)k5_prep, grid, dim3(256), fs, st, args);
+  return cudaLaunchKernel((const void*)k5_prep, grid, dim3(256), args, fs, st);
 }
 
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st) {

@@ -1027,6 +1027,8 @@ __global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict_
                                                      uint32_t* __restrict__ hist_clear,
                                                      int* __restrict__ fctr_clear, int nfctr) {
   const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x, lane = d & 31;
+  // the next layer's (PDL-launched, waiting) prep may become resident now
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // the fused layer kernel (complete) was the last user of its work counters
   if (fctr_clear && row == 0 && b == 0)

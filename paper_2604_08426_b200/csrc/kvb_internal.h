@@ -207,7 +207,7 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
                                  uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr,
                                  const float* svd_logits = nullptr, int fused = 0);
 // the two halves of launch_attend: per-step query prep, then the attention
-cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl = false);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
                                    int D, float* out, float* lse, cudaStream_t st);
