@@ -282,16 +282,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       qraw[ks][2] = ok ? __ldg(rr + 8) : 0.f;
       qraw[ks][3] = ok ? __ldg(rr + 9) : 0.f;
     }
-    const float* qt = p.qt2 + (size_t)b * HG * p.r;
-#pragma unroll
-    for (int ks = 0; ks < NKS; ++ks)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        const int rr = ks * 16 + 2 * tig + 8 * hf;
-        qtraw[ks][hf] = (p.svd && ok && rr < p.r)
-                            ? *reinterpret_cast<const float2*>(qt + ((size_t)(rr >> 1) * HG + warp * G + qcol) * 2)
-                            : make_float2(0.f, 0.f);
-      }
   }
   const uint32_t* bm = p.res_bm + (size_t)b * p.W;
   const int32_t* pre = p.res_prefix + (size_t)b * p.W;
@@ -304,6 +294,21 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
   pdl_wait();  // the selection (token / chunk list) of the previous kernel
   KVB_STAMP(6);
+  // q~ (k5_prep) only after the wait: the prep triggers its dependents at
+  // entry, so it may still be running while this grid is resident
+  if (warp < H) {
+    const bool ok = qcol < G;
+    const float* qt = p.qt2 + (size_t)b * HG * p.r;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int rr = ks * 16 + 2 * tig + 8 * hf;
+        qtraw[ks][hf] = (p.svd && ok && rr < p.r)
+                            ? *reinterpret_cast<const float2*>(qt + ((size_t)(rr >> 1) * HG + warp * G + qcol) * 2)
+                            : make_float2(0.f, 0.f);
+      }
+  }
   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     // top-K from the scan's scores + histogram into a bitmap in the (not yet
     // used) ring, then ascending ids: each thread owns a run of words, one scan
