@@ -292,6 +292,29 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   int32_t* ud = ur + p.Rcap;                                 // [Rcap + 1]
   if (p.mode == 1)  // residents are store state: load them before waiting on the scan
     for (int i = tid; i < nres; i += nthr) ur[i] = p.res_ids[(size_t)b * p.Rcap + i];
+  // prologue top-K (VAR 2): the first tiles are this CTA's residents (exact
+  // K/V, store state) -- stage up to 2 full resident tiles into ring slots 0..
+  // before waiting on the scan, so their data lands during the selection.
+  // Same slot / owner mapping as produce() for k < pre_done (it skips them).
+  int pre_done = 0;
+  if (VAR == 2 && p.mode == 1 && p.sel_scores && !(p.dbg & 2)) {
+    pre_done = min(min(2, n_rloc / ett), nst - 1);
+    const int vbytes0 = H * kBD * 2;
+    for (int k = 0; k < pre_done; ++k) {
+      if (k % H != warp) continue;
+      unsigned char* st = ring + (size_t)k * p.stage_bytes;
+      const int j = lane & 15;
+      uint32_t bytes = lane < 16 && j < ett ? (uint32_t)(2 * vbytes0) : 0u;
+      bytes = __reduce_add_sync(FULL, bytes);
+      if (lane == 0) mbar_arrive_tx(full + k, bytes);
+      __syncwarp();
+      if (j < ett) {
+        const size_t off = ((size_t)b * p.Rcap + (r_lo + k * ett + j)) * vbytes0;
+        if (lane < 16) bulk_g2s(st + j * p.vrow, p.res_v + off, vbytes0, full + k);
+        else bulk_g2s(st + ett * p.vrow + j * p.krow_ex, p.res_k + off, vbytes0, full + k);
+      }
+    }
+  }
   pdl_wait();  // the selection (token / chunk list) of the previous kernel
   KVB_STAMP(6);
   // q~ (k5_prep) only after the wait: the prep triggers its dependents at
@@ -312,9 +335,11 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     // top-K from the scan's scores + histogram into a bitmap in the (not yet
     // used) ring, then ascending ids: each thread owns a run of words, one scan
-    uint32_t* wb = reinterpret_cast<uint32_t*>(ring);
+    // the selection's scratch lives in the ring slots after the prefetched ones
+    unsigned char* pro = ring + (size_t)pre_done * p.stage_bytes;
+    uint32_t* wb = reinterpret_cast<uint32_t*>(pro);
     uint32_t* sk = wb + ((p.Wc + 3) & ~3);
-    const size_t ring_bytes = (size_t)nst * p.stage_bytes;
+    const size_t ring_bytes = (size_t)(nst - pre_done) * p.stage_bytes;
     const size_t used = (size_t)((p.Wc + 3) & ~3) * 4;
     const float* scs = p.sel_scores + (size_t)b * p.C;
     // stage the sequence's scores in the ring's tail by bulk copies (overlaps
@@ -323,7 +348,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     const bool staged = (sbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(scs) & 15) == 0) &&
                         used + sbytes + 4096 * 8 <= ring_bytes && !(p.dbg & 4);
     __shared__ __align__(8) uint64_t stage_bar;
-    float* stage = staged ? reinterpret_cast<float*>(ring + ring_bytes - sbytes) : nullptr;
+    float* stage = staged ? reinterpret_cast<float*>(pro + ring_bytes - sbytes) : nullptr;
     if (staged && tid == 0) {
       mbar_init(&stage_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -482,7 +507,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       ++pk_rnd;
     }
     if (++pk_own == H) pk_own = 0;
-    if (k >= ntiles || !mine) return;
+    if (k >= ntiles || !mine || k < pre_done) return;  // k < pre_done: staged before the wait
     if (rnd > 0) mbar_wait(empty + stg, (rnd - 1) & 1);
     const bool sv = k >= t_ex;
     const int tt = sv ? kBT : ett;
