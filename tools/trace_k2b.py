@@ -22,9 +22,21 @@ def main():
         a.variant = sys.argv[1]
     torch.cuda.set_device(0)
     lib = _lib.load()
-    stores, (H, G, D) = bench.build_layers(a, 0)
-    st = stores[0]
-    K = st.n_select(a.budget / a.ctx)
+    if a.variant == "c4":  # 1M ctx, 4 kv / 28 q heads, batch 1 (one shard = whole sequence)
+        from paper_2604_08426_b200 import sharded as SH
+
+        H, G, D, n = 4, 7, 128, 1 << 20
+        a.batch = 1
+        spec = SH.ShardSpec(n, 8, 1, 0)
+        k = torch.randn((1, n, H, D), device="cuda", dtype=torch.bfloat16)
+        v = torch.randn((1, n, H, D), device="cuda", dtype=torch.bfloat16)
+        st = SH.build_shard(k, v, spec, SH.SoloExchange())
+        del k, v
+        K = SH.global_k(n, 8, 0.0156)
+    else:
+        stores, (H, G, D) = bench.build_layers(a, 0)
+        st = stores[0]
+        K = st.n_select(a.budget / a.ctx)
     plan = st.decode_plan(G, K)
     q = torch.randn((a.batch, H, G, D), device="cuda")
     for _ in range(3):
