@@ -1168,7 +1168,7 @@ bool fused_layer_supported(const kvb_store* s, int G, int K) {
   return s->d.landmark_kind == KVB_LM_DENSE && s->d.kv_dtype == KVB_BF16 &&
          (E == 1024 || E == 512) && s->d.head_dim == kBD && s->C <= 32768 &&
          attend_bulk_supported(s, G, s->d.max_resident + K * s->d.chunk_size, K) &&
-         (s->d.slow_kind != KVB_SLOW_SVD || s->d.svd_rank % 2 == 0);
+         (s->d.slow_kind != KVB_SLOW_SVD || s->d.svd_rank == 160);
 }
 
 int attend_bulk_splits(const kvb_store* s, int positions_cap) {
@@ -1279,12 +1279,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
     p.splits_fused = g.splits;
     const int nv = E / 256;
 #define KVB_FUSED_NKS(Q, NVv)                                                        \
-  switch (nks) {                                                                     \
+  switch (nks) {  /* experimental path: exact keys or rank 160 only (build time) */  \
     case 0: fn = (const void*)k5_fused_layer<Q, 0, NVv>; break;                      \
-    case 2: fn = (const void*)k5_fused_layer<Q, 2, NVv>; break;                      \
-    case 4: fn = (const void*)k5_fused_layer<Q, 4, NVv>; break;                      \
-    case 6: fn = (const void*)k5_fused_layer<Q, 6, NVv>; break;                      \
-    case 8: fn = (const void*)k5_fused_layer<Q, 8, NVv>; break;                      \
     case 10: fn = (const void*)k5_fused_layer<Q, 10, NVv>; break;                    \
     default: return cudaErrorNotSupported;                                           \
   }
