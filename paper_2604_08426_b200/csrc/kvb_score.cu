@@ -78,56 +78,111 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
   const int wpc = blockDim.x >> 5;
   const int gw = blockIdx.x * wpc + (threadIdx.x >> 5);
   const int nw = gridDim.x * wpc;
-  for (int c = gw * 2; c < C; c += nw * 2) {
-    const bool two = (c + 1) < C;
-    const T* r0 = base + (size_t)c * E;
-    const T* r1 = r0 + E;
-    float a0 = 0.f, a1 = 0.f;
-    if constexpr (VW * sizeof(T) == 16) {
-      uint4 v0[NV], v1[NV];
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int v = lane + 32 * i;
-        if (v < nvec) {
-          v0[i] = ld_stream(r0 + (size_t)v * VW);
-          if (two) v1[i] = ld_stream(r1 + (size_t)v * VW);
+  // RW rows in flight per warp: 2 for 2 KiB rows (8 heads bf16), 4 for
+  // narrower rows (C4: 4 heads) so each warp keeps ~4 KiB of loads in flight
+  constexpr int RW = (VW * sizeof(T) == 16 && NV <= 2) ? 4 : 2;
+  if constexpr (RW == 2) {
+    for (int c = gw * 2; c < C; c += nw * 2) {
+      const bool two = (c + 1) < C;
+      const T* r0 = base + (size_t)c * E;
+      const T* r1 = r0 + E;
+      float a0 = 0.f, a1 = 0.f;
+      if constexpr (VW * sizeof(T) == 16) {
+        uint4 v0[NV], v1[NV];
+  #pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int v = lane + 32 * i;
+          if (v < nvec) {
+            v0[i] = ld_stream(r0 + (size_t)v * VW);
+            if (two) v1[i] = ld_stream(r1 + (size_t)v * VW);
+          }
+        }
+  #pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int v = lane + 32 * i;
+          if (v < nvec) {
+            float f[VW];
+            Vec<T>::unpack(v0[i], f);
+  #pragma unroll
+            for (int j = 0; j < VW; ++j) a0 = fmaf(qr[i][j], f[j], a0);
+            if (two) {
+              Vec<T>::unpack(v1[i], f);
+  #pragma unroll
+              for (int j = 0; j < VW; ++j) a1 = fmaf(qr[i][j], f[j], a1);
+            }
+          }
+        }
+      } else {  // scalar layout (VW == 1): odd row sizes
+  #pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int v = lane + 32 * i;
+          if (v < nvec) {
+            a0 = fmaf(qr[i][0], to_f32(r0[v]), a0);
+            if (two) a1 = fmaf(qr[i][0], to_f32(r1[v]), a1);
+          }
         }
       }
+      a0 = warp_sum_butterfly(a0);
+      a1 = warp_sum_butterfly(a1);
+      if (lane == 0) {
+        out[c] = a0;
+        if (hist) atomicAdd(&shist[score_key(a0) >> 21], 1u);
+        if (two) {
+          out[c + 1] = a1;
+          if (hist) atomicAdd(&shist[score_key(a1) >> 21], 1u);
+        }
+      }
+    }
+  } else {
+  for (int c = gw * RW; c < C; c += nw * RW) {
+    float a[RW];
 #pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int v = lane + 32 * i;
-        if (v < nvec) {
-          float f[VW];
-          Vec<T>::unpack(v0[i], f);
+    for (int r = 0; r < RW; ++r) a[r] = 0.f;
+    if constexpr (VW * sizeof(T) == 16) {
+      uint4 v[RW][NV];
 #pragma unroll
-          for (int j = 0; j < VW; ++j) a0 = fmaf(qr[i][j], f[j], a0);
-          if (two) {
-            Vec<T>::unpack(v1[i], f);
+      for (int r = 0; r < RW; ++r)
 #pragma unroll
-            for (int j = 0; j < VW; ++j) a1 = fmaf(qr[i][j], f[j], a1);
+        for (int i = 0; i < NV; ++i) {
+          const int vv = lane + 32 * i;
+          if (vv < nvec && c + r < C) v[r][i] = ld_stream(base + (size_t)(c + r) * E + (size_t)vv * VW);
+        }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        if (c + r >= C) break;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int vv = lane + 32 * i;
+          if (vv < nvec) {
+            float f[VW];
+            Vec<T>::unpack(v[r][i], f);
+#pragma unroll
+            for (int jj = 0; jj < VW; ++jj) a[r] = fmaf(qr[i][jj], f[jj], a[r]);
           }
         }
       }
     } else {  // scalar layout (VW == 1): odd row sizes
 #pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int v = lane + 32 * i;
-        if (v < nvec) {
-          a0 = fmaf(qr[i][0], to_f32(r0[v]), a0);
-          if (two) a1 = fmaf(qr[i][0], to_f32(r1[v]), a1);
+      for (int r = 0; r < RW; ++r) {
+        if (c + r >= C) break;
+        const T* rr = base + (size_t)(c + r) * E;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int vv = lane + 32 * i;
+          if (vv < nvec) a[r] = fmaf(qr[i][0], to_f32(rr[vv]), a[r]);
         }
       }
     }
-    a0 = warp_sum_butterfly(a0);
-    a1 = warp_sum_butterfly(a1);
-    if (lane == 0) {
-      out[c] = a0;
-      if (hist) atomicAdd(&shist[score_key(a0) >> 21], 1u);
-      if (two) {
-        out[c + 1] = a1;
-        if (hist) atomicAdd(&shist[score_key(a1) >> 21], 1u);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      if (c + r >= C) break;
+      const float x = warp_sum_butterfly(a[r]);
+      if (lane == 0) {
+        out[c + r] = x;
+        if (hist) atomicAdd(&shist[score_key(x) >> 21], 1u);
       }
     }
+  }
   }
   if (hist) {
     __syncthreads();
