@@ -304,7 +304,11 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
     const int32_t* __restrict__ cand, int nc, int C, int n, float* __restrict__ tok_s, int H,
     int ngroups, int gbytes, int tiles_per_cta) {
   constexpr int kTPI = 4;
-  __shared__ uint32_t lut[2][4 * 32];
+  // pair LUT: entry e = (code 2ks) | (code 2ks + 1) << 2 = one nibble of the
+  // lane's code word -> uint2 {half2 cb[c0], half2 cb[c1]} = the A-fragment
+  // registers {a0, a2} (row g4) or {a1, a3} (row g4 + 8) of k-step ks in one
+  // LDS.64; 16 entries x 32 lane copies x 8 B, hi and lo tables
+  __shared__ __align__(16) uint2 lut[2][16 * 32];
   __shared__ float part[2][HMAX][kTPI * kTileRows];  // double-buffered: one barrier per iteration
   extern __shared__ int32_t s_cand[];               // [2 per] candidate ids, then [2 per] base scores
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -321,12 +325,14 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
     s_cand[i] = c;
     s_base[i] = __ldg(chunk_s + (size_t)b * C + c);
   }
-  for (int i = threadIdx.x; i < 4 * 32; i += blockDim.x) {
-    const int e = i >> 5;
-    const __half2 hx = __floats2half2_rn(cb[2 * e], cb[2 * e + 1]);
-    const float2 fx = __half22float2(hx);
-    lut[0][i] = h2u(hx);
-    lut[1][i] = h2u(__floats2half2_rn(cb[2 * e] - fx.x, cb[2 * e + 1] - fx.y));
+  for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {
+    const int e = i >> 5, c0 = e & 3, c1 = e >> 2;
+    const __half2 h0 = __floats2half2_rn(cb[2 * c0], cb[2 * c0 + 1]);
+    const __half2 h1 = __floats2half2_rn(cb[2 * c1], cb[2 * c1 + 1]);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    lut[0][i] = make_uint2(h2u(h0), h2u(h1));
+    lut[1][i] = make_uint2(h2u(__floats2half2_rn(cb[2 * c0] - f0.x, cb[2 * c0 + 1] - f0.y)),
+                           h2u(__floats2half2_rn(cb[2 * c1] - f1.x, cb[2 * c1 + 1] - f1.y)));
   }
   uint32_t bhi[8][2], blo[8][2];
   {
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
   }
   __syncthreads();
   const unsigned char* lraw = reinterpret_cast<const unsigned char*>(&lut[0][0]);
-  const uint32_t lane4 = (uint32_t)lane * 4u;
+  const uint32_t lane8 = (uint32_t)lane * 8u;
   const uint8_t* cbase = codes + ((size_t)b * H + h) * (size_t)ngroups * gbytes + g4 * 16 + 4 * tig;
   const float* fbase = factors + ((size_t)b * H + h) * ngroups;
   const float sg0 = (__popc((2 * tig) & g4) & 1) ? -1.f : 1.f;
@@ -383,24 +389,20 @@ __global__ void __launch_bounds__(HMAX * 32) k1h_resid(
       float c[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f}, c3[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        // k-step ks: codes 2 ks (a0 / a1) and 2 ks + 1 (a2 / a3), rows g4 / g4 + 8
-        auto off = [&](uint32_t w, int s) {
-          return ((s >= 7 ? (w >> (s - 7)) : (w << (7 - s))) & 0x180u) | lane4;
+        // k-step ks: the nibble at bit 4 ks of each row's word holds codes
+        // 2 ks (a0 / a1) and 2 ks + 1 (a2 / a3): byte offset nibble * 256 | lane * 8
+        const int sh = 4 * ks;
+        auto off = [&](uint32_t w) {
+          return ((sh >= 8 ? (w >> (sh - 8)) : (w << (8 - sh))) & 0xF00u) | lane8;
         };
-        const int s0 = 4 * ks, s1 = 4 * ks + 2;
-        const uint32_t o0 = off(wv[u][0], s0), o1 = off(wv[u][1], s0);
-        const uint32_t o2 = off(wv[u][0], s1), o3 = off(wv[u][1], s1);
-        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(lraw + o0);
-        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(lraw + o1);
-        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(lraw + o2);
-        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(lraw + o3);
-        const uint32_t l0 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o0);
-        const uint32_t l1 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o1);
-        const uint32_t l2 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o2);
-        const uint32_t l3 = *reinterpret_cast<const uint32_t*>(lraw + 512 + o3);
-        mma_f16(c, a0, a1, a2, a3, bhi[ks][0], bhi[ks][1]);
-        mma_f16(c2, a0, a1, a2, a3, blo[ks][0], blo[ks][1]);
-        mma_f16(c3, l0, l1, l2, l3, bhi[ks][0], bhi[ks][1]);
+        const uint32_t o0 = off(wv[u][0]), o1 = off(wv[u][1]);
+        const uint2 A02 = *reinterpret_cast<const uint2*>(lraw + o0);   // row g4: a0, a2
+        const uint2 A13 = *reinterpret_cast<const uint2*>(lraw + o1);   // row g4 + 8: a1, a3
+        const uint2 L02 = *reinterpret_cast<const uint2*>(lraw + 4096 + o0);
+        const uint2 L13 = *reinterpret_cast<const uint2*>(lraw + 4096 + o1);
+        mma_f16(c, A02.x, A13.x, A02.y, A13.y, bhi[ks][0], bhi[ks][1]);
+        mma_f16(c2, A02.x, A13.x, A02.y, A13.y, blo[ks][0], blo[ks][1]);
+        mma_f16(c3, L02.x, L13.x, L02.y, L13.y, bhi[ks][0], bhi[ks][1]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) c[i] = (c[i] + c2[i]) + c3[i];
