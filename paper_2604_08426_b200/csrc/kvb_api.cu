@@ -828,9 +828,12 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     KVB_CUDA(launch_select(s, L, st), "candidate chunks");
   }
   // stage 2: candidate tokens (:153), residual-refined scores (:155-158)
-  KVB_CUDA(launch_candidate_tokens(s, joined ? cand_sorted : chunk_ids, (int)nc, cand_tok, cand_count,
-                                   cand_sorted, st),
-           "candidate tokens");
+  if (joined)  // the candidate set is already ascending
+    KVB_CUDA(launch_candidate_tokens_sorted(s, cand_sorted, (int)nc, cand_tok, cand_count, st),
+             "candidate tokens");
+  else
+    KVB_CUDA(launch_candidate_tokens(s, chunk_ids, (int)nc, cand_tok, cand_count, cand_sorted, st),
+             "candidate tokens");
   if (!a->exact_scores && resid_tc_supported(s))
     KVB_CUDA(launch_residual_scores_tc(s, q, a->queries_per_head, chunk_s, cand_sorted, (int)nc,
                                        tok_s, rtws, st),

@@ -140,6 +140,8 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
                        void** args);
 
 // Ascending list of the tokens of the selected chunks (Appendix-E stage 2).
+cudaError_t launch_candidate_tokens_sorted(const kvb_store* s, const int32_t* cand_sorted, int n_cand,
+                                           int32_t* cand_tok, int32_t* cand_count, cudaStream_t st);
 cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,
                                     int32_t* cand_tok, int32_t* cand_count,
                                     int32_t* cand_chunks_sorted, cudaStream_t st);

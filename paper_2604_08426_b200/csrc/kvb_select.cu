@@ -971,6 +971,35 @@ k_candidate_tokens(const int32_t* __restrict__ cand, int n_cand, int C, int n, i
   }
 }
 
+// Candidate chunks already ascending (K2b sorted output): the padded token
+// layout of k_candidate_tokens without the bitmap re-sort, one thread per
+// (position, token slot) over the whole grid.
+__global__ void k_candidate_tokens_sorted(const int32_t* __restrict__ cand_sorted, int n_cand, int C,
+                                          int n, int cs, int32_t* __restrict__ cand_tok,
+                                          int32_t* __restrict__ cand_count) {
+  const int b = blockIdx.y;
+  const int total = n_cand * cs;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = cand_sorted[(size_t)b * n_cand + i / cs];
+    cand_tok[(size_t)b * total + i] = c * cs + i % cs;  // tokens past n: never ranked (count)
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // only the last chunk can be short, and it sorts last
+    const bool tail = cand_sorted[(size_t)b * n_cand + n_cand - 1] == C - 1;
+    cand_count[b] = total - (tail ? (C * cs - n) : 0);
+  }
+}
+
+cudaError_t launch_candidate_tokens_sorted(const kvb_store* s, const int32_t* cand_sorted, int n_cand,
+                                           int32_t* cand_tok, int32_t* cand_count, cudaStream_t st) {
+  const int total = n_cand * s->d.chunk_size;
+  const int blocks = std::min((total + 255) / 256, 512);
+  count_launch();
+  k_candidate_tokens_sorted<<<dim3(blocks, s->d.batch), 256, 0, st>>>(
+      cand_sorted, n_cand, s->C, s->d.n_tokens, s->d.chunk_size, cand_tok, cand_count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chunks, int n_cand,
                                     int32_t* cand_tok, int32_t* cand_count,
                                     int32_t* cand_chunks_sorted, cudaStream_t st) {
