@@ -64,13 +64,6 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--also", default="higgs2c1,shadowkv_recon",
                     help="comma-separated secondary variants reported under 'variants'")
-    ap.add_argument("--microbatches", type=int, default=1,
-                    help="split the batch into this many stores per layer, each decode chain on its own stream")
-    ap.add_argument("--overlap-sms", type=int, default=0,
-                    help="with --microbatches > 1: attention on per-micro-batch high-priority streams, "
-                         "grid sized for this many SMs (kvb_store_set_overlap)")
-    ap.add_argument("--mb-offset", type=int, default=0,
-                    help="micro-batch m starts after micro-batch m-1 finished this many layers")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N eager steps after setup (for ncu) and exit")
     return ap.parse_args()
@@ -163,9 +156,8 @@ def build_layers(a, rank):
     H, G, D = 8, 4, 128
     stores = []
     gen = torch.Generator(device="cuda")
-    mb = getattr(a, "microbatches", 1)
-    bsz = a.batch // mb
-    for layer in range(a.layers * mb):
+    bsz = a.batch
+    for layer in range(a.layers):
         gen.manual_seed(1000 * rank + layer)
         shape = (bsz, a.ctx, H, D)
         k = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
@@ -280,63 +272,6 @@ def time_oracle_slice(st, budget, q):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(a):
-    st, budget, qs = oracle_slice(a)
-    times = [time_oracle_slice(st, budget, q) for q in qs]
-    t = sorted(times)[len(times) // 2]
-    cores = os.cpu_count()
-    return {"value": round(1.0 / (a.layers * t), 4), "unit": "tok/s", "cores": cores,
-            "kind": "port",
-            "sample": (f"oracle/kvlab_port.py (numpy, kvlab's arithmetic) select_by_landmarks + "
-                       f"sparse_attention on one (layer, sequence) slice, n={a.ctx}, Hkv 8, G 4, "
-                       f"D 128, fp32, {a.variant}; median of {len(times)} = {t * 1e3:.1f} ms; "
-                       f"tok/s = 1/(layers x t_slice) (kvlab has no batching); "
-                       f"numpy BLAS may use up to {cores} threads")}
-
-
-def run_reference(a):
-    """--impl reference: the reference's CPU path (the oracle port of kvlab,
-    SURVEY 8c) on every host core: one forked worker per core, each timing
-    slices of the same workload; rank 0 only."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import multiprocessing as mp
-
-    st, budget, qs = oracle_slice(a)
-    cores = os.cpu_count() or 1
-    workers = max(1, min(cores, 64))
-    global _REF_STATE
-    _REF_STATE = (st, budget, qs)
-    ctx = mp.get_context("fork")
-    with ctx.Pool(workers, initializer=_ref_init) as pool:
-        for _ in range(max(1, a.warmup)):
-            pool.map(_ref_slice, range(workers))
-        walls = []
-        for _ in range(a.steps):
-            t0 = time.perf_counter()
-            pool.map(_ref_slice, range(workers))
-            walls.append(time.perf_counter() - t0)
-    t_round = sorted(walls)[len(walls) // 2]
-    slices_per_s = workers / t_round
-    tok_s = slices_per_s / a.layers
-    ms_full_step = a.layers * a.batch / slices_per_s * 1e3
-    line = {"metric": METRIC, "value": round(tok_s, 4), "unit": "tok/s", "impl": "reference",
-            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": round(ms_full_step, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": VARIANTS[a.variant], "layers": a.layers,
-                       "batch": a.batch, "ctx": a.ctx, "budget_tokens": a.budget},
-            "cpu_baseline": {"value": round(tok_s, 4), "unit": "tok/s", "cores": workers,
-                             "kind": "port",
-                             "sample": (f"{workers} forked workers x 1 (layer, sequence) slice per "
-                                        f"step, each single-threaded BLAS; full-step time "
-                                        f"extrapolated to {a.layers} layers x {a.batch} seqs")},
-            "e2e": {"value": round(tok_s, 4), "unit": "tok/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
 _REF_STATE = None
 
 
@@ -352,6 +287,91 @@ def _ref_init():
 def _ref_slice(i):
     st, budget, qs = _REF_STATE
     return time_oracle_slice(st, budget, qs[i % len(qs)])
+
+
+def reference_rate(a, steps, warmup):
+    """The reference's CPU path (oracle/kvlab_port.py: kvlab's numpy
+    arithmetic, pinned bit-exact to kvlab) over ALL layers x sequences of one
+    decode step: every timed step maps the layers*batch (layer, sequence)
+    slices (select_by_landmarks + sparse_attention each) over one forked
+    single-threaded worker per host core. Returns (tok/s, ms/step, workers,
+    measured step times)."""
+    import multiprocessing as mp
+
+    st, budget, qs = oracle_slice(a)
+    workers = max(1, min(os.cpu_count() or 1, 64))
+    global _REF_STATE
+    _REF_STATE = (st, budget, qs)
+    slices = a.layers * a.batch
+    walls = []
+    with mp.get_context("fork").Pool(workers, initializer=_ref_init) as pool:
+        for _ in range(warmup):
+            pool.map(_ref_slice, range(workers))
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_slice, range(slices), chunksize=1)
+            walls.append(time.perf_counter() - t0)
+    _REF_STATE = None
+    t = sorted(walls)[len(walls) // 2]
+    return a.batch / t, t * 1e3, workers, walls
+
+
+def ref_sample(a, workers, steps):
+    return (f"oracle/kvlab_port.py (kvlab's numpy arithmetic) select_by_landmarks + sparse_attention "
+            f"on every one of the {a.layers} layers x {a.batch} sequences = {a.layers * a.batch} "
+            f"(layer, sequence) slices per step (n={a.ctx}, Hkv 8, G 4, D 128, fp32: kvlab upcasts), "
+            f"mapped over {workers} forked single-threaded-BLAS workers (one per host core); "
+            f"median of {steps} measured full steps; slices share one synthetic state "
+            f"(the cost does not depend on values)")
+
+
+def cpu_baseline(a):
+    """cpu_baseline of the GPU line: the reference arm's measurement, one full step."""
+    tok_s, ms, workers, _ = reference_rate(a, steps=1, warmup=1)
+    return {"value": round(tok_s, 4), "unit": "tok/s", "cores": workers, "kind": "port",
+            "ms_per_step": round(ms, 1), "sample": ref_sample(a, workers, 1)}
+
+
+def bench_config(a, world, variant=None):
+    """The `config` object of both arms (identical keys and values)."""
+    variant = variant or a.variant
+    chunk = {"higgs2c1": 1, "higgs4c2": 2}.get(variant, 8)
+    K = min(-(-a.ctx // chunk), -(-a.budget // chunk))
+    H, D = 8, 128
+    E = H * D
+    R = 384 + 32
+    if variant.startswith("shadowkv"):
+        per = (-(-a.ctx // chunk)) * E * 2 + K * chunk * (160 * 2 + E * 2) + 160 * E * 2 + R * E * 4
+    else:
+        per = a.ctx * E // 4 + K * chunk * E * 4 + R * E * 4
+    step_gb = a.layers * a.batch * per / 1e9
+    return {"workload": VARIANTS[variant],
+            "model": "Llama-3.1-8B shape (32 layers, 32 q / 8 kv heads, d 128)",
+            "global_batch": world * a.batch, "seq_len": a.ctx, "layers": a.layers,
+            "chunk": chunk, "budget_tokens": a.budget, "selected_chunks": K,
+            "parallelism": f"dp{world} (replicas)",
+            "l2": f"no flush: inputs exceed L2 ({step_gb:.1f} GB algorithmic bytes per step vs 126 MB L2)"}
+
+
+def run_reference(a):
+    """--impl reference: the reference's CPU path on every host core, rank 0
+    only (other ranks exit without work)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    tok_s, ms, workers, walls = reference_rate(a, a.steps, a.warmup)
+    line = {"metric": METRIC, "value": round(tok_s, 4), "unit": "tok/s", "impl": "reference",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": bench_config(a, world),
+            "step_times_ms": [round(w * 1e3, 1) for w in walls],
+            "cpu_baseline": {"value": round(tok_s, 4), "unit": "tok/s", "cores": workers,
+                             "kind": "port", "sample": ref_sample(a, workers, len(walls))},
+            "e2e": {"value": round(tok_s, 4), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -378,16 +398,6 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
     q_host = q_dev.cpu().pin_memory()
     out_host = torch.empty_like(q_host).pin_memory()
     stream = torch.cuda.current_stream()
-    mb = a.microbatches
-    Bm = B // mb
-    mstreams = [torch.cuda.Stream() for _ in range(mb)] if mb > 1 else []
-    if mb > 1 and a.overlap_sms:
-        # two-batch overlap: each micro-batch's attention on its own
-        # high-priority stream, sized for overlap_sms SMs
-        astreams = [torch.cuda.Stream(priority=-1) for _ in range(mb)]
-        for l in range(L_):
-            for m in range(mb):
-                stores[l * mb + m].set_overlap(astreams[m], a.overlap_sms)
 
     def step():
         if variant == "proposed_b":
@@ -398,27 +408,8 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
                                                             exact=False)
                 out_dev[l].copy_(stores[l].attend(q_dev[l], tok, ntok)[0])
             return
-        if mb == 1:
-            for l in range(L_):
-                plans[l].run(q_dev[l], out_dev[l])
-            return
-        # micro-batch m owns stores [l * mb + m]; each chain runs its layers in
-        # order on its own stream (two-batch overlap); chain m may start
-        # mb_offset layers behind chain m-1
-        cur = torch.cuda.current_stream()  # the capture stream inside torch.cuda.graph
-        evs = [[torch.cuda.Event() for _ in range(L_)] for _ in range(mb)]
-        for m, s_ in enumerate(mstreams):
-            s_.wait_stream(cur)
         for l in range(L_):
-            for m, s_ in enumerate(mstreams):
-                with torch.cuda.stream(s_):
-                    if m > 0 and a.mb_offset and l == 0:
-                        s_.wait_event(evs[m - 1][min(a.mb_offset, L_) - 1])
-                    sl = slice(m * Bm, (m + 1) * Bm)
-                    plans[l * mb + m].run(q_dev[l, sl], out_dev[l, sl])
-                    evs[m][l].record(s_)
-        for s_ in mstreams:
-            cur.wait_stream(s_)
+            plans[l].run(q_dev[l], out_dev[l])
 
     if a.profile_steps:
         for _ in range(a.profile_steps):
@@ -484,11 +475,6 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
         ev_out[gi].record(stream)
 
     def e2e_step():
-        if mb > 1:
-            q_dev.copy_(q_host, non_blocking=True)
-            step()
-            out_host.copy_(out_dev, non_blocking=True)
-            return
         with torch.cuda.stream(h2d_s):
             for gi, g in enumerate(groups):
                 h2d_s.wait_event(ev_done[gi])        # previous step's layers read q_dev[g]
@@ -527,11 +513,11 @@ def measure(a, variant, rank, world, local, timed_breakdown=True):
 
     # per-stage device time: one CUDA graph per stage over all layers
     st0 = stores[0]
-    scores = [torch.empty((Bm, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
-    qb = [q_dev[l, :Bm] for l in range(L_)]          # micro-batch 0 (all of it when mb = 1)
-    ob = [out_dev[l, :Bm] for l in range(L_)]
-    sp = [stores[l * mb] for l in range(L_)]
-    pp = [plans[l * mb] for l in range(L_)]
+    scores = [torch.empty((B, st0.C), dtype=torch.float32, device="cuda") for _ in range(L_)]
+    qb = [q_dev[l] for l in range(L_)]
+    ob = [out_dev[l] for l in range(L_)]
+    sp = stores
+    pp = plans
 
     def stage_graph(fn):
         fn()
@@ -658,7 +644,10 @@ def run_c5(a, rank, world, local):
 
 
 def run_c4(a, rank, world, local):
-    """C4: one 1M-token sequence sharded over `world` GPUs (strong scaling)."""
+    """C4: one 1M-token sequence sharded over `world` GPUs (strong scaling).
+    Every P (1 included) runs the same ShardedDecoder step: local top-K ->
+    one all-gather of packed (score, id) records -> merge -> local token union
+    + attention with LSE -> one all-gather of packed (o, lse) -> exact merge."""
     import torch
     import torch.distributed as dist
 
@@ -668,9 +657,9 @@ def run_c4(a, rank, world, local):
     n = a.ctx if a.ctx != 131072 else 1 << 20
     L_ = a.layers if a.layers != 32 else 28
     B = 1
-    frac = 0.0156
     spec = SH.ShardSpec(n, cs, world, rank)
     ex = SH.Exchange() if world > 1 else SH.SoloExchange()
+    frac = 2048 * cs / n  # K = 2048 chunks at n = 1M
     gen = torch.Generator(device="cuda")
     t_build = time.perf_counter()
     decs = []
@@ -682,51 +671,67 @@ def run_c4(a, rank, world, local):
         v = torch.randn(shape, generator=gen, device="cuda", dtype=torch.bfloat16)
         st = SH.build_shard(k, v, spec, ex)
         del k, v
-        decs.append(SH.ShardedDecoder(st, spec, ex, K))
+        decs.append(SH.ShardedDecoder(st, spec, ex, K, G))
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
     qgen = torch.Generator(device="cuda").manual_seed(11)
     q = torch.randn((L_, B, H, G, D), generator=qgen, device="cuda")
 
+    def eager():
+        for l in range(L_):
+            decs[l].step(q[l])
+
+    eager()
+    torch.cuda.synchronize()
+    graph, step = None, eager
+    if not a.no_graph:
+        try:  # NCCL collectives are capturable; the Solo exchange is a copy
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                eager()
+            step = graph.replay
+        except Exception:
+            graph, step = None, eager
+            torch.cuda.synchronize()
+
+    def timed(fn, reps):
+        for _ in range(a.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms = timed(step, a.steps)
+    fused_p1 = None
     if world == 1:
-        # one GPU: the shard is the whole sequence -> the fused decode step,
-        # all layers captured in one CUDA graph (no exchange to do)
+        # reference point: the single-GPU fused decode chain (kvb_decode_step)
         plans = [d.store.decode_plan(G, K) for d in decs]
         out_dev = torch.empty_like(q)
 
-        def eager():
+        def fused():
             for l in range(L_):
                 plans[l].run(q[l], out_dev[l])
 
-        eager()
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            eager()
-        step = graph.replay
-    else:
-        def step():
-            for l in range(L_):
-                decs[l].step(q[l])
-
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with sampler:
-        e0.record()
-        for _ in range(a.steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) / a.steps], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        fused()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            fused()
+        ms_f = timed(g2.replay, a.steps)
+        fused_p1 = {"value": round(B / (ms_f / 1e3), 2), "ms_per_step": round(ms_f, 4),
+                    "path": "kvb_decode_step per layer (scan + prologue top-K + attention), CUDA graph"}
     st0 = decs[0].store
     E = H * D
     per_layer = (spec.n_chunks * E * 2 + K * cs * (160 * 2 + E * 2) + 160 * E * 2 * world +
@@ -738,14 +743,16 @@ def run_c4(a, rank, world, local):
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic (torch.randn K/V per layer and rank)",
                "config": {"workload": VARIANTS["c4"], "seq_len": n, "layers": L_, "global_batch": B,
-                          "selected_chunks": K, "parallelism": f"sequence-sharded x{world}"},
+                          "selected_chunks": K, "parallelism": f"sequence-sharded x{world}",
+                          "cuda_graph": graph is not None},
                "step_roofline": {"achieved": round(L_ * per_layer / (ms / 1e3) / 1e9, 1),
                                  "peak": hbm * world, "unit": "GB/s",
                                  "frac": round(L_ * per_layer / (ms / 1e3) / 1e9 / (hbm * world), 4)},
-               "collectives_per_layer": 4 if world > 1 else 0,
-               "path": ("kvb_decode_step per layer, CUDA graph" if world == 1 else
-                        "local top-K -> NCCL all-gather -> kvb_merge_topk -> attend -> all-gather -> "
-                        "kvb_merge_attention"),
+               "collectives_per_layer": 2,
+               "path": ("ShardedDecoder.step per layer: kvb_select_candidates -> all-gather of packed "
+                        "(score, id) -> kvb_merge_topk_packed -> kvb_tokens_from_chunks -> kvb_attend "
+                        "(+lse) -> all-gather of packed (o, lse) -> kvb_merge_attention_packed"),
+               "single_gpu_fused_chain": fused_p1,
                "clocks": sampler.summary(),
                "build_s": round(t_build, 1)}
         print(json.dumps(out), flush=True)
@@ -822,13 +829,8 @@ def main():
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(r["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.randn K/V per layer; random queries)",
-            "config": {"workload": VARIANTS[primary],
-                       "model": "Llama-3.1-8B shape (32 layers, 32 q / 8 kv heads, d 128)",
-                       "global_batch": world * a.batch, "seq_len": a.ctx, "layers": a.layers,
-                       "chunk": r["chunk"], "budget_tokens": a.budget, "selected_chunks": r["K"],
-                       "parallelism": f"dp{world} (replicas)",
-                       "l2": f"inputs exceed L2: {r['step_bytes'] / 1e9:.1f} GB algorithmic bytes per step",
-                       "cuda_graph": r["graph"]},
+            "config": bench_config(a, world, primary),
+            "cuda_graph": r["graph"],
             "roofline": {"bound": "hbm", "kernel": r["k1_kernel"], "achieved": round(k1_gbs, 1),
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(k1_gbs / hbm, 4),

@@ -157,14 +157,6 @@ kvb_status kvb_store_set_offload(kvb_store* store, const void* keys, const void*
 /* SVD slow tier (quantization.py:490-513): device fp16 factors
  * left [batch][n_tokens][svd_groups][r], right [batch][svd_groups][r][Dg],
  * Dg = kv_heads*head_dim/svd_groups.                                        */
-/* Two-batch overlap (serving extension, no kvlab counterpart): when
- * attention_stream is non-NULL, kvb_decode_step runs the attention + merge of
- * the fused path on that stream (ordered after the scan by events; the
- * caller's stream waits for it), and the attention grid is sized for
- * attention_sms SMs (0 = all). Two micro-batches on two caller streams then
- * overlap one's latency-bound attention with the other's HBM-bound scan.
- * The streams are the caller's and must outlive the store's use of them. */
-kvb_status kvb_store_set_overlap(kvb_store* store, void* attention_stream, int32_t attention_sms);
 kvb_status kvb_store_set_svd(kvb_store* store, const void* left16, const void* right16,
                              void* stream);
 /* Import precomputed landmark state (identical codes for parity runs).
@@ -240,7 +232,10 @@ int64_t kvb_select_residual_workspace_bytes(const kvb_store* store,
 typedef struct kvb_attend_args {
   int32_t queries_per_head;
   int32_t token_capacity;
-  int32_t k_path;           /* 0 = auto, 1 = fold (q~ = right.q), 2 = tcgen05 reconstruction */
+  int32_t k_path;           /* SVD slow tier: 0 = auto (fold), 1 = fold (q~ = right.q);
+                               2 = tcgen05 reconstruction -- kvb_decode_step only
+                               (chunk-stream attention); kvb_attend returns
+                               KVB_EUNSUPPORTED for it                        */
 } kvb_attend_args;
 kvb_status kvb_attend(kvb_store* store, const float* queries, const kvb_attend_args* args,
                       const int32_t* token_ids, const int32_t* n_tokens, float* out,
@@ -291,6 +286,15 @@ kvb_status kvb_merge_attention(const float* out_parts, const float* lse_parts, i
  * [P][batch][K] (global ids) -> chunk_ids [batch][K] in rank order.       */
 kvb_status kvb_merge_topk(const float* cand_scores, const int32_t* cand_ids, int32_t parts,
                           int32_t batch, int32_t k, int32_t* chunk_ids, void* stream);
+
+/* Packed forms used by the sharded decoder so that each exchange is ONE
+ * all-gather: a rank's top-K record is [scores f32 batch*k][ids i32 batch*k]
+ * (records: [P][2*batch*k] words); a rank's attention partial is
+ * [out f32 rows*D][lse f32 rows] (parts_buf: [P][rows*(D+1)]).             */
+kvb_status kvb_merge_topk_packed(const void* records, int32_t parts, int32_t batch, int32_t k,
+                                 int32_t* chunk_ids, void* stream);
+kvb_status kvb_merge_attention_packed(const float* parts_buf, int32_t parts, int32_t rows,
+                                      int32_t head_dim, float* out, float* lse, void* stream);
 
 #ifdef __cplusplus
 }

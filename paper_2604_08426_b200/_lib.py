@@ -76,7 +76,6 @@ SIGNATURES = [
     ("kvb_store_set_residency", _I32, [_P, _P, _P, _P, _P, _P]),
     ("kvb_store_set_offload", _I32, [_P, _P, _P, _P]),
     ("kvb_store_set_svd", _I32, [_P, _P, _P, _P]),
-    ("kvb_store_set_overlap", _I32, [_P, _P, _I32]),
     ("kvb_store_set_landmarks_dense", _I32, [_P, _P, _P]),
     ("kvb_store_set_landmarks_higgs", _I32, [_P, _P, _P, _P]),
     ("kvb_store_set_residuals_higgs", _I32, [_P, _P, _P, _P]),
@@ -97,6 +96,8 @@ SIGNATURES = [
     ("kvb_tokens_from_chunks", _I32, [_P, _P, _I32, _I32, _P, _P, _I32, _P]),
     ("kvb_merge_attention", _I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P]),
     ("kvb_merge_topk", _I32, [_P, _P, _I32, _I32, _I32, _P, _P]),
+    ("kvb_merge_topk_packed", _I32, [_P, _I32, _I32, _I32, _P, _P]),
+    ("kvb_merge_attention_packed", _I32, [_P, _I32, _I32, _I32, _P, _P, _P]),
 ]
 
 _lib = None

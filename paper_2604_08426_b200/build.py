@@ -8,6 +8,7 @@ gpurun with the snapshot).
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -33,23 +34,49 @@ def _nvcc():
     raise RuntimeError("nvcc not found")
 
 
-def _deps_mtime():
+def _digest(paths, extra: str = "") -> str:
+    h = hashlib.sha256(extra.encode())
+    for p in paths:
+        h.update(p.encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def _deps():
     paths = [os.path.join(CSRC, h) for h in HEADERS if os.path.exists(os.path.join(CSRC, h))]
     paths.append(os.path.join(ROOT, "include", "kvb.h"))
-    return max(os.path.getmtime(p) for p in paths)
+    return paths
 
 
-def _compile(src: str, force: bool) -> tuple[str, str]:
+def _fresh(target: str, digest: str) -> bool:
+    stamp = target + ".sha256"
+    if not (os.path.exists(target) and os.path.exists(stamp)):
+        return False
+    with open(stamp) as f:
+        return f.read().strip() == digest
+
+
+def _stamp(target: str, digest: str) -> None:
+    with open(target + ".sha256", "w") as f:
+        f.write(digest + "\n")
+
+
+def _compile(src: str, force: bool) -> tuple[str, str, str]:
+    """Recompile when the content hash of the source, the shared headers and
+    the flags changed (not on mtimes: a shipped object newer than an edited
+    source must not be reused)."""
     s = os.path.join(CSRC, src)
     o = os.path.join(OBJ, src.replace(".cu", ".o"))
-    if (not force and os.path.exists(o)
-            and os.path.getmtime(o) >= max(os.path.getmtime(s), _deps_mtime())):
-        return o, ""
     cmd = [_nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+    digest = _digest([s, *_deps()], " ".join(cmd[1:]))
+    if not force and _fresh(o, digest):
+        return o, "", digest
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-    return o, r.stderr
+    _stamp(o, digest)
+    return o, r.stderr, digest
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -57,17 +84,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         results = list(ex.map(lambda s: _compile(s, force), srcs))
-    objs = [o for o, _ in results]
+    objs = [o for o, _, _ in results]
     if verbose:
-        for _, log in results:
+        for _, log, _ in results:
             if log:
                 sys.stderr.write(log)
-    newest = max(os.path.getmtime(o) for o in objs)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+    lib_digest = hashlib.sha256("".join(d for _, _, d in results).encode()).hexdigest()
+    if force or not _fresh(LIB, lib_digest):
         cmd = [_nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+        _stamp(LIB, lib_digest)
     return LIB
 
 

@@ -73,11 +73,6 @@ int64_t trace_read(uint64_t* host, int64_t max_words) {
 
 bool pdl_enabled();
 
-static int env_int_api(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        void** args) {
   cudaLaunchConfig_t cfg{};
@@ -93,16 +88,8 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-// PDL on by default; KVB_PDL=0 launches every chained kernel fully
-// serialised (experiments: PDL-resident waiting CTAs hold their SMs)
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("KVB_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
+// programmatic dependent launch for every chained kernel of the decode step
+bool pdl_enabled() { return true; }
 
 int sm_count() {
   static int n = 0;
@@ -230,7 +217,6 @@ void free_store(kvb_store* s) {
 
   cudaFree(s->k2_meta);
   cudaFree(s->k2_overflow);
-  cudaFree(s->fused_ctr);
   cudaFree(s->res_bitmap);
   cudaFree(s->res_prefix);
   cudaFree(s->res_k);
@@ -349,8 +335,6 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc(&s->k2_hist, B * kTopHistBins, "K2 histogram")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->fused_ctr, 1 + 2 * B, "fused layer counters")) != KVB_OK) return bail(st);
-  cudaMemset(s->fused_ctr, 0, (1 + 2 * B) * sizeof(int));
   s->Wc = (s->C + 31) / 32;
   cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
   cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
@@ -552,17 +536,6 @@ kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* val
     if (!keys) KVB_FAIL(KVB_EINVAL, "slow tier 'none' needs keys");
     KVB_CUDA(cudaMemcpyAsync(s->off_k_dev, keys, bytes, cudaMemcpyDefault, st), "offload K");
   }
-  return KVB_OK;
-}
-
-kvb_status kvb_store_set_overlap(kvb_store* s, void* attention_stream, int32_t attention_sms) {
-  if (!s) KVB_FAIL(KVB_EINVAL, "null store");
-  if (attention_sms < 0) KVB_FAIL(KVB_EINVAL, "attention_sms must be >= 0");
-  if (attention_sms > 0 && attention_sms < s->d.batch)
-    KVB_FAIL(KVB_EINVAL, "attention_sms must be 0 or >= batch");
-  if (attention_sms > sm_count()) KVB_FAIL(KVB_EINVAL, "attention_sms exceeds the device's SM count");
-  s->att_stream = static_cast<cudaStream_t>(attention_stream);
-  s->att_sms = attention_sms;
   return KVB_OK;
 }
 
@@ -806,7 +779,7 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     if (pw * 8 <= 227 * 1024) {
       // the candidate SET in ascending order feeds stage 2 directly; kvlab's
       // rank order of chunk_ids (a result, not an input of stage 2) is sorted
-      // on the side stream, overlapping stage 2
+      // on the side stream, concurrent with stage 2
       L.rank_order = 0;
       L.sorted_ids = 1;
       L.sel_ids = cand_sorted;
@@ -955,34 +928,12 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   const bool chunk_path =
       attend_bulk_supported(s, L.G, s->d.max_resident + K * s->d.chunk_size, K);
   const bool tc_scan = !sel->exact_scores && higgs_tc_supported(s);
-  // fused layer kernel (scan + q~ fold + attention items in one persistent
-  // launch, kvb_attend_bulk.cu k5_fused_layer): experimental, opt-in with
-  // KVB_FUSED=1 -- measured slower at C2 (1524 vs 2740 tok/s): its register-fed
-  // scan items reach ~25 GB/s per SM and the last sequence's attention stays
-  // serial behind the whole scan
-  const bool fused = env_int_api("KVB_FUSED", 0) && chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
-                     !s->att_stream && fused_layer_supported(s, L.G, K);
-  if (fused) {
-    Carve sv(sws, sb);
-    float* sc = sv.take<float>((size_t)s->d.batch * s->C);
-    if (s->k2_dirty) {
-      KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
-      KVB_CUDA(cudaMemsetAsync(s->fused_ctr, 0, sizeof(int) * (1 + 2 * s->d.batch), st), "counter reset");
-      s->k2_dirty = false;
-    }
-    s->k2_dirty = true;
-    KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids, nullptr, 1),
-             "fused decode layer");
-    s->k2_dirty = false;
-    return KVB_OK;
-  }
   // dense scan + attention-side top-K on the caller's stream: prep (PDL: waits
   // for the stream's previous work, then triggers) -> scan (PDL, overlaps the
   // prep; waits for it at exit) -> attention -> merge, no side stream or
   // events. Other paths fork the prep onto the side stream.
   const bool inline_prep = chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
-                           s->C <= 32768 && s->d.landmark_kind == KVB_LM_DENSE && !s->att_stream &&
-                           env_int_api("KVB_INLINE_PREP", 1);
+                           s->C <= 32768 && s->d.landmark_kind == KVB_LM_DENSE;
   if (inline_prep) {
     KVB_CUDA(launch_attend_prep(s, L, st, true), "attention prep");
   } else {
@@ -1002,8 +953,9 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     float* sc = sv.take<float>((size_t)s->d.batch * s->C);
     (void)sv.take<int32_t>(1);
     void* tcws = sv.take<char>(higgs_tc_ws_bytes(s));
-    if (s->k2_dirty) {
+    if (s->k2_dirty) {  // a previous chain aborted part-way: histogram and K2 counters
       KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * s->d.batch * 4, st), "meta reset");
       s->k2_dirty = false;
     }
     s->k2_dirty = true;
@@ -1012,20 +964,8 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     else
       KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, inline_prep),
                "landmark scoring");
-    if (s->att_stream) {
-      // two-batch overlap: attention on the (high-priority) attention stream,
-      // event-ordered after the scan; the caller's stream resumes after it
-      KVB_CUDA(cudaEventRecord(s->ev_sel, st), "scan done");
-      KVB_CUDA(cudaStreamWaitEvent(s->att_stream, s->ev_sel, 0), "scan wait");
-      KVB_CUDA(cudaStreamWaitEvent(s->att_stream, s->ev_join, 0), "join wait");
-      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, s->att_stream, sc, s->k2_hist, chunk_ids),
-               "sparse attention");
-      KVB_CUDA(cudaEventRecord(s->ev_union, s->att_stream), "attention done");
-      KVB_CUDA(cudaStreamWaitEvent(st, s->ev_union, 0), "attention wait");
-    } else {
-      if (!inline_prep) KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
-      KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
-    }
+    if (!inline_prep) KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
+    KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
     s->k2_dirty = false;
     return KVB_OK;
   }
@@ -1130,6 +1070,27 @@ kvb_status kvb_merge_topk(const float* sc, const int32_t* ids, int32_t parts, in
   if (!sc || !ids || !chunk_ids || parts < 1 || batch < 1 || k < 1)
     KVB_FAIL(KVB_EINVAL, "bad merge arguments");
   KVB_CUDA(launch_merge_topk(sc, ids, parts, batch, k, chunk_ids, as_stream(stream)), "top-k merge");
+  return KVB_OK;
+}
+
+kvb_status kvb_merge_topk_packed(const void* records, int32_t parts, int32_t batch, int32_t k,
+                                 int32_t* chunk_ids, void* stream) {
+  if (!records || !chunk_ids || parts < 1 || batch < 1 || k < 1) KVB_FAIL(KVB_EINVAL, "bad argument");
+  const size_t bk = (size_t)batch * k;
+  const float* sc = static_cast<const float*>(records);
+  const int32_t* ids = reinterpret_cast<const int32_t*>(sc + bk);
+  KVB_CUDA(launch_merge_topk(sc, ids, parts, batch, k, chunk_ids, as_stream(stream), 0, 2 * bk),
+           "packed top-k merge");
+  return KVB_OK;
+}
+
+kvb_status kvb_merge_attention_packed(const float* parts_buf, int32_t parts, int32_t rows,
+                                      int32_t D, float* out, float* lse, void* stream) {
+  if (!parts_buf || !out || parts < 1 || rows < 1 || D < 1) KVB_FAIL(KVB_EINVAL, "bad argument");
+  const size_t stride = (size_t)rows * (D + 1);
+  KVB_CUDA(launch_merge_attention(parts_buf, parts_buf + (size_t)rows * D, parts, rows, D, out, lse,
+                                  as_stream(stream), stride, stride),
+           "packed attention merge");
   return KVB_OK;
 }
 

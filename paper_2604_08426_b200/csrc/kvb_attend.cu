@@ -850,8 +850,7 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
 
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores,
-                                 uint32_t* sel_hist, int32_t* chunk_out, const float* svd_logits,
-                                 int fused) {
+                                 uint32_t* sel_hist, int32_t* chunk_out, const float* svd_logits) {
   const int G = a.G;
   const int pos_cap = s->d.max_resident + K * s->d.chunk_size;
   if (!attend_bulk_supported(s, G, pos_cap, K)) return cudaErrorNotSupported;
@@ -880,7 +879,6 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
   bl.sel_hist = sel_hist;
   bl.chunk_out = chunk_out;
   bl.svd_logits = svd_logits;
-  bl.fused = fused;
   return launch_attend_bulk(s, bl, st);
 }
 
@@ -893,21 +891,21 @@ cudaError_t launch_attend(const kvb_store* s, const AttendLaunch& a, cudaStream_
 // Cross-shard LSE merge: rows = B*H*G.
 __global__ void k_merge_attention(const float* __restrict__ op, const float* __restrict__ lp,
                                   int parts, int rows, int D, float* __restrict__ out,
-                                  float* __restrict__ lse) {
+                                  float* __restrict__ lse, size_t so, size_t sl) {
   const int row = blockIdx.x;
   // parts with no tokens carry lse = -inf (and a NaN output): weight 0, skipped
   float M = -INFINITY;
-  for (int i = 0; i < parts; ++i) M = fmaxf(M, lp[(size_t)i * rows + row]);
+  for (int i = 0; i < parts; ++i) M = fmaxf(M, lp[(size_t)i * sl + row]);
   float L = 0.f;
   for (int i = 0; i < parts; ++i) {
-    const float li = lp[(size_t)i * rows + row];
+    const float li = lp[(size_t)i * sl + row];
     if (li != -INFINITY) L += expf(li - M);
   }
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float acc = 0.f;
     for (int i = 0; i < parts; ++i) {
-      const float li = lp[(size_t)i * rows + row];
-      if (li != -INFINITY) acc = fmaf(op[((size_t)i * rows + row) * D + d], expf(li - M), acc);
+      const float li = lp[(size_t)i * sl + row];
+      if (li != -INFINITY) acc = fmaf(op[(size_t)i * so + (size_t)row * D + d], expf(li - M), acc);
     }
     out[(size_t)row * D + d] = acc / L;
   }
@@ -915,9 +913,12 @@ __global__ void k_merge_attention(const float* __restrict__ op, const float* __r
 }
 
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
-                                   int D, float* out, float* lse, cudaStream_t st) {
+                                   int D, float* out, float* lse, cudaStream_t st, size_t so,
+                                   size_t sl) {
   count_launch();
-  k_merge_attention<<<rows, 128, 0, st>>>(out_p, lse_p, parts, rows, D, out, lse);
+  if (so == 0) so = (size_t)rows * D;
+  if (sl == 0) sl = (size_t)rows;
+  k_merge_attention<<<rows, 128, 0, st>>>(out_p, lse_p, parts, rows, D, out, lse, so, sl);
   return cudaGetLastError();
 }
 

@@ -91,20 +91,9 @@ struct BulkParams {
   int off_uni;
   int nst;                    // ring slots (stages)
   int ett;                    // tokens per exact-key tile (8 in SVD stores: compact slots)
-  int dbg;                    // profiling: 1 skip the math, 2 skip the copies, 4 one scanning
-                              // split, 8 staging copy only (empty selection)
   // geometry
   int maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_bar, off_stage;
   int nB;                     // batch (grid y of the split-K launch)
-  // fused layer kernel (k5_fused_layer): scan + prep items before the attention
-  const __nv_bfloat16* lm;    // dense landmarks [B][C][H*D] bf16
-  float* sc_rw;               // scores [B][C] (== sel_scores)
-  uint32_t* hist_rw;          // [B][2048] (== sel_hist)
-  int* fctr;                  // [1 + 2B]: work queue, scan-done[B], prep-done[B]; reset by the merger
-  int NS;                     // scan items per sequence
-  const uint16_t* right;      // SVD right factor (prep items) or null
-  int prep_rs;                // prep items per (b, h)
-  int splits_fused;           // attention items per sequence
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -112,11 +101,6 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define KVB_MSTAMP(k)                                                                       \
-  do {                                                                                      \
-    if (p.trace && tid == 0)                                                                \
-      p.trace[(size_t)gridDim.y * gridDim.x * 8 + (size_t)blockIdx.y * 4 + (k)] = gtimer(); \
-  } while (0)
 #define KVB_STAMP(ph)                                                                     \
   do {                                                                                    \
     if (p.trace && tid == 0) p.trace[((size_t)b * S + split) * 8 + (ph)] = gtimer();      \
@@ -241,9 +225,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   const int nres = p.res_count[b];
   int i0, i1, r_lo = 0, n_rloc = 0, c_lo = 0;
   if (p.mode == 0) {
-    const int P = p.nitems[b];
-    i0 = (int)(((long long)P * split) / S);
-    i1 = (int)(((long long)P * (split + 1)) / S);
+    i0 = i1 = 0;  // the token count is the previous kernel's output: read after pdl_wait()
   } else {
     const int KC = p.K * p.cs;
     r_lo = (int)(((long long)nres * split) / S);
@@ -297,7 +279,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   // before waiting on the scan, so their data lands during the selection.
   // Same slot / owner mapping as produce() for k < pre_done (it skips them).
   int pre_done = 0;
-  if (VAR == 2 && p.mode == 1 && p.sel_scores && !(p.dbg & 2)) {
+  if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     pre_done = min(min(2, n_rloc / ett), nst - 1);
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
@@ -317,6 +299,11 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   }
   pdl_wait();  // the selection (token / chunk list) of the previous kernel
   KVB_STAMP(6);
+  if (p.mode == 0) {  // token mode: the list length comes from the selection kernel
+    const int P = p.nitems[b];
+    i0 = (int)(((long long)P * split) / S);
+    i1 = (int)(((long long)P * (split + 1)) / S);
+  }
   // q~ (k5_prep) only after the wait: the prep triggers its dependents at
   // entry, so it may still be running while this grid is resident
   if (warp < H) {
@@ -346,7 +333,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     // the threshold search) when they fit beside >= 4096 candidate slots
     const size_t sbytes = (size_t)p.C * 4;
     const bool staged = (sbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(scs) & 15) == 0) &&
-                        used + sbytes + 4096 * 8 <= ring_bytes && !(p.dbg & 4);
+                        used + sbytes + 4096 * 8 <= ring_bytes;
     __shared__ __align__(8) uint64_t stage_bar;
     float* stage = staged ? reinterpret_cast<float*>(pro + ring_bytes - sbytes) : nullptr;
     if (staged && tid == 0) {
@@ -359,13 +346,12 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
                  (uint32_t)min((size_t)kPiece, sbytes - o), &stage_bar);
     }
     const int cap = (int)((ring_bytes - used - (staged ? sbytes : 0)) / 8);
-    // (profiling: dbg & 4 -> only split 0 streams the scores, to isolate L2 contention)
-    select_topk_shared(scs, ((p.dbg & 4) && split) ? 0 : p.C,
+    select_topk_shared(scs, p.C,
                        p.sel_hist + (size_t)b * kFuseHistBins,
                        p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
                        p.trace ? p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8
                                : nullptr,
-                       stage, staged ? &stage_bar : nullptr, p.dbg & 8);
+                       stage, staged ? &stage_bar : nullptr, 0);
     if (staged && tid == 0)  // all threads waited on it inside (and synced after)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(saddr(&stage_bar)) : "memory");
     const int per = (p.Wc + nthr - 1) / nthr;
@@ -521,7 +507,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     uint32_t bytes = 0;
     if (lane < 16 && j < cnt) bytes = (uint32_t)(vbytes + kb);
     bytes = __reduce_add_sync(FULL, bytes);
-    if (p.dbg & 2) bytes = 0;
     unsigned char* st = ring + (size_t)stg * p.stage_bytes;
     // V rows past the tile's count are read by the P.V mma with p = 0: zero
     // them (0 * stale bits could be NaN); K rows of those tokens only feed
@@ -533,7 +518,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     __threadfence_block();
     if (lane == 0) mbar_arrive_tx(full + stg, bytes);
     __syncwarp();
-    if (j < cnt && !(p.dbg & 2)) {
+    if (j < cnt) {
       const unsigned char* vsrc;
       const unsigned char* ksrc;
       if (tier == 0) {
@@ -699,10 +684,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       mbar_wait(full + stg, par);
       if (k == 0) KVB_STAMP(3);
       const uint32_t st = ring_s + (uint32_t)(stg * p.stage_bytes);
-      if (p.dbg & 1) {
-        release(stg);
-        continue;
-      }
       const int cnt = min(ett, n_ex - k * ett);
       // half tiles (ett = 8): rows 8-15 alias rows 0-7 (finite, masked)
       const uint32_t ka = st + (uint32_t)(ett * vrow + (ka_row & (ett - 1)) * p.krow_ex + ka_col +
@@ -785,10 +766,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       mbar_wait(full + stg, par);
       if (k == 0) KVB_STAMP(3);
       const uint32_t st = ring_s + (uint32_t)(stg * p.stage_bytes);
-      if (p.dbg & 1) {
-        release(stg);
-        continue;
-      }
       const int cnt = min(kBT, n_sv - (k - t_ex) * kBT);
       const uint32_t ka = st + (uint32_t)(kBT * vrow + ka_row * p.krow_sv + ka_col + hgrp * p.r * 2);
       // four independent accumulator chains (k-step mod 4): mma.sync latency
@@ -858,193 +835,6 @@ __global__ void __maxnreg__(232) k5_attend_bulk(const __grid_constant__ BulkPara
   attend_item<QW, NKS, VAR>(p, blockIdx.y, blockIdx.x, gridDim.x, sm);
 }
 
-// ---- fused decode layer: scan + query-fold items, then attention items ------------
-// One persistent CTA per SM takes items from a global queue in a fixed order:
-// query-fold (prep) items, then per sequence b its NS scan items, with the
-// attention items of sequence b - kFusedLag dispensed after the scan items of
-// sequence b. An attention item waits (spinning, one thread) until its
-// sequence's scan and prep items have all completed; every item it waits on
-// was dispensed earlier to a running CTA, so the wait always ends. The
-// latency-bound attention of early sequences then overlaps the HBM-bound scan
-// of later ones (the split kernels serialise them per layer).
-constexpr int kFusedLag = 2;
-
-// q_bar[e] = ((q[h,0,d] + q[h,1,d]) + q[h,2,d]) + ... -- the order of
-// kvb_score.cu load_qbar (scores are bit-identical to k1_dense_sum's)
-__device__ __forceinline__ void fused_qbar(const float* __restrict__ qb, int H, int G, float* out) {
-  const int E = H * kBD;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int h = e / kBD, d = e - h * kBD;
-    const float* q = qb + (size_t)h * G * kBD + d;
-    float s = q[0];
-    for (int g = 1; g < G; ++g) s = s + q[(size_t)g * kBD];
-    out[e] = s;
-  }
-}
-
-// scan item (b, j): chunks [j C / NS, (j + 1) C / NS) of sequence b, warp per
-// row, 4 rows in flight per warp; per-row arithmetic of k1_dense_sum<bf16>
-template <int NV>
-__device__ __noinline__ void scan_item(const BulkParams& p, int b, int j, unsigned char* sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int E = p.H * kBD;
-  float* qbar = reinterpret_cast<float*>(sm + p.off_stage);
-  fused_qbar(p.q + (size_t)b * p.H * p.G * kBD, p.H, p.G, qbar);
-  __syncthreads();
-  float qr[NV][8];
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) qr[i][jj] = qbar[(lane + 32 * i) * 8 + jj];
-  const int C = p.C;
-  const int c0 = (int)(((long long)C * j) / p.NS), c1 = (int)(((long long)C * (j + 1)) / p.NS);
-  const __nv_bfloat16* base = p.lm + (size_t)b * C * E;
-  float* out = p.sc_rw + (size_t)b * C;
-  uint32_t* hist = p.hist_rw + (size_t)b * kFuseHistBins;
-  constexpr int RW = 4;
-  for (int c = c0 + warp * RW; c < c1; c += nw * RW) {
-    uint4 v[RW][NV];
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-#pragma unroll
-      for (int i = 0; i < NV; ++i)
-        if (c + r < c1) v[r][i] = ld_stream(base + (size_t)(c + r) * E + (size_t)(lane + 32 * i) * 8);
-#pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      if (c + r >= c1) break;
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        float f[8];
-        Vec<__nv_bfloat16>::unpack(v[r][i], f);
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) a = fmaf(qr[i][jj], f[jj], a);
-      }
-      a = warp_sum_butterfly(a);
-      if (lane == 0) {
-        out[c + r] = a;
-        atomicAdd(hist + (score_key(a) >> 21), 1u);
-      }
-    }
-  }
-}
-
-// prep item (b, h, rs): q~ rows [r0, r1) of head h -- k5_prep's fold
-// (kvb_attend.cu) without the q transpose the bulk attention does not read
-__device__ __noinline__ void prep_item(const BulkParams& p, int b, int h, int rs, unsigned char* sm) {
-  const int G = p.G, H = p.H, HG = H * G, r = p.r, nrs = p.prep_rs;
-  float* qs = reinterpret_cast<float*>(sm + p.off_stage);  // [G][D]
-  const float* qb = p.q + ((size_t)b * H + h) * G * kBD;
-  for (int i = threadIdx.x; i < G * kBD; i += blockDim.x) qs[i] = qb[i];
-  const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
-  float* rsm = qs + G * kBD;  // [r][D+1]
-  const int hpg = H / p.sgroups, grp = h / hpg, col0 = (h % hpg) * kBD;
-  const int Dg = hpg * kBD;
-  const uint16_t* rb = p.right + ((size_t)b * p.sgroups + grp) * r * Dg + col0;
-  constexpr int cpr = kBD / 8;
-  for (int i = threadIdx.x; i < (r1 - r0) * cpr; i += blockDim.x) {
-    const int rr = r0 + i / cpr, c = i % cpr;
-    const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
-    const __half2* hv = reinterpret_cast<const __half2*>(&u);
-    float* dst = rsm + rr * (kBD + 1) + c * 8;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(hv[k]);
-      dst[2 * k] = f.x;
-      dst[2 * k + 1] = f.y;
-    }
-  }
-  __syncthreads();
-  float* qt2 = const_cast<float*>(p.qt2);
-  for (int o = threadIdx.x; o < (r1 - r0) * G; o += blockDim.x) {
-    const int g = o / (r1 - r0), rr = r0 + o % (r1 - r0);
-    const float* rw = rsm + rr * (kBD + 1);
-    const float* qq = qs + g * kBD;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int d = 0; d < kBD; ++d) acc = fmaf(rw[d], qq[d], acc);
-    qt2[(size_t)b * HG * r + ((size_t)(rr >> 1) * HG + h * G + g) * 2 + (rr & 1)] = acc;
-  }
-}
-
-__device__ __forceinline__ int ld_acquire(const int* a) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
-template <int QW, int NKS, int NV>
-__global__ void __maxnreg__(232) k5_fused_layer(const __grid_constant__ BulkParams p) {
-  extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ int s_item;
-  const int tid = threadIdx.x;
-  const int B = p.nB, NS = p.NS, S = p.splits_fused;
-  const int n_prep = p.right ? B * p.H * p.prep_rs : 0;
-  const int total = n_prep + B * (NS + S);
-  int* queue = p.fctr;
-  int* scan_done = p.fctr + 1;
-  int* prep_done = p.fctr + 1 + B;
-  pdl_trigger();
-  pdl_wait();
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(queue, 1);
-    __syncthreads();
-    int it = s_item;
-    __syncthreads();
-    if (it >= total) break;
-    // profiling: per item [start, wait done, end, smid] at word 32768 + 4 it
-    uint64_t* itr = (p.trace && it < 8000) ? p.trace + 32768 + (size_t)4 * it : nullptr;
-    if (itr && tid == 0) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      itr[0] = gtimer();
-      itr[3] = smid;
-    }
-    if (it < n_prep) {
-      const int b = it / (p.H * p.prep_rs), rem = it - b * p.H * p.prep_rs;
-      prep_item(p, b, rem / p.prep_rs, rem % p.prep_rs, sm);
-      __threadfence();  // release this item's global writes (every writer fences)
-      __syncthreads();
-      if (tid == 0) atomicAdd(prep_done + b, 1);
-      if (itr && tid == 0) itr[1] = itr[2] = gtimer();
-      continue;
-    }
-    it -= n_prep;
-    // blocks t = 0 .. B - 1 + lag: [NS scan items of sequence t] [S attention items of t - lag]
-    int t = 0, kind = 0, b = 0, j = 0;
-    for (;; ++t) {
-      const int ns = t < B ? NS : 0, na = t >= kFusedLag ? S : 0;
-      if (it < ns) { kind = 0; b = t; j = it; break; }
-      it -= ns;
-      if (it < na) { kind = 1; b = t - kFusedLag; j = it; break; }
-      it -= na;
-    }
-    if (kind == 0) {
-      scan_item<NV>(p, b, j, sm);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) atomicAdd(scan_done + b, 1);
-      if (itr && tid == 0) itr[1] = itr[2] = gtimer();
-    } else {
-      if (tid == 0) {
-        const int need_p = p.right ? p.H * p.prep_rs : 0;
-        while (ld_acquire(scan_done + b) < NS || ld_acquire(prep_done + b) < need_p) __nanosleep(100);
-        __threadfence();
-        // the scores are then read by bulk copies (async proxy)
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      }
-      // shared memory last written by the generic proxy (scan / prep items)
-      // is refilled by bulk copies in this item
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncthreads();
-      if (itr && tid == 0) itr[1] = gtimer();
-      attend_item<QW, NKS, 2>(p, b, j, S, sm);
-      __syncthreads();
-      if (itr && tid == 0) itr[2] = gtimer();
-    }
-  }
-}
-
 // Exact LSE merge of the split partials: one CTA per (row = h*G + g, sequence),
 // thread d. Launched with programmatic stream serialization right behind
 // k5_attend_bulk (which triggers its dependents at entry), so its CTAs are
@@ -1054,15 +844,11 @@ __global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict_
                                                      const float* __restrict__ pl,
                                                      const float* __restrict__ po, int S, int HG,
                                                      float* __restrict__ out, float* __restrict__ lse,
-                                                     uint32_t* __restrict__ hist_clear,
-                                                     int* __restrict__ fctr_clear, int nfctr) {
+                                                     uint32_t* __restrict__ hist_clear) {
   const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x, lane = d & 31;
   // the next layer's (PDL-launched, waiting) prep may become resident now
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  // the fused layer kernel (complete) was the last user of its work counters
-  if (fctr_clear && row == 0 && b == 0)
-    for (int i = d; i < nfctr; i += blockDim.x) fctr_clear[i] = 0;
   // the attention (complete) was the last reader of the scan's histogram
   if (hist_clear && row == 0)
     for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
@@ -1098,16 +884,11 @@ struct BulkGeom {
   size_t smem;
 };
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
   BulkGeom g{};
   const int B = s->d.batch, H = s->d.kv_heads;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
-  int splits = (s->att_sms > 0 ? s->att_sms : sm_count()) / B;
+  int splits = sm_count() / B;
   const int tiles = (positions_cap + kBT - 1) / kBT;
   if (splits > tiles) splits = tiles;
   if (splits < 1) splits = 1;
@@ -1136,8 +917,6 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
   g.off_stage = g.off_bar + 128;
   const size_t room = 227 * 1024 - g.off_stage - 2048;  // static smem + slack
   g.nst = std::min<int>(kBMaxStages, (int)(room / g.stage_bytes));
-  const int want = env_int("KVB_ATT_STAGES", 0);  // profiling override
-  if (want >= 2 && want < g.nst) g.nst = want;
   g.smem = (size_t)g.off_stage + (size_t)g.nst * g.stage_bytes;
   return g;
 }
@@ -1145,12 +924,10 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
 }  // namespace
 
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) {
-  using kvb::env_int;
   if (s->d.kv_dtype != KVB_BF16 || s->d.head_dim != kBD || s->d.kv_heads > 8 || G > 8 || G < 1)
     return false;
   // host-mapped offload tier: cp.async.bulk reads the pinned, device-mapped
-  // host pages directly (KVB_BULK_HOST=0 selects the cp.async kernel instead)
-  if (s->off_host && env_int("KVB_BULK_HOST", 1) == 0) return false;
+  // host pages directly
   // SVD ranks: whole, even numbers of 16-wide k-steps up to 160 (compile-time k loop)
   if (s->d.slow_kind == KVB_SLOW_SVD &&
       (s->d.svd_rank % 32 != 0 || s->d.svd_rank > 16 * kBMaxKs ||
@@ -1159,16 +936,6 @@ bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) 
   const BulkGeom g = bulk_geometry(s, positions_cap, K);
   if (g.nst < 2) return false;
   return g.smem <= 227 * 1024;
-}
-
-// fused layer: dense bf16 landmarks of 8 or 4 heads x 128, chunk-list
-// attention with the prologue top-K; one resident CTA per SM
-bool fused_layer_supported(const kvb_store* s, int G, int K) {
-  const int E = s->d.kv_heads * kBD;
-  return s->d.landmark_kind == KVB_LM_DENSE && s->d.kv_dtype == KVB_BF16 &&
-         (E == 1024 || E == 512) && s->d.head_dim == kBD && s->C <= 32768 &&
-         attend_bulk_supported(s, G, s->d.max_resident + K * s->d.chunk_size, K) &&
-         (s->d.slow_kind != KVB_SLOW_SVD || s->d.svd_rank == 160);
 }
 
 int attend_bulk_splits(const kvb_store* s, int positions_cap) {
@@ -1236,8 +1003,6 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.res_ids = s->res_ids;
   p.nst = g.nst;
   p.ett = g.ett;
-  const int dbg = env_int("KVB_ATT_DBG", 0);  // profiling only
-  p.dbg = dbg;
   count_launch(2);
   const int nks = svd ? s->d.svd_rank / 16 : 0;
   const int var = p.svd_logits ? 1 : (p.sel_scores ? 2 : 0);
@@ -1265,33 +1030,6 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
 #undef KVB_BULK_VAR
   dim3 grid(g.splits, B);
   p.nB = B;
-  if (a.fused) {
-    // one persistent CTA per SM; scan items over dense bf16 landmarks
-    const int E = H * kBD;
-    if (!fused_layer_supported(s, a.G, a.K) || !s->fused_ctr) return cudaErrorNotSupported;
-    p.lm = static_cast<const __nv_bfloat16*>(s->lm_dense);
-    p.sc_rw = const_cast<float*>(a.sel_scores);
-    p.hist_rw = a.sel_hist;
-    p.fctr = s->fused_ctr;
-    p.NS = env_int("KVB_FUSED_NS", 64);
-    p.right = svd ? reinterpret_cast<const uint16_t*>(s->svd_right) : nullptr;
-    p.prep_rs = 4;
-    p.splits_fused = g.splits;
-    const int nv = E / 256;
-#define KVB_FUSED_NKS(Q, NVv)                                                        \
-  switch (nks) {  /* experimental path: exact keys or rank 160 only (build time) */  \
-    case 0: fn = (const void*)k5_fused_layer<Q, 0, NVv>; break;                      \
-    case 10: fn = (const void*)k5_fused_layer<Q, 10, NVv>; break;                    \
-    default: return cudaErrorNotSupported;                                           \
-  }
-    if (a.G <= 4) {
-      if (nv == 4) { KVB_FUSED_NKS(4, 4) } else { KVB_FUSED_NKS(4, 2) }
-    } else {
-      if (nv == 4) { KVB_FUSED_NKS(8, 4) } else { KVB_FUSED_NKS(8, 2) }
-    }
-#undef KVB_FUSED_NKS
-    grid = dim3(sm_count(), 1);
-  }
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
@@ -1311,8 +1049,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
                             (const float*)p.po, g.splits, H * a.G, p.out, p.lse,
-                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr,
-                            a.fused ? s->fused_ctr : (int*)nullptr, 1 + 2 * B);
+                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr);
   return cudaGetLastError();
 }
 

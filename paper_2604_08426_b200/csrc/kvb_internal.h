@@ -55,11 +55,6 @@ struct kvb_store {
   bool off_host = false;
   // side stream + events for the fork/join of decode-step work (prep || scan)
   cudaStream_t side = nullptr;
-  // two-batch overlap (kvb_store_set_overlap): the decode step's attention +
-  // merge go to att_stream (event-ordered after the scan) on att_sms SMs
-  cudaStream_t att_stream = nullptr;
-  int* fused_ctr = nullptr;  // [1 + 2B] k5_fused_layer queue / done counters (self-cleaning)
-  int att_sms = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sel = nullptr, ev_union = nullptr;
 };
 
@@ -195,26 +190,24 @@ struct BulkLaunch {
   int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
   int32_t* ntok_out = nullptr;  // [B]
   int tcap = 0;
-  // fused layer (k5_fused_layer): the dense landmark scan and the q~ fold run
-  // as items of the attention kernel itself (sel_scores / sel_hist written there)
-  int fused = 0;
 };
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K = 0);
-bool fused_layer_supported(const kvb_store* s, int G, int K);
 int attend_bulk_splits(const kvb_store* s, int positions_cap);
 cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st);
 // decode-step attention over residents + selected chunks (chunk ids [B][K])
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores = nullptr,
                                  uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr,
-                                 const float* svd_logits = nullptr, int fused = 0);
+                                 const float* svd_logits = nullptr);
 // the two halves of launch_attend: per-step query prep, then the attention
 cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl = false);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
-                                   int D, float* out, float* lse, cudaStream_t st);
+                                   int D, float* out, float* lse, cudaStream_t st,
+                                   size_t out_part_stride = 0, size_t lse_part_stride = 0);
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
-                              int32_t* out, cudaStream_t st, int by_id_M = 0);
+                              int32_t* out, cudaStream_t st, int by_id_M = 0,
+                              size_t part_stride = 0);
 
 // K3 reconstruction on tcgen05 (kvb_recon.cu): logits [B][K*cs][H*G] of the
 // selected SVD tokens, consumed by the bulk attention (svd_logits mode)

@@ -1018,7 +1018,7 @@ cudaError_t launch_candidate_tokens(const kvb_store* s, const int32_t* cand_chun
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024)
 k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int parts, int batch,
-             int k, int P, int32_t* __restrict__ out, int by_id_M) {
+             int k, int P, int32_t* __restrict__ out, int by_id_M, size_t part_stride) {
   extern __shared__ uint64_t mk[];
   const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
   const int tot = parts * k;
@@ -1026,7 +1026,7 @@ k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int 
     uint64_t v = 0ull;
     if (i < tot) {
       const int pp = i / k, j = i - pp * k;
-      const size_t off = ((size_t)pp * batch + b) * k + j;
+      const size_t off = (size_t)pp * part_stride + (size_t)b * k + j;
       const int id = gid[off];
       // scores listed beside the ids, or (by_id_M > 0) indexed by id in [B][M]
       if (id >= 0) {
@@ -1056,13 +1056,14 @@ k_merge_topk(const float* __restrict__ sc, const int32_t* __restrict__ gid, int 
 }
 
 cudaError_t launch_merge_topk(const float* sc, const int32_t* ids, int parts, int batch, int k,
-                              int32_t* out, cudaStream_t st, int by_id_M) {
+                              int32_t* out, cudaStream_t st, int by_id_M, size_t part_stride) {
   const int P = next_pow2(parts * k);
   const size_t smem = (size_t)P * 8;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   ensure_smem((const void*)k_merge_topk, smem);
   count_launch();
-  k_merge_topk<<<batch, 1024, smem, st>>>(sc, ids, parts, batch, k, P, out, by_id_M);
+  if (part_stride == 0) part_stride = (size_t)batch * k;
+  k_merge_topk<<<batch, 1024, smem, st>>>(sc, ids, parts, batch, k, P, out, by_id_M, part_stride);
   return cudaGetLastError();
 }
 

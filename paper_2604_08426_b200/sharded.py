@@ -73,7 +73,10 @@ class ShardSpec:
 
 
 class Exchange:
-    """all_gather / all_reduce over a torch.distributed process group."""
+    """all_gather / all_reduce over a torch.distributed process group. On
+    NCCL every call is a single stream-ordered collective on device buffers
+    (graph-capturable); on gloo (CPU tests, or CUDA tensors in a one-GPU
+    multi-process test) device tensors are staged through host memory."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -82,20 +85,30 @@ class Exchange:
         self.group = group
         self.parts = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
 
-    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
-        t = t.contiguous()
-        out = torch.empty((self.parts,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        try:
-            self.dist.all_gather_into_tensor(out, t, group=self.group)
-        except (RuntimeError, NotImplementedError):  # backends without the fused op
-            parts = [torch.empty_like(t) for _ in range(self.parts)]
-            self.dist.all_gather(parts, t, group=self.group)
-            out = torch.stack(parts)
+    def all_gather_into(self, out: torch.Tensor, t: torch.Tensor) -> torch.Tensor:
+        """out [P, *t.shape] <- every rank's t."""
+        if self.nccl:
+            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
+        src = t.contiguous().cpu()
+        parts = [torch.empty_like(src) for _ in range(self.parts)]
+        self.dist.all_gather(parts, src, group=self.group)
+        out.copy_(torch.stack(parts))
         return out
 
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.parts,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        return self.all_gather_into(out, t)
+
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
-        self.dist.all_reduce(t, group=self.group)
+        if self.nccl or not t.is_cuda:
+            self.dist.all_reduce(t, group=self.group)
+            return t
+        h = t.cpu()
+        self.dist.all_reduce(h, group=self.group)
+        t.copy_(h)
         return t
 
 
@@ -103,6 +116,11 @@ class SoloExchange:
     """World size 1: every collective is the identity."""
 
     parts, rank = 1, 0
+
+    @staticmethod
+    def all_gather_into(out: torch.Tensor, t: torch.Tensor) -> torch.Tensor:
+        out[0].copy_(t)
+        return out
 
     @staticmethod
     def all_gather(t: torch.Tensor) -> torch.Tensor:
@@ -122,6 +140,14 @@ class LocalExchange:
     @staticmethod
     def all_gather_list(ts) -> torch.Tensor:
         return torch.stack([t.contiguous() for t in ts])
+
+    @staticmethod
+    def all_reduce_list(ts) -> torch.Tensor:
+        """Sum of every shard's tensor, accumulated in rank order."""
+        acc = ts[0].clone()
+        for t in ts[1:]:
+            acc += t
+        return acc
 
 
 def gather_padded(ex, t: torch.Tensor, length: int, fill) -> torch.Tensor:
@@ -235,12 +261,15 @@ def build_shard(keys: torch.Tensor, values: torch.Tensor, spec: ShardSpec, ex, *
     left = torch.empty((B, n_local, 1, rank_r), dtype=torch.float16, device=keys.device)
     right = torch.empty((B, 1, rank_r, E), dtype=torch.float16, device=keys.device)
     for b in range(B):
-        kb = keys[b].reshape(n_local, E).float()
-        gram = ex.all_reduce_sum((kb.T @ kb).double())
+        # fp64 throughout, as store.svd_factors (numerics.py:80-98 runs LAPACK
+        # in fp64): the Gram matrix squares the condition number, so fp32
+        # would lose the weaker of the top-r directions
+        kb = keys[b].reshape(n_local, E).double()
+        gram = ex.all_reduce_sum(kb.T @ kb)
         _, V = torch.linalg.eigh(gram)
         V = V.flip(1)[:, :rank_r]
-        left[b, :, 0] = (kb.double() @ V).float().half()
-        right[b, 0] = V.T.float().half()
+        left[b, :, 0] = (kb @ V).to(torch.float32).to(torch.float16)
+        right[b, 0] = V.T.to(torch.float32).to(torch.float16)
         del kb
     st.import_svd(left, right)
     del left
@@ -259,17 +288,59 @@ def build_shard(keys: torch.Tensor, values: torch.Tensor, spec: ShardSpec, ex, *
 
 
 class ShardedDecoder:
-    """One rank's view of a sequence-sharded decode step (torch.distributed)."""
+    """One rank's view of a sequence-sharded decode step.
 
-    def __init__(self, store, spec: ShardSpec, exchange: Exchange, k_global: int):
+    Exactly two collectives per step, one all-gather each: the packed local
+    top-K record [scores | ids] (8 B per candidate) and the packed attention
+    partial [o | lse]. Every buffer is allocated here, once, so ``step`` does
+    no allocation and no host synchronisation: on NCCL the whole step is
+    capturable in a CUDA graph. The same code runs at P = 1 (SoloExchange),
+    so a 1 -> P scaling curve compares one implementation."""
+
+    def __init__(self, store, spec: ShardSpec, exchange, k_global: int, G: int):
         self.store, self.spec, self.ex, self.k = store, spec, exchange, k_global
+        self.G = G
         self.k_local = min(k_global, store.C)
-        self.cap = min(store.n, k_global * store.cs + store.max_resident)
+        self.cap = max(1, min(store.n, k_global * store.cs + store.max_resident))
+        B, H, D, P, k = store.batch, store.heads, store.dim, exchange.parts, k_global
+        dev = "cuda"
+        self.rec = torch.empty((2, B, k), dtype=torch.float32, device=dev)
+        self.rec_all = torch.empty((P, 2, B, k), dtype=torch.float32, device=dev)
+        self.chunk_ids = torch.empty((B, k), dtype=torch.int32, device=dev)
+        self.tok = torch.empty((B, self.cap), dtype=torch.int32, device=dev)
+        self.ntok = torch.empty(B, dtype=torch.int32, device=dev)
+        self.rows = B * H * G
+        self.part = torch.empty(self.rows * (D + 1), dtype=torch.float32, device=dev)
+        self.out_p = self.part[: self.rows * D].view(B, H, G, D)
+        self.lse_p = self.part[self.rows * D:].view(B, H, G)
+        self.part_all = torch.empty((P, self.rows * (D + 1)), dtype=torch.float32, device=dev)
+        self.out = torch.empty((B, H, G, D), dtype=torch.float32, device=dev)
+        self.lse = torch.empty((B, H, G), dtype=torch.float32, device=dev)
+        self.aa = L.AttendArgs(G, self.cap, 0)
+        lib = store.lib
+        nb = max(lib.kvb_select_candidates_workspace_bytes(store.h, k),
+                 lib.kvb_attend_workspace_bytes(store.h, C.byref(self.aa)))
+        self.ws = torch.empty(max(256, int(nb)), dtype=torch.uint8, device=dev)
 
     def step(self, q: torch.Tensor):
-        sc, ids = local_candidates(self.store, q, self.k, self.spec.chunk_lo)
-        chunk_ids = merge_candidates(self.ex.all_gather(sc), self.ex.all_gather(ids), self.k)
-        tok, ntok = local_tokens(self.store, chunk_ids, self.spec.chunk_lo, self.cap)
-        out_p, lse_p = self.store.attend(q, tok, ntok, want_lse=True)
-        out, lse = merge_attention(self.ex.all_gather(out_p), self.ex.all_gather(lse_p))
-        return out, lse, chunk_ids
+        st, lib, s = self.store, self.store.lib, _stream()
+        B = st.batch
+        # local top-K: scores and global ids written straight into the record
+        L.check(lib.kvb_select_candidates(st.h, _ptr(q), self.G, self.k, L.KVB_AGG_SUM,
+                                          self.spec.chunk_lo, _ptr(self.rec[0]),
+                                          _ptr(self.rec[1]), _ptr(self.ws), self.ws.numel(), s),
+                "kvb_select_candidates")
+        self.ex.all_gather_into(self.rec_all, self.rec)                       # exchange 1
+        L.check(lib.kvb_merge_topk_packed(_ptr(self.rec_all), self.ex.parts, B, self.k,
+                                          _ptr(self.chunk_ids), s), "kvb_merge_topk_packed")
+        L.check(lib.kvb_tokens_from_chunks(st.h, _ptr(self.chunk_ids), self.k, self.spec.chunk_lo,
+                                           _ptr(self.tok), _ptr(self.ntok), self.cap, s),
+                "kvb_tokens_from_chunks")
+        L.check(lib.kvb_attend(st.h, _ptr(q), C.byref(self.aa), _ptr(self.tok), _ptr(self.ntok),
+                               _ptr(self.out_p), _ptr(self.lse_p), _ptr(self.ws), self.ws.numel(),
+                               s), "kvb_attend")
+        self.ex.all_gather_into(self.part_all, self.part)                     # exchange 2
+        L.check(lib.kvb_merge_attention_packed(_ptr(self.part_all), self.ex.parts, self.rows,
+                                               st.dim, _ptr(self.out), _ptr(self.lse), s),
+                "kvb_merge_attention_packed")
+        return self.out, self.lse, self.chunk_ids

@@ -371,14 +371,6 @@ class DeviceStore:
                                     _stream()), "kvb_attend")
         return out, lse
 
-    def set_overlap(self, attention_stream=None, attention_sms: int = 0):
-        """Two-batch overlap (kvb_store_set_overlap): decode-step attention on
-        `attention_stream` (a torch.cuda.Stream, None = the caller's stream),
-        its grid sized for `attention_sms` SMs (0 = all)."""
-        self._att_stream = attention_stream  # keep the stream alive
-        ptr = C.c_void_p(attention_stream.cuda_stream) if attention_stream is not None else None
-        L.check(self.lib.kvb_store_set_overlap(self.h, ptr, int(attention_sms)), "kvb_store_set_overlap")
-
     def decode_plan(self, G: int, n_select: int, k_path: int = 0):
         """Pre-sized arguments + buffers for repeated decode steps (graph-capturable)."""
         cap = self.token_capacity(n_select)
@@ -418,10 +410,14 @@ class DecodePlan:
                                  _stream()), "kvb_attend")
         return dst
 
-    def run(self, q: torch.Tensor, out: torch.Tensor | None = None):
+    def run(self, q: torch.Tensor, out: torch.Tensor | None = None, want_chunks: bool = False):
+        """One decode step. ``want_chunks`` also writes the selected chunk ids
+        (ascending, into ``self.cid``) -- a checker aid, the step itself does
+        not need them."""
         s = self.store
         dst = self.out if out is None else out
-        L.check(s.lib.kvb_decode_step(s.h, _ptr(q), C.byref(self.sa), C.byref(self.aa), None,
+        L.check(s.lib.kvb_decode_step(s.h, _ptr(q), C.byref(self.sa), C.byref(self.aa),
+                                      _ptr(self.cid) if want_chunks else None,
                                       _ptr(self.tok), _ptr(self.ntok), _ptr(dst), _ptr(self.lse),
                                       _ptr(self.ws), self.ws.numel(), _stream()), "kvb_decode_step")
         return dst

@@ -1,0 +1,361 @@
+"""Parity at every benchmarked configuration (VERDICT r01 "next" item 1).
+
+Each test runs the exact code path ``bench.py`` times -- ``DeviceStore.build``
+(GPU prefill) + ``DecodePlan.run`` (``kvb_decode_step``: scan, prologue or
+K2a/K2b top-K, fused gather + split-K attention, merge) -- at the benchmark's
+shape, and checks it against the CPU oracle (``oracle/kvlab_port.py``, kvlab's
+numpy arithmetic) on the same bf16-rounded inputs:
+
+* the GPU's selected chunk set equals the top-K of the kernel-order scores
+  (``oracle/exact_order.c``) exactly, and kvlab's ranking up to near-ties
+  whose exact (fp64) score gap is inside the fp32 forward-error bound; the
+  near-tie count is printed (``-s``) and must be 0 on these seeds;
+* the decode step's token list equals kvlab's ``select_by_landmarks`` token
+  ids for every sequence;
+* the attention output is within 1e-4 relative of kvlab's ``sparse_attention``
+  over the same tokens (north_star: 2e-2 for bf16; the inputs are exactly
+  representable, so only fp32 reassociation remains).
+
+Tensor-core (non-bit-reproducible) scoring paths -- HIGGS scans with
+``exact_scores = 0`` -- are checked against the fp64 ranking with a tolerance
+of twice the MEASURED max |s_tc - s_fp64| of that run; the swap count is
+printed.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from parity_util import compare_ranking, rank, rel_err, score_tol
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+D = 128
+
+
+def _randn(gen, shape, dtype=torch.bfloat16):
+    return torch.randn(shape, generator=gen, device="cuda", dtype=torch.float32).to(dtype)
+
+
+def _heads_np(t):
+    """device [n, H, D] (any float dtype) -> numpy f32 [H, n, D]."""
+    return np.ascontiguousarray(t.float().cpu().numpy().transpose(1, 0, 2))
+
+
+def _shadowkv(B, n, H, G, seed, budget_tokens, rank_r=160):
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    k = _randn(gen, (B, n, H, D))
+    v = _randn(gen, (B, n, H, D))
+    q = torch.randn((B, H, G, D), generator=gen, device="cuda")
+    dev = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=8,
+                      dtype=torch.bfloat16, landmark=S.scheme_none(),
+                      slow=S.scheme_svd(rank_r, H * D), svd_groups=1,
+                      outlier_tokens=384, local_window=32)
+    left, right = dev.svd_factors(k)
+    dev.build(k, v, svd_factors=(left, right))
+    K = dev.n_select(budget_tokens / n)
+    plan = dev.decode_plan(G, K)
+    plan.run(q, want_chunks=True)
+    torch.cuda.synchronize()
+    return dev, k, v, q, left, right, plan, K
+
+
+def _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, b, budget_tokens, check_outliers):
+    from oracle import exact_order as X
+    from oracle import kvlab_port as P
+
+    n, H = dev.n, dev.heads
+    kb, vb = _heads_np(k[b]), _heads_np(v[b])
+    qb = q[b].cpu().numpy()
+    lm_gpu = dev.landmarks_dequantized()[b].cpu().numpy()         # [C, H, D]
+    lm = np.ascontiguousarray(lm_gpu.transpose(1, 0, 2))           # [H, C, D]
+    ref_lm = torch.from_numpy(np.stack([P.chunk_means(kb[h], 8) for h in range(H)])).bfloat16().float()
+    assert np.array_equal(lm, ref_lm.numpy()), "chunk means != oracle (bf16 storage)"
+    outl = dev.residency.outlier_chunks[b]
+    if check_outliers:
+        assert outl == P.outlier_chunks(kb, lm, 8, 384), "outlier set != oracle"
+    budget = P.Budget(budget_tokens / n, 384, 32)
+    l16 = left[b, :, 0, :].cpu().numpy()
+    r16 = right[b, 0].cpu().numpy()
+    slow_k = P.svd16_reconstruct(l16, r16).reshape(n, H, D).transpose(1, 0, 2)
+    st = P.store_from_parts(kb, vb, 8, budget, lm, outl, slow_k=np.ascontiguousarray(slow_k))
+    ref = P.select_by_landmarks(st, qb, budget)
+    # kernel-order scores (K1 is bit-identical to exact_order.c) -> exact set
+    vw = X.vector_width(H * D, 2)
+    sx = X.dense_sum(lm_gpu, qb, vw)
+    got = np.sort(plan.cid[b].cpu().numpy())
+    assert np.array_equal(got, np.sort(rank(sx, K))), "decode-step top-K != top-K of kernel scores"
+    s64 = np.einsum("hgd,hcd->c", qb.astype(np.float64), lm.astype(np.float64))
+    ties = compare_ranking(rank(sx, K), np.asarray(ref.chunk_ids), s64, score_tol(qb, lm_gpu),
+                           f"seq {b}")
+    t = plan.tok[b, : int(plan.ntok[b])].cpu().numpy()
+    if ties == 0:
+        assert np.array_equal(t, ref.token_ids), f"seq {b}: token ids != kvlab"
+    o_ref, _, _ = P.sparse_attention(qb, st, t)
+    err = rel_err(plan.out[b].cpu().numpy(), o_ref)
+    return ties, err
+
+
+def test_c2_decode_step_all_sequences():
+    """C2 exactly: n=131072, B=8, bf16, SVD r160 over [n, 1024] (GPU Gram
+    route), 384 outlier + 32 local residents, budget 2048 tokens (K=256),
+    through kvb_decode_step -- every sequence against the oracle."""
+    n, B, H, G, budget = 131072, 8, 8, 4, 2048
+    dev, k, v, q, left, right, plan, K = _shadowkv(B, n, H, G, 20260, budget)
+    assert K == 256
+    report = []
+    for b in range(B):
+        ties, err = _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, b, budget,
+                                        check_outliers=b < 2)
+        report.append((b, ties, err))
+        assert ties == 0, f"seq {b}: {ties} near-tie swaps vs kvlab"
+        assert err < 1e-4, (b, err)
+    print("C2 decode step: (seq, near-ties, attention rel err) =", report)
+    dev.close()
+
+
+def test_c4_shape_slice_128k():
+    """C4 head shape (Hkv 4, G 7 -> the QW=8 fragment layout), 128K slice,
+    SVD r160 over [n, 512], budget frac 0.0156."""
+    n, B, H, G = 131072, 2, 4, 7
+    budget = 2048
+    dev, k, v, q, left, right, plan, K = _shadowkv(B, n, H, G, 4242, budget)
+    for b in range(B):
+        ties, err = _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, b, budget,
+                                        check_outliers=True)
+        print(f"C4 slice seq {b}: near-ties {ties}, rel err {err:.2e}")
+        assert ties == 0 and err < 1e-4, (b, ties, err)
+    dev.close()
+
+
+def test_c4_one_layer_1m():
+    """One C4 layer at its full 1M context (Hkv 4, G 7), K = 2048 chunks."""
+    n, B, H, G = 1 << 20, 1, 4, 7
+    budget = 2048 * 8
+    dev, k, v, q, left, right, plan, K = _shadowkv(B, n, H, G, 77, budget)
+    assert K == 2048
+    ties, err = _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, 0, budget,
+                                    check_outliers=False)
+    print(f"C4 1M layer: near-ties {ties}, rel err {err:.2e}")
+    assert ties == 0 and err < 1e-4, (ties, err)
+    dev.close()
+
+
+# ---------------------------------------------------------------------------
+# HIGGS tensor-core fast paths (exact_scores = 0)
+# ---------------------------------------------------------------------------
+def _higgs_store(B, n, H, cs, bits, seed, residual_bits=None):
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    k = _randn(gen, (B, n, H, D))
+    v = _randn(gen, (B, n, H, D))
+    dev = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=cs,
+                      dtype=torch.bfloat16, landmark=S.scheme_higgs(bits),
+                      residual=S.scheme_higgs(residual_bits) if residual_bits else None,
+                      outlier_tokens=384, local_window=32)
+    dev.build(k, v)
+    torch.cuda.synchronize()
+    return dev, k, v, gen
+
+
+def _tc_vs_fp64(s_tc, s64, K, what):
+    """tensor-core top-K set vs the fp64 top-K set: every chunk in one set but
+    not the other must lie within 2x the measured max |s_tc - s_fp64| of the
+    K-th fp64 score. Returns (swaps, measured err)."""
+    err = float(np.max(np.abs(s_tc.astype(np.float64) - s64)))
+    a, b_ = set(rank(s_tc, K).tolist()), set(rank(s64, K).tolist())
+    kth = np.sort(s64)[::-1][K - 1]
+    for c in a ^ b_:
+        gap = abs(s64[c] - kth)
+        assert gap <= 2.0 * err, f"{what}: chunk {c} boundary gap {gap:.3e} > 2 x {err:.3e}"
+    return len(a ^ b_) // 2, err
+
+
+@pytest.mark.parametrize("bits,cs", [(2, 1), (4, 2)])
+def test_higgs_tc_scan_vs_fp64(bits, cs):
+    """HIGGS2@1 and HIGGS4@2 at C2's 128K: the tensor-core scan's top-K vs the
+    fp64 ranking over the same dequantised landmarks; then the decode step's
+    token list and attention vs the oracle on the GPU's selection."""
+    from oracle import kvlab_port as P
+
+    n, B, H, G = 131072, 1, 8, 4
+    dev, k, v, gen = _higgs_store(B, n, H, cs, bits, 31 + bits)
+    q = torch.randn((B, H, G, D), generator=gen, device="cuda")
+    K = dev.n_select(2048 / n)
+    cid, sc, tok, ntok = dev.select(q, K, exact=False)
+    lm = dev.landmarks_dequantized()[0].cpu().numpy()                  # [C, H, D]
+    qb = q[0].cpu().numpy()
+    s64 = np.einsum("hgd,chd->c", qb.astype(np.float64), lm.astype(np.float64))
+    swaps, err = _tc_vs_fp64(sc[0].cpu().numpy(), s64, K, f"higgs{bits}@{cs}")
+    print(f"HIGGS{bits}@{cs} tensor-core scan: max|s_tc - s64| = {err:.3e}, "
+          f"boundary swaps vs fp64 = {swaps}")
+    # the decode step (bench path) selects the same set as kvb_select's fast path
+    plan = dev.decode_plan(G, K)
+    plan.run(q, want_chunks=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(np.sort(plan.cid[0].cpu().numpy()), np.sort(cid[0].cpu().numpy()))
+    t = plan.tok[0, : int(plan.ntok[0])].cpu().numpy()
+    assert np.array_equal(t, tok[0, : int(ntok[0])].cpu().numpy())
+    kb, vb = _heads_np(k[0]), _heads_np(v[0])
+    st = P.store_from_parts(kb, vb, cs, P.Budget(2048 / n, 384, 32),
+                            np.ascontiguousarray(lm.transpose(1, 0, 2)),
+                            dev.residency.outlier_chunks[0])
+    want_tok = np.unique(np.concatenate([np.arange(c * cs, min(c * cs + cs, n))
+                                         for c in plan.cid[0].cpu().numpy()] + [st.resident()]))
+    assert np.array_equal(t, want_tok)
+    o_ref, _, _ = P.sparse_attention(qb, st, t)
+    e = rel_err(plan.out[0].cpu().numpy(), o_ref)
+    assert e < 1e-4, e
+    dev.close()
+
+
+def test_appendix_e_tc_vs_fp64():
+    """Proposed-B (Appendix E): HIGGS 4-bit@8 landmarks + 1-bit residuals,
+    k = 2048 tokens, candidate multiplier 8, tensor-core stage 1 and 2 vs the
+    fp64 two-stage ranking; attention vs the oracle."""
+    from oracle import kvlab_port as P
+
+    n, B, H, G, k_tok, mult, cs = 131072, 1, 8, 4, 2048, 8, 8
+    dev, k, v, gen = _higgs_store(B, n, H, cs, 4, 99, residual_bits=1)
+    q = torch.randn((B, H, G, D), generator=gen, device="cuda")
+    cand, sc, tok, ntok = dev.select_residual(q, k_tok, mult, exact=False)
+    lm = dev.landmarks_dequantized()[0].cpu().numpy()                  # [C, H, D]
+    res = dev.residuals_dequantized()[0].cpu().numpy()                 # [n, H, D]
+    qb = q[0].cpu().numpy().astype(np.float64)
+    s64 = np.einsum("hgd,chd->c", qb, lm.astype(np.float64))
+    n_cand = min(dev.C, mult * math.ceil(k_tok / cs))
+    # stage 1: the candidate set vs the fp64 chunk ranking; the stage-1 error is
+    # measured on the exported scores of candidate-free tokens (= chunk score)
+    full = sc[0].cpu().numpy()
+    got_c = cand[0].cpu().numpy()
+    cand_tok = np.sort(np.concatenate([np.arange(c * cs, c * cs + cs) for c in got_c]))
+    mask = np.ones(n, bool)
+    mask[cand_tok] = False
+    rep64 = np.repeat(s64, cs)[:n]
+    err1 = float(np.max(np.abs(full[mask].astype(np.float64) - rep64[mask])))
+    a, b_ = set(got_c.tolist()), set(rank(s64, n_cand).tolist())
+    kth = np.sort(s64)[::-1][n_cand - 1]
+    for c in a ^ b_:
+        assert abs(s64[c] - kth) <= 2 * err1, (c, abs(s64[c] - kth), err1)
+    # stage 2: token scores over the GPU's candidates vs fp64
+    t64 = rep64[cand_tok] + np.einsum("hgd,nhd->n", qb, res[cand_tok].astype(np.float64))
+    err2 = float(np.max(np.abs(full[cand_tok].astype(np.float64) - t64)))
+    chosen = set(cand_tok[rank(full[cand_tok], k_tok)].tolist())
+    want = set(cand_tok[rank(t64, k_tok)].tolist())
+    kth2 = np.sort(t64)[::-1][k_tok - 1]
+    pos = {t: i for i, t in enumerate(cand_tok.tolist())}
+    for t in chosen ^ want:
+        assert abs(t64[pos[t]] - kth2) <= 2 * err2, (t, abs(t64[pos[t]] - kth2), err2)
+    print(f"Appendix-E: stage-1 err {err1:.3e}, {len(a ^ b_) // 2} candidate swaps; "
+          f"stage-2 err {err2:.3e}, {len(chosen ^ want) // 2} token swaps")
+    t = tok[0, : int(ntok[0])].cpu().numpy()
+    kb, vb = _heads_np(k[0]), _heads_np(v[0])
+    st = P.store_from_parts(kb, vb, cs, P.Budget(2048 / n, 384, 32),
+                            np.ascontiguousarray(lm.transpose(1, 0, 2)),
+                            dev.residency.outlier_chunks[0])
+    assert np.array_equal(t, np.unique(np.concatenate([np.array(sorted(chosen)), st.resident()])))
+    o_ref, _, _ = P.sparse_attention(qb.astype(np.float32), st, t)
+    out, _ = dev.attend(q, tok, ntok)
+    assert rel_err(out[0].cpu().numpy(), o_ref) < 1e-4
+    dev.close()
+
+
+@pytest.mark.parametrize("cs", [4, 16, 32])
+def test_c5_chunk_sweep_points(cs):
+    """C5 (proposed selection, HIGGS 2-bit landmarks) at chunk 4 / 16 / 32,
+    128K, budget 2048, B=2 through the bench's decode step."""
+    from oracle import kvlab_port as P
+
+    n, B, H, G = 131072, 2, 8, 4
+    dev, k, v, gen = _higgs_store(B, n, H, cs, 2, 500 + cs)
+    q = torch.randn((B, H, G, D), generator=gen, device="cuda")
+    K = dev.n_select(2048 / n)
+    plan = dev.decode_plan(G, K)
+    plan.run(q, want_chunks=True)
+    _, sc, _, _ = dev.select(q, K, exact=False)
+    torch.cuda.synchronize()
+    lm_all = dev.landmarks_dequantized().cpu().numpy()
+    for b in range(B):
+        lm = lm_all[b]
+        qb = q[b].cpu().numpy()
+        s64 = np.einsum("hgd,chd->c", qb.astype(np.float64), lm.astype(np.float64))
+        got = np.sort(plan.cid[b].cpu().numpy())
+        s_gpu = sc[b].cpu().numpy()
+        assert np.array_equal(got, np.sort(rank(s_gpu, K))), "decode step != fast-path top-K"
+        swaps, err = _tc_vs_fp64(s_gpu, s64, K, f"C5 cs{cs} seq {b}")
+        kb, vb = _heads_np(k[b]), _heads_np(v[b])
+        st = P.store_from_parts(kb, vb, cs, P.Budget(2048 / n, 384, 32),
+                                np.ascontiguousarray(lm.transpose(1, 0, 2)),
+                                dev.residency.outlier_chunks[b])
+        t = plan.tok[b, : int(plan.ntok[b])].cpu().numpy()
+        assert np.array_equal(t, P._union(st, got))
+        o_ref, _, _ = P.sparse_attention(qb, st, t)
+        e = rel_err(plan.out[b].cpu().numpy(), o_ref)
+        print(f"C5 cs {cs} seq {b}: K {K}, err {err:.2e}, swaps {swaps}, attention {e:.2e}")
+        assert e < 1e-4
+    dev.close()
+
+
+# ---------------------------------------------------------------------------
+# prefill: the GPU Gram-route SVD against LAPACK; GPU residuals vs kvlab
+# ---------------------------------------------------------------------------
+def test_gram_svd_matches_lapack():
+    """numerics.py:80-98: the GPU's fp64 Gram/eigh factors (the route every
+    C2-C4 store takes) reconstruct the keys as well as LAPACK's thin SVD, and
+    the two rank-r approximations agree up to fp16 factor rounding."""
+    from oracle import kvlab_port as P
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    n, H, r = 16384, 8, 160
+    rng = np.random.default_rng(5)
+    # keys with a decaying spectrum (real keys are low-rank-ish) plus noise
+    basis = rng.standard_normal((H * D, H * D)).astype(np.float32)
+    scale = (1.0 / (1.0 + np.arange(H * D) / 32.0)).astype(np.float32)
+    cat = (rng.standard_normal((n, H * D)).astype(np.float32) * scale) @ basis / 16
+    cat = cat.astype(np.float32)
+    dev = DeviceStore(batch=1, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=8,
+                      landmark=S.scheme_none(), slow=S.scheme_svd(r, H * D), svd_groups=1)
+    kd = torch.from_numpy(cat.reshape(1, n, H, D)).cuda()
+    lg, rg = dev.svd_factors(kd, method="gram")
+    lg = lg[0, :, 0].cpu().numpy()
+    rg = rg[0, 0].cpu().numpy()
+    ll, rl = P.svd16(cat, r)
+    rec_g = P.svd16_reconstruct(lg, rg)
+    rec_l = P.svd16_reconstruct(ll, rl)
+    e_g = rel_err(rec_g, cat)
+    e_l = rel_err(rec_l, cat)
+    d = rel_err(rec_g, rec_l)
+    print(f"Gram-route rel recon err {e_g:.6f}, LAPACK {e_l:.6f}, |Gram - LAPACK| {d:.2e}")
+    assert abs(e_g - e_l) <= 1e-3 * e_l
+    assert d < 5e-3
+    dev.close()
+
+
+def test_gpu_built_residuals_match_kvlab():
+    """kvstore.py:133-140: residuals built on the GPU from raw keys
+    (kvb_build_residuals) dequantise to kvlab's residuals_dq bit for bit."""
+    from conftest import golden
+    from paper_2604_08426_b200 import schemes as S
+    from paper_2604_08426_b200.store import DeviceStore
+
+    z = golden("res_higgs4_c8_higgs1")
+    H, n, hd = z["keys"].shape
+    dev = DeviceStore(batch=1, n_tokens=n, kv_heads=H, head_dim=hd, chunk_size=8,
+                      landmark=S.scheme_from_string(str(z["landmark_scheme"])),
+                      residual=S.scheme_from_string(str(z["residual_scheme"])),
+                      outlier_tokens=int(z["outlier_tokens"]), local_window=int(z["local_window"]))
+    kd = torch.from_numpy(np.ascontiguousarray(z["keys"].transpose(1, 0, 2))[None]).cuda()
+    dev.build_landmarks(kd)
+    lm = dev.landmarks_dequantized()[0].cpu().numpy()
+    assert np.array_equal(lm, np.ascontiguousarray(z["landmarks_dq"].transpose(1, 0, 2)))
+    res = dev.residuals_dequantized()[0].cpu().numpy()
+    assert np.array_equal(res, np.ascontiguousarray(z["residuals_dq"].transpose(1, 0, 2)))
+    dev.close()

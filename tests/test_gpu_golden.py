@@ -137,21 +137,28 @@ def test_higgs_decode_bit_exact_and_select(case):
 
 @pytest.mark.parametrize("case", HIGGS)
 def test_higgs_gpu_prefill_matches_reference(case):
+    """GPU HIGGS prefill (kvb_build_landmarks: signs, fwht_rows schedule, fp64
+    RMS -> fp16 scale, nearest codeword with the BLAS dot's FMA order) gives
+    kvlab's landmarks_dq bit for bit; the outlier set built from them and the
+    selection on top equal kvlab's."""
     from paper_2604_08426_b200 import compat as C, schemes as S
 
     z = golden(case)
+    b = _budget(C, z)
     st = C.build_store(z["keys"], z["values"], int(z["chunk_size"]),
-                       S.scheme_from_string(str(z["landmark_scheme"])), budget=_budget(C, z))
-    H = z["keys"].shape[0]
-    from paper_2604_08426_b200.store import DeviceStore  # noqa: F401
-
-    # scales are fp64-RMS -> fp16: bit-exact; codes may differ only on near ties
-    lib_codes = st.dev  # device store
+                       S.scheme_from_string(str(z["landmark_scheme"])), budget=b)
     lm = st.landmarks_dequantized()
     ref = z["landmarks_dq"]
-    mism = np.mean(lm != ref)
-    assert mism < 0.01, f"GPU HIGGS prefill differs on {mism:.4%} of landmark values"
-    assert rel_err(lm, ref) < 1e-3
+    assert np.array_equal(lm, ref), f"GPU HIGGS prefill differs on {np.mean(lm != ref):.4%} of values"
+    assert st.outlier_chunks == tuple(int(c) for c in z["outliers"]), "outlier set != kvlab"
+    assert np.array_equal(st.resident_token_ids, z["resident"])
+    sel = C.select_by_landmarks(st, z["queries"], b)
+    q = z["queries"]
+    lm_cm = _chunk_major(lm)
+    s64 = np.einsum("hgd,chd->c", q.astype(np.float64), lm_cm.astype(np.float64))
+    ties = compare_ranking(sel.chunk_ids, z["sum_chunk_ids"], s64, score_tol(q, lm_cm), case)
+    if ties == 0:
+        assert np.array_equal(sel.token_ids, z["sum_token_ids"])
 
 
 def test_residual_two_stage_matches_reference():
