@@ -91,11 +91,21 @@ def _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, b, budget_tokens, ch
     got = np.sort(plan.cid[b].cpu().numpy())
     assert np.array_equal(got, np.sort(rank(sx, K))), "decode-step top-K != top-K of kernel scores"
     s64 = np.einsum("hgd,hcd->c", qb.astype(np.float64), lm.astype(np.float64))
-    ties = compare_ranking(rank(sx, K), np.asarray(ref.chunk_ids), s64, score_tol(qb, lm_gpu),
-                           f"seq {b}")
+    tol = score_tol(qb, lm_gpu)
+    # rank-order positions that differ from kvlab's: each one a near-tie
+    # (exact score gap inside the fp32 forward-error bound), asserted inside
+    ties = compare_ranking(rank(sx, K), np.asarray(ref.chunk_ids), s64, tol, f"seq {b}")
     t = plan.tok[b, : int(plan.ntok[b])].cpu().numpy()
-    if ties == 0:
+    diff = set(got.tolist()) ^ set(ref.chunk_ids)
+    if not diff:  # same selected set (swaps, if any, are inside the top-K)
         assert np.array_equal(t, ref.token_ids), f"seq {b}: token ids != kvlab"
+    else:  # a boundary near-tie: both chunks within tol of the K-th exact score
+        kth = np.sort(s64)[::-1][K - 1]
+        for c in diff:
+            assert abs(s64[c] - kth) <= tol, (b, c, abs(s64[c] - kth), tol)
+    if ties:
+        print(f"seq {b}: {ties} rank positions differ from kvlab by near-ties (tol {tol:.2e}); "
+              f"selected sets {'equal' if not diff else 'differ at the boundary'}")
     o_ref, _, _ = P.sparse_attention(qb, st, t)
     err = rel_err(plan.out[b].cpu().numpy(), o_ref)
     return ties, err
@@ -141,8 +151,10 @@ def test_c4_one_layer_1m():
     assert K == 2048
     ties, err = _check_shadowkv_seq(dev, k, v, q, left, right, plan, K, 0, budget,
                                     check_outliers=False)
-    print(f"C4 1M layer: near-ties {ties}, rel err {err:.2e}")
-    assert ties == 0 and err < 1e-4, (ties, err)
+    # 131072 chunk scores: a few rank-order near-ties are expected and each is
+    # justified inside _check_shadowkv_seq (gap <= the fp32 error bound)
+    print(f"C4 1M layer: near-tie rank positions {ties}, rel err {err:.2e}")
+    assert ties <= 16 and err < 1e-4, (ties, err)
     dev.close()
 
 
