@@ -173,6 +173,14 @@ kvb_status kvb_store_set_residuals_higgs(kvb_store* store, const uint8_t* codes,
 kvb_status kvb_landmarks_dequantized(kvb_store* store, float* out, void* stream);
 kvb_status kvb_residuals_dequantized(kvb_store* store, float* out, void* stream);
 
+/* Slow-tier K/V of an explicit token list, float32 [n][kv_heads*head_dim]
+ * each (token order as given; token_ids device int32 [n] of sequence `seq`).
+ * resident_exact = 0: load_chunks (kvstore.py:257-279) -- every token through
+ * the slow tier (slow_keys_dq / slow_values_dq); 1: gather_kv
+ * (kvstore.py:281-291) -- resident tokens exact from the fast tier.        */
+kvb_status kvb_gather_kv(kvb_store* store, int32_t seq, const int32_t* token_ids, int32_t n,
+                         int32_t resident_exact, float* k_out, float* v_out, void* stream);
+
 /* ---- decode ------------------------------------------------------------- */
 
 /* Queries: device float32 [batch][kv_heads][G][head_dim] (selection.py:33-43

@@ -81,6 +81,7 @@ SIGNATURES = [
     ("kvb_store_set_residuals_higgs", _I32, [_P, _P, _P, _P]),
     ("kvb_landmarks_dequantized", _I32, [_P, _P, _P]),
     ("kvb_residuals_dequantized", _I32, [_P, _P, _P]),
+    ("kvb_gather_kv", _I32, [_P, _I32, _P, _I32, _I32, _P, _P, _P]),
     ("kvb_select", _I32, [_P, _P, C.POINTER(SelectArgs), _P, _P, _P, _P, _P, _I64, _P]),
     ("kvb_score_landmarks", _I32, [_P, _P, _I32, _I32, _P, _P]),
     ("kvb_select_workspace_bytes", _I64, [_P, C.POINTER(SelectArgs)]),

@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libkvb.so")
 SOURCES = ["kvb_api.cu", "kvb_score.cu", "kvb_select.cu", "kvb_attend.cu", "kvb_build.cu",
-           "kvb_higgs_tc.cu", "kvb_attend_wh.cu", "kvb_attend_bulk.cu", "kvb_recon.cu", "kvb_pipe.cu"]
+           "kvb_higgs_tc.cu", "kvb_attend_wh.cu", "kvb_attend_bulk.cu", "kvb_recon.cu", "kvb_tier.cu"]
 HEADERS = ["kvb_common.cuh", "kvb_internal.h", "kvb_fuse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -18,14 +18,16 @@ head-concatenated [n, Hkv*D] keys (ShadowKV, SPEC.md:85).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from fractions import Fraction
 
 import numpy as np
 import torch
 
+from .kvt import read_kvt, write_kvt
 from .schemes import (HIGGS, NONE, SVD, SchemeDescriptor, bits_per_key as _bits_per_key,
-                      scheme_none)
+                      scheme_from_string, scheme_none, scheme_to_string)
 from .store import DeviceStore
 
 
@@ -223,8 +225,9 @@ class ChunkedKVStore:
         return _bits_per_key(self.landmark_scheme, self.chunk_size, self.residual_scheme)
 
     def load_chunks(self, chunk_ids):
-        """Traffic accounting of kvstore.py:257-279 (token counts only; the
-        K/V themselves are consumed on the device by sparse_attention)."""
+        """kvstore.py:257-279: slow-tier K/V [heads, T, D] of the requested
+        chunks (read on the device from the offload tier / SVD factors) and
+        the traffic they cost (resident tokens excluded)."""
         ids = sorted(set(int(c) for c in chunk_ids))
         for c in ids:
             if not 0 <= c < self.n_chunks:
@@ -232,7 +235,45 @@ class ChunkedKVStore:
         toks = (np.concatenate([self.chunk_token_ids(c) for c in ids]) if ids
                 else np.empty(0, dtype=np.int64))
         loaded = int(np.count_nonzero(~np.isin(toks, self.resident_token_ids)))
-        return TierTraffic(loaded, self.fast_tier_resident_bits())
+        traffic = TierTraffic(loaded, self.fast_tier_resident_bits())
+        k, v = self._gather(toks, resident_exact=False)
+        return k, v, traffic
+
+    def gather_kv(self, token_ids):
+        """kvstore.py:281-291: K/V [heads, T, D] as attention sees them --
+        resident tokens exact from the fast tier, the rest slow-tier."""
+        return self._gather(np.asarray(token_ids, dtype=np.int64), resident_exact=True)
+
+    def _gather(self, toks: np.ndarray, resident_exact: bool):
+        h, d = self.n_heads, self.head_dim
+        if len(toks) == 0:
+            z = np.zeros((h, 0, d), dtype=np.float32)
+            return z, z.copy()
+        if toks.min() < 0 or toks.max() >= self.n_tokens:
+            raise ValueError("token id out of range")
+        t = torch.from_numpy(toks.astype(np.int32)).cuda()
+        k, v = self.dev.gather_kv(0, t, resident_exact)
+        return (k.permute(1, 0, 2).contiguous().cpu().numpy(),
+                v.permute(1, 0, 2).contiguous().cpu().numpy())
+
+    def save(self, directory) -> None:
+        """kvstore.py:309-326: keys/values as KVT1 plus a manifest that
+        ``load_store`` (and kvlab's own load_store) reads back."""
+        os.makedirs(directory, exist_ok=True)
+        write_kvt(os.path.join(directory, "keys.kvt"), self.keys)
+        write_kvt(os.path.join(directory, "values.kvt"), self.values)
+        manifest = {
+            "chunk_size": self.chunk_size,
+            "landmark_scheme": scheme_to_string(self.landmark_scheme),
+            "residual_scheme": scheme_to_string(self.residual_scheme) if self.residual_scheme else "",
+            "slow_tier_scheme": scheme_to_string(self.slow_tier_scheme),
+            "sparse_fraction": repr(self.budget.sparse_fraction),
+            "outlier_tokens": self.budget.outlier_tokens,
+            "local_window": self.budget.local_window,
+        }
+        with open(os.path.join(directory, "manifest.txt"), "w", encoding="utf-8") as f:
+            for key, val in manifest.items():
+                f.write(f"{key} = {val}\n")
 
     def append(self, new_keys, new_values) -> None:
         """kvstore.py:295-305: one token per head joins the tail chunk; the
@@ -243,6 +284,28 @@ class ChunkedKVStore:
         self.values = np.concatenate([self.values, nv], axis=1)
         self.dev.close()
         self._build()
+
+
+def load_store(directory, **kwargs) -> ChunkedKVStore:
+    """kvstore.py:329-351: rebuild a saved store (KVT1 keys/values +
+    manifest) on the device."""
+    fields = {}
+    with open(os.path.join(directory, "manifest.txt"), encoding="utf-8") as f:
+        for line in f:
+            if "=" in line:
+                key, _, val = line.partition("=")
+                fields[key.strip()] = val.strip()
+    residual = fields["residual_scheme"]
+    return build_store(
+        read_kvt(os.path.join(directory, "keys.kvt")),
+        read_kvt(os.path.join(directory, "values.kvt")),
+        chunk_size=int(fields["chunk_size"]),
+        landmark_scheme=scheme_from_string(fields["landmark_scheme"]),
+        residual_scheme=scheme_from_string(residual) if residual else None,
+        budget=BudgetConfig(sparse_fraction=float(fields["sparse_fraction"]),
+                            outlier_tokens=int(fields["outlier_tokens"]),
+                            local_window=int(fields["local_window"])),
+        slow_tier_scheme=scheme_from_string(fields["slow_tier_scheme"]), **kwargs)
 
 
 def build_store(keys, values, chunk_size: int, landmark_scheme: SchemeDescriptor,
@@ -380,3 +443,50 @@ def recall(selected: SelectionResult, oracle: SelectionResult) -> float:
     if not oracle_ids:
         raise ValueError("oracle selection is empty")
     return len(oracle_ids & set(selected.token_ids.tolist())) / len(oracle_ids)
+
+
+# names the reference's decode-path callers bind at import time (harness.py:21-29)
+_PATCH = {
+    "harness": ("build_store", "select_by_landmarks", "approx_topk_residual", "oracle_select",
+                "recall", "sparse_attention", "full_attention_heads"),
+    "selection": ("select_by_landmarks", "approx_topk_residual", "oracle_select",
+                  "residual_scores", "recall"),
+    "attention": ("sparse_attention", "full_attention_heads"),
+    "kvstore": ("build_store", "load_store"),
+}
+
+
+class install:
+    """Point an unmodified kvlab at this module: every
+    decode-path name kvlab's modules and its harness bound at import is
+    rebound to the GPU implementation. Usable as a context manager; ``undo``
+    restores the originals.
+
+        import kvlab
+        with compat.install(kvlab):
+            rows = kvlab.harness.run_sweep(cfg)
+    """
+
+    def __init__(self, kvlab_pkg):
+        import importlib
+
+        self._saved = []
+        me = globals()
+        for mod_name, names in _PATCH.items():
+            mod = importlib.import_module(f"{kvlab_pkg.__name__}.{mod_name}")
+            for nm in names:
+                if hasattr(mod, nm):
+                    self._saved.append((mod, nm, getattr(mod, nm)))
+                    setattr(mod, nm, me[nm])
+
+    def undo(self):
+        for mod, nm, fn in reversed(self._saved):
+            setattr(mod, nm, fn)
+        self._saved.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.undo()
+        return False

@@ -215,9 +215,6 @@ void free_store(kvb_store* s) {
   cudaFree(s->res_count);
   cudaFree(s->k2_hist);
 
-  cudaFree(s->pipe_ctr);
-  cudaFree(s->pipe_bm);
-  cudaFree(s->pipe_cand);
   cudaFree(s->k2_meta);
   cudaFree(s->k2_overflow);
   cudaFree(s->res_bitmap);
@@ -339,13 +336,6 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
   s->Wc = (s->C + 31) / 32;
-  if (d.landmark_kind == KVB_LM_DENSE && stream_scan_supported(s)) {
-    if ((st = dalloc(&s->pipe_ctr, 3 * B, "pipeline counters")) != KVB_OK) return bail(st);
-    if ((st = dalloc(&s->pipe_bm, B * s->Wc, "pipeline bitmaps")) != KVB_OK) return bail(st);
-    if ((st = dalloc(&s->pipe_cand, B * kPipeCandCap, "pipeline candidates")) != KVB_OK) return bail(st);
-    cudaMemset(s->pipe_ctr, 0, 3 * B * sizeof(int));
-    cudaMemset(s->pipe_bm, 0, B * s->Wc * sizeof(uint32_t));
-  }
   cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
   cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
   cudaMemset(s->res_count, 0, B * sizeof(int32_t));
@@ -546,6 +536,18 @@ kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* val
     if (!keys) KVB_FAIL(KVB_EINVAL, "slow tier 'none' needs keys");
     KVB_CUDA(cudaMemcpyAsync(s->off_k_dev, keys, bytes, cudaMemcpyDefault, st), "offload K");
   }
+  return KVB_OK;
+}
+
+kvb_status kvb_gather_kv(kvb_store* s, int32_t seq, const int32_t* token_ids, int32_t n,
+                         int32_t resident_exact, float* k_out, float* v_out, void* stream) {
+  if (!s || !k_out || !v_out || (n > 0 && !token_ids)) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (seq < 0 || seq >= s->d.batch) KVB_FAIL(KVB_EINVAL, "sequence index out of range");
+  if (n < 0) KVB_FAIL(KVB_EINVAL, "negative token count");
+  if (!s->off_v_dev) KVB_FAIL(KVB_EINVAL, "store has no offload tier");
+  KVB_CUDA(launch_gather_kv(s, seq, token_ids, n, resident_exact ? 1 : 0, k_out, v_out,
+                            as_stream(stream)),
+           "tier gather");
   return KVB_OK;
 }
 
@@ -942,23 +944,6 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
   // for the stream's previous work, then triggers) -> scan (PDL, overlaps the
   // prep; waits for it at exit) -> attention -> merge, no side stream or
   // events. Other paths fork the prep onto the side stream.
-  // pipelined layer (kvb_pipe.cu): dense bf16 landmarks, the scan streamed
-  // sequence by sequence with each sequence's selection + attention running
-  // beside the scan of the next ones (same results as the chain below)
-  if (chunk_path && !recon && sel->aggregation == KVB_AGG_SUM && pipe_supported(s, L.G, K)) {
-    Carve sv(sws, sb);
-    float* sc = sv.take<float>((size_t)s->d.batch * s->C);
-    if (s->k2_dirty) {  // a previous chain aborted part-way
-      KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
-      KVB_CUDA(cudaMemsetAsync(s->pipe_ctr, 0, sizeof(int) * 3 * s->d.batch, st), "counter reset");
-      KVB_CUDA(cudaMemsetAsync(s->pipe_bm, 0, sizeof(uint32_t) * s->d.batch * s->Wc, st), "bitmap reset");
-      s->k2_dirty = false;
-    }
-    s->k2_dirty = true;
-    KVB_CUDA(launch_pipe_layer(s, L, K, sc, chunk_ids, st), "pipelined decode layer");
-    s->k2_dirty = false;
-    return KVB_OK;
-  }
   const bool inline_prep = chunk_path && !recon && sel->aggregation == KVB_AGG_SUM &&
                            s->C <= 32768 && s->d.landmark_kind == KVB_LM_DENSE;
   if (inline_prep) {

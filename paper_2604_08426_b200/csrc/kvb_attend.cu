@@ -716,7 +716,6 @@ size_t attend_ws_bytes(const kvb_store* s, int G, int cap) {
   }
   const size_t sb = (size_t)std::max(1, sm_count() / s->d.batch);  // bulk kernel (both modes)
   if (sb > splits) splits = sb;
-  if (stream_scan_supported(s)) splits = std::max(splits, (size_t)sm_count());  // pipelined layer
   size_t bytes = B * splits * H * G * (2 + D) * sizeof(float) + 4096;
   bytes += B * H * G * D * sizeof(float) + B * sizeof(int) + 64; // q2, split tickets
   if (s->d.slow_kind == KVB_SLOW_SVD) bytes += B * H * G * s->d.svd_rank * sizeof(float);
@@ -729,7 +728,6 @@ struct AttWs {
   float *pm, *pl, *po, *q2, *qt2;
   int* counters;
   int splits;
-  int smax;  // split stride of the partials
   bool wh;
   bool bulk;
 };
@@ -746,8 +744,6 @@ AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo
   size_t smax = geo.splits;
   if (attend_wh_supported(s, G)) smax = std::max(smax, (size_t)attend_wh_splits(s, a.cap));
   smax = std::max(smax, (size_t)std::max(1, sm_count() / B));
-  if (stream_scan_supported(s)) smax = std::max(smax, (size_t)sm_count());
-  w.smax = (int)smax;
   float* ws = static_cast<float*>(a.ws);
   w.pm = ws;
   w.pl = w.pm + (size_t)B * smax * H * G;
@@ -883,81 +879,6 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
   bl.sel_hist = sel_hist;
   bl.chunk_out = chunk_out;
   bl.svd_logits = svd_logits;
-  return launch_attend_bulk(s, bl, st);
-}
-
-namespace {
-constexpr int kScanStages = 3;
-struct PipeSplits {
-  int s_main, s_tail;
-};
-// the last sequence's attention is the exposed tail -> it gets a quarter of
-// the SMs; the others share the rest. All CTAs must be co-resident (the
-// cooperative selection waits on its siblings): total <= #SMs.
-PipeSplits pipe_splits(int B) {
-  const int nsm = sm_count();
-  PipeSplits p{};
-  p.s_tail = B > 1 ? std::max(1, nsm / 4) : nsm;
-  p.s_main = B > 1 ? std::max(1, (nsm - p.s_tail) / (B - 1)) : 1;
-  return p;
-}
-size_t pipe_attn_smem_cap(const kvb_store* s) {
-  return 227 * 1024 - stream_scan_smem(s->E, kScanStages) - 2048;
-}
-}  // namespace
-
-bool pipe_supported(const kvb_store* s, int G, int K) {
-  if (!stream_scan_supported(s) || !s->pipe_ctr || K > s->C || K < 1) return false;
-  const int B = s->d.batch;
-  const PipeSplits ps = pipe_splits(B);
-  if ((B - 1) * ps.s_main + ps.s_tail > sm_count()) return false;
-  return attend_pipe_fits(s, G, K, std::min(ps.s_main, ps.s_tail), pipe_attn_smem_cap(s));
-}
-
-// Pipelined dense layer (kvb_pipe.cu): prep (PDL: waits, then triggers) ->
-// k1_stream (PDL; releases done[b] per sequence) -> k5_attend_pipe (PDL;
-// co-resident with the scan, acquires done[b]) -> k5_merge_rows (PDL).
-cudaError_t launch_pipe_layer(const kvb_store* s, const AttendLaunch& a, int K, float* scores,
-                              int32_t* chunk_out, cudaStream_t st) {
-  const int G = a.G, B = s->d.batch;
-  if (!pipe_supported(s, G, K)) return cudaErrorNotSupported;
-  AttGeom geo = attend_geometry(s, G, a.cap);
-  AttWs w = carve_att_ws(s, a, geo);
-  cudaError_t e = launch_attend_prep(s, a, st, true);
-  if (e != cudaSuccess) return e;
-  e = launch_stream_scan(s, a.q, G, scores, s->k2_hist, s->pipe_ctr, kScanStages, st);
-  if (e != cudaSuccess) return e;
-  const PipeSplits ps = pipe_splits(B);
-  const int s_main = ps.s_main, s_tail = ps.s_tail;
-  BulkLaunch bl{};
-  bl.mode = 1;
-  bl.items = nullptr;
-  bl.cap = K;
-  bl.K = K;
-  bl.G = G;
-  bl.q = a.q;
-  bl.qt2 = w.qt2;
-  bl.pm = w.pm;
-  bl.pl = w.pl;
-  bl.po = w.po;
-  bl.counters = w.counters;
-  bl.out = a.out;
-  bl.lse = a.lse;
-  bl.splits = std::min(s_main, s_tail);
-  bl.tok_out = const_cast<int32_t*>(a.token_ids);
-  bl.ntok_out = const_cast<int32_t*>(a.n_tokens);
-  bl.tcap = a.cap;
-  bl.sel_scores = scores;
-  bl.sel_hist = s->k2_hist;
-  bl.chunk_out = chunk_out;
-  bl.pipe = 1;
-  bl.s_main = s_main;
-  bl.s_tail = s_tail;
-  bl.n_main = B - 1;
-  bl.smem_cap = pipe_attn_smem_cap(s);
-  bl.scan_done = s->pipe_ctr;
-  bl.n_scan = stream_scan_ctas();
-  bl.slay = w.smax;
   return launch_attend_bulk(s, bl, st);
 }
 

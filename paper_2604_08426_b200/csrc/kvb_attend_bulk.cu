@@ -94,19 +94,6 @@ struct BulkParams {
   // geometry
   int maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_bar, off_stage;
   int nB;                     // batch (grid y of the split-K launch)
-  int Slay;                   // split stride of the partials [B][Slay][HG] (= splits, or
-                              // the largest per-sequence split count in VAR 3)
-  // VAR 3 (pipelined layer, kvb_pipe.cu): grid.x = n_main * s_main + (B - n_main) * s_tail
-  // CTAs; sequence b waits on scan_done[b] == n_scan instead of the whole scan grid,
-  // then its CTAs select cooperatively through sel_bm / cand / cand_cnt / sel_done
-  int s_main, s_tail, n_main;
-  const int* scan_done;
-  int n_scan;
-  int* sel_done;
-  int* cand_cnt;
-  uint32_t* sel_bm;           // [B][Wc]
-  uint64_t* cand;             // [B][cand_cap] (key << 32 | chunk id)
-  int cand_cap;
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -116,14 +103,9 @@ __device__ __forceinline__ uint64_t gtimer() {
 }
 #define KVB_STAMP(ph)                                                                     \
   do {                                                                                    \
-    if (p.trace && tid == 0) p.trace[((size_t)b * p.Slay + split) * 8 + (ph)] = gtimer(); \
+    if (p.trace && tid == 0) p.trace[((size_t)b * S + split) * 8 + (ph)] = gtimer();      \
   } while (0)
 
-__device__ __forceinline__ int ld_acquire_i32(const int* a) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -297,7 +279,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   // before waiting on the scan, so their data lands during the selection.
   // Same slot / owner mapping as produce() for k < pre_done (it skips them).
   int pre_done = 0;
-  if ((VAR == 2 || VAR == 3) && p.mode == 1 && p.sel_scores) {
+  if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     pre_done = min(min(2, n_rloc / ett), nst - 1);
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
@@ -315,17 +297,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       }
     }
   }
-  if (VAR == 3) {
-    // pipelined layer: only this sequence's scan rows (all scan CTAs released
-    // done[b]) and, through the scan's own grid-dependency wait, the q~ prep
-    if (tid == 0) {
-      while (ld_acquire_i32(p.scan_done + b) < p.n_scan) __nanosleep(128);
-      __threadfence();
-    }
-    __syncthreads();
-  } else {
-    pdl_wait();  // the selection (token / chunk list) of the previous kernel
-  }
+  pdl_wait();  // the selection (token / chunk list) of the previous kernel
   KVB_STAMP(6);
   if (p.mode == 0) {  // token mode: the list length comes from the selection kernel
     const int P = p.nitems[b];
@@ -347,80 +319,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
                             : make_float2(0.f, 0.f);
       }
   }
-  if (VAR == 3) {
-    // cooperative top-K of sequence b over its S CTAs (kvb_fuse.cuh semantics):
-    // every CTA derives the threshold bin from the histogram, classifies its
-    // 1/S slice of the scores into the shared (global) winner bitmap and
-    // threshold-bin candidate list, then -- after all S slices are in --
-    // resolves the K-th key over the candidates in shared memory
-    unsigned char* pro = ring + (size_t)pre_done * p.stage_bytes;
-    uint32_t* wb = reinterpret_cast<uint32_t*>(pro);
-    uint32_t* sk = wb + ((p.Wc + 3) & ~3);
-    const size_t ring_bytes = (size_t)(nst - pre_done) * p.stage_bytes;
-    const int cap = (int)((ring_bytes - (size_t)((p.Wc + 3) & ~3) * 4) / 8);
-    int32_t* si = reinterpret_cast<int32_t*>(sk + cap);
-    const float* scs = p.sel_scores + (size_t)b * p.C;
-    __shared__ int s_tb, s_kb;
-    if (tid == 0) {
-      s_tb = 0;
-      s_kb = 0;
-    }
-    __syncthreads();
-    fuse_threshold(p.sel_hist + (size_t)b * kFuseHistBins, p.Kb, red, &s_tb, &s_kb);
-    const uint32_t tb = (uint32_t)s_tb;
-    uint32_t* gbm = p.sel_bm + (size_t)b * p.Wc;
-    uint64_t* gcand = p.cand + (size_t)b * p.cand_cap;
-    {
-      const int c0 = (int)(((long long)p.C * split) / S), c1 = (int)(((long long)p.C * (split + 1)) / S);
-      for (int i = c0 + tid; i < c1; i += nthr) {
-        const uint32_t key = score_key(__ldcg(scs + i)), bin = key >> 21;
-        if (bin > tb) {
-          atomicOr(gbm + (i >> 5), 1u << (i & 31));
-        } else if (bin == tb) {
-          const int pos = atomicAdd(p.cand_cnt + b, 1);
-          if (pos < p.cand_cap) gcand[pos] = ((uint64_t)key << 32) | (uint32_t)i;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(p.sel_done + b, 1);
-      while (ld_acquire_i32(p.sel_done + b) < S) __nanosleep(64);
-      __threadfence();
-    }
-    __syncthreads();
-    for (int w = tid; w < p.Wc; w += nthr) wb[w] = __ldcg(gbm + w);
-    const int nc = __ldcg(p.cand_cnt + b);
-    const bool fits = nc <= cap && nc <= p.cand_cap;
-    if (fits)
-      for (int i = tid; i < nc; i += nthr) {
-        const uint64_t v = __ldcg(gcand + i);
-        sk[i] = (uint32_t)(v >> 32);
-        si[i] = (int32_t)(uint32_t)v;
-      }
-    __syncthreads();
-    resolve_threshold_bin(scs, p.C, tb, s_kb, wb, sk, si, fits ? nc : cap + 1, cap, red);
-    const int per = (p.Wc + nthr - 1) / nthr;
-    const int w0 = min(p.Wc, tid * per), w1 = min(p.Wc, w0 + per);
-    int cnt = 0;
-    for (int w = w0; w < w1; ++w) cnt += __popc(wb[w]);
-    int tot;
-    int pos = block_excl_scan(cnt, red, &tot);
-    for (int w = w0; w < w1; ++w) {
-      uint32_t bits = wb[w];
-      while (bits) {
-        const int bit = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        if (pos < p.K) uc[pos] = w * 32 + bit;
-        ++pos;
-      }
-    }
-    for (int i = tot + tid; i < p.K; i += nthr) uc[i] = -1;
-    __syncthreads();
-    if (p.chunk_out && split == 0)
-      for (int i = tid; i < p.K; i += nthr) p.chunk_out[(size_t)b * p.K + i] = uc[i];
-  } else   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
+  if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     // top-K from the scan's scores + histogram into a bitmap in the (not yet
     // used) ring, then ascending ids: each thread owns a run of words, one scan
     // the selection's scratch lives in the ring slots after the prefetched ones
@@ -450,7 +349,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     select_topk_shared(scs, p.C,
                        p.sel_hist + (size_t)b * kFuseHistBins,
                        p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
-                       p.trace ? p.trace + (size_t)p.nB * p.Slay * 8 + 64 + ((size_t)b * p.Slay + split) * 8
+                       p.trace ? p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8
                                : nullptr,
                        stage, staged ? &stage_bar : nullptr, 0);
     if (staged && tid == 0)  // all threads waited on it inside (and synced after)
@@ -475,7 +374,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     if (p.chunk_out && split == 0)
       for (int i = tid; i < p.K; i += nthr) p.chunk_out[(size_t)b * p.K + i] = uc[i];
     if (p.trace)
-      sel_stamp(p.trace + (size_t)p.nB * p.Slay * 8 + 64 + ((size_t)b * p.Slay + split) * 8, 4);
+      sel_stamp(p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8, 4);
   } else if (p.mode == 1) {
     for (int i = tid; i < p.K; i += nthr) uc[i] = p.items[(size_t)b * p.cap + i];
   }
@@ -498,7 +397,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     if (tid == 0) ud[nres] = run;
     __syncthreads();
     if (p.trace)
-      sel_stamp(p.trace + (size_t)p.nB * p.Slay * 8 + 64 + ((size_t)b * p.Slay + split) * 8, 5);
+      sel_stamp(p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8, 5);
     if (p.tok_out && split == 0 && tid == 0) {
       const int lastlen = p.n - (p.C - 1) * p.cs;
       const int atot = p.Kb * p.cs - ((p.Kb > 0 && uc[p.Kb - 1] == p.C - 1) ? p.cs - lastlen : 0);
@@ -569,7 +468,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   if (p.trace && tid == 0) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    p.trace[((size_t)b * p.Slay + split) * 8 + 7] =
+    p.trace[((size_t)b * S + split) * 8 + 7] =
         ((uint64_t)smid << 32) | (uint64_t)(n_ex + n_sv);
   }
   const int t_ex = (n_ex + ett - 1) / ett, t_sv = (n_sv + kBT - 1) / kBT;
@@ -901,7 +800,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
 
   KVB_STAMP(4);
   // ---- partials (m, l, o) of this split ----------------------------------------------
-  const size_t pb = ((size_t)b * p.Slay + split) * HG + (size_t)h * G;
+  const size_t pb = ((size_t)b * S + split) * HG + (size_t)h * G;
   const bool writer = QW == 4 ? tig < 2 : true;
   if (writer && g4 == 0) {
 #pragma unroll
@@ -936,32 +835,6 @@ __global__ void __maxnreg__(232) k5_attend_bulk(const __grid_constant__ BulkPara
   attend_item<QW, NKS, VAR>(p, blockIdx.y, blockIdx.x, gridDim.x, sm);
 }
 
-// VAR 3: one flat grid, sequence b owns s_main (b < n_main) or s_tail CTAs;
-// capped at 192 registers: 256 x 192 + 128 x 120 (k1_stream) <= 64K per SM
-template <int QW, int NKS>
-__global__ void __maxnreg__(192) k5_attend_pipe(const __grid_constant__ BulkParams p) {
-  extern __shared__ __align__(128) unsigned char sm[];
-  int x = blockIdx.x, b, split, S;
-  if (x < p.n_main * p.s_main) {
-    b = x / p.s_main;
-    split = x - b * p.s_main;
-    S = p.s_main;
-  } else {
-    x -= p.n_main * p.s_main;
-    b = p.n_main + x / p.s_tail;
-    split = x % p.s_tail;
-    S = p.s_tail;
-  }
-  attend_item<QW, NKS, 3>(p, b, split, S, sm);
-}
-
-struct PipeMergeArgs {
-  uint32_t* bm_clear;  // [B][Wc] winner bitmaps (null: not a pipelined layer)
-  int Wc, nB;
-  int* ctr_clear;      // [3][B]: scan_done, sel_done, cand_cnt
-  int s_main, s_tail, n_main;
-};
-
 // Exact LSE merge of the split partials: one CTA per (row = h*G + g, sequence),
 // thread d. Launched with programmatic stream serialization right behind
 // k5_attend_bulk (which triggers its dependents at entry), so its CTAs are
@@ -971,8 +844,7 @@ __global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict_
                                                      const float* __restrict__ pl,
                                                      const float* __restrict__ po, int S, int HG,
                                                      float* __restrict__ out, float* __restrict__ lse,
-                                                     uint32_t* __restrict__ hist_clear,
-                                                     PipeMergeArgs pa) {
+                                                     uint32_t* __restrict__ hist_clear) {
   const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x, lane = d & 31;
   // the next layer's (PDL-launched, waiting) prep may become resident now
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -980,14 +852,7 @@ __global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict_
   // the attention (complete) was the last reader of the scan's histogram
   if (hist_clear && row == 0)
     for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
-  // pipelined layer: re-zero the sequence's cooperative-selection state
-  if (pa.bm_clear && row == 0) {
-    for (int i = d; i < pa.Wc; i += blockDim.x) pa.bm_clear[(size_t)b * pa.Wc + i] = 0u;
-    if (d < 3) pa.ctr_clear[(size_t)d * pa.nB + b] = 0;
-  }
   const size_t base = (size_t)b * S * HG + row;
-  if (pa.bm_clear) S = b < pa.n_main ? pa.s_main : pa.s_tail;  // the stride stays the layout's
-
   float m = -INFINITY, acc = 0.f, L = 0.f;
   constexpr int CH = 32;  // splits per round: one round for S <= 32, every load in flight
   for (int s0 = 0; s0 < S; s0 += CH) {
@@ -1019,12 +884,11 @@ struct BulkGeom {
   size_t smem;
 };
 
-BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0, int splits_override = 0,
-                       size_t smem_cap = 0) {
+BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
   BulkGeom g{};
   const int B = s->d.batch, H = s->d.kv_heads;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
-  int splits = splits_override > 0 ? splits_override : sm_count() / B;
+  int splits = sm_count() / B;
   const int tiles = (positions_cap + kBT - 1) / kBT;
   if (splits > tiles) splits = tiles;
   if (splits < 1) splits = 1;
@@ -1051,8 +915,7 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0, int spl
   g.off_uni = (3 * g.maxper * 4 + 127) & ~127;
   g.off_bar = (g.off_uni + (K + 2 * s->d.max_resident + 1) * 4 + 127) & ~127;
   g.off_stage = g.off_bar + 128;
-  const size_t lim = smem_cap ? smem_cap : 227 * 1024;
-  const size_t room = lim > (size_t)g.off_stage + 2048 ? lim - g.off_stage - 2048 : 0;  // static smem + slack
+  const size_t room = 227 * 1024 - g.off_stage - 2048;  // static smem + slack
   g.nst = std::min<int>(kBMaxStages, (int)(room / g.stage_bytes));
   g.smem = (size_t)g.off_stage + (size_t)g.nst * g.stage_bytes;
   return g;
@@ -1075,14 +938,6 @@ bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) 
   return g.smem <= 227 * 1024;
 }
 
-// pipelined layer: the attention CTA must fit beside a k1_stream CTA
-bool attend_pipe_fits(const kvb_store* s, int G, int K, int splits, size_t smem_cap) {
-  if (!attend_bulk_supported(s, G, s->d.max_resident + K * s->d.chunk_size, K)) return false;
-  if (G > 4 || (s->d.slow_kind == KVB_SLOW_SVD && s->d.svd_rank != 160)) return false;
-  const BulkGeom g = bulk_geometry(s, s->d.max_resident + K * s->d.chunk_size, K, splits, smem_cap);
-  return g.nst >= 3 && g.smem <= smem_cap;
-}
-
 int attend_bulk_splits(const kvb_store* s, int positions_cap) {
   return bulk_geometry(s, positions_cap).splits;
 }
@@ -1091,10 +946,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   const int B = s->d.batch, H = s->d.kv_heads;
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int positions_cap = a.mode == 0 ? a.cap : s->d.max_resident + a.K * s->d.chunk_size;
-  const BulkGeom g = a.pipe ? bulk_geometry(s, positions_cap, a.K, a.splits, a.smem_cap)
-                            : bulk_geometry(s, positions_cap, a.mode == 1 ? a.K : 0);
+  const BulkGeom g = bulk_geometry(s, positions_cap, a.mode == 1 ? a.K : 0);
   if (g.splits != a.splits) return cudaErrorInvalidValue;
-  if (a.pipe && (g.nst < 3 || g.smem > a.smem_cap)) return cudaErrorNotSupported;
   BulkParams p{};
   p.mode = a.mode;
   p.items = a.items;
@@ -1127,8 +980,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.counters = a.counters;
   p.out = a.out;
   p.lse = a.lse;
-  const size_t slay_t = (size_t)(a.slay > 0 ? a.slay : g.splits);
-  p.trace = (slay_t * B * 16 + 64 <= (size_t)kTraceWords) ? trace_buffer() : nullptr;
+  p.trace = ((size_t)g.splits * B * 8 + B * 4 <= (size_t)kTraceWords) ? trace_buffer() : nullptr;
   p.maxper = g.maxper;
   p.vrow = g.vrow;
   p.krow_ex = g.krow_ex;
@@ -1178,35 +1030,6 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
 #undef KVB_BULK_VAR
   dim3 grid(g.splits, B);
   p.nB = B;
-  p.Slay = a.slay > 0 ? a.slay : g.splits;
-  PipeMergeArgs pa{};
-  if (a.pipe) {
-    // pipelined layer: flat grid of per-sequence split counts (kvb_pipe.cu)
-    if (a.G > 4 || a.svd_logits) return cudaErrorNotSupported;
-    switch (nks) {
-      case 0: fn = (const void*)k5_attend_pipe<4, 0>; break;
-      case 10: fn = (const void*)k5_attend_pipe<4, 10>; break;
-      default: return cudaErrorNotSupported;
-    }
-    p.s_main = a.s_main;
-    p.s_tail = a.s_tail;
-    p.n_main = a.n_main;
-    p.scan_done = a.scan_done;
-    p.n_scan = a.n_scan;
-    p.sel_done = s->pipe_ctr + B;
-    p.cand_cnt = s->pipe_ctr + 2 * B;
-    p.sel_bm = s->pipe_bm;
-    p.cand = s->pipe_cand;
-    p.cand_cap = kPipeCandCap;
-    grid = dim3(a.n_main * a.s_main + (B - a.n_main) * a.s_tail, 1);
-    pa.bm_clear = s->pipe_bm;
-    pa.Wc = s->Wc;
-    pa.nB = B;
-    pa.ctr_clear = s->pipe_ctr;
-    pa.s_main = a.s_main;
-    pa.s_tail = a.s_tail;
-    pa.n_main = a.n_main;
-  }
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
@@ -1225,8 +1048,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
-                            (const float*)p.po, p.Slay, H * a.G, p.out, p.lse,
-                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr, pa);
+                            (const float*)p.po, g.splits, H * a.G, p.out, p.lse,
+                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr);
   return cudaGetLastError();
 }
 

@@ -81,91 +81,13 @@ __device__ __forceinline__ void fuse_mbar_wait0(uint64_t* b) {
       : "memory");
 }
 
-// Second half of the selection, shared by the per-CTA prologue and the
-// cooperative (pipelined) one: sbm already holds every key above the
-// threshold bin tb; sk/si hold the nc keys (and ids) inside it, kb of which
-// must be taken. Marks the K-th key T's winners: keys above T, then the
-// lowest ids among the ties. With nc > cap (the candidates did not fit) the
-// same bisection runs block-wide over every score of the bin in sc[0, M).
-static __device__ void resolve_threshold_bin(const float* __restrict__ sc, int M, uint32_t tb, int kb,
-                                      uint32_t* sbm, const uint32_t* sk, const int32_t* si, int nc,
-                                      int cap, int* red, uint64_t* tr = nullptr) {
-  __shared__ int s_gt, s_eq;
-  __shared__ uint32_t s_T;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  if (nc <= cap) {
-    {
-      __shared__ int khist[128];
-      uint32_t T0;
-      int gt, eq;
-      block_kth_key([&](int i) { return sk[i]; }, nc, tb << 21, kb, khist, red, &T0, &gt, &eq);
-      if (tid == 0) {
-        s_T = T0;
-        s_gt = gt;
-        s_eq = eq;
-      }
-    }
-    __syncthreads();
-    sel_stamp(tr, 2);
-    const uint32_t T = s_T;
-    const int need = kb - s_gt;
-    const bool all_ties = need == s_eq;
-    for (int i = tid; i < nc; i += nthr) {
-      const uint32_t k = sk[i];
-      bool take = k > T || (all_ties && k == T);
-      if (!take && k == T) {  // the `need` lowest ids among the ties
-        int rank = 0;
-        for (int j = 0; j < nc; ++j) rank += (sk[j] == T && si[j] < si[i]) ? 1 : 0;
-        take = rank < need;
-      }
-      if (take) atomicOr(sbm + (si[i] >> 5), 1u << (si[i] & 31));
-    }
-  } else {
-    // overflow: the same bisection block-wide over every score of the bin
-    uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
-    while (lo < hi) {
-      const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
-      int c = 0;
-      for (int i = tid; i < M; i += nthr) {
-        const uint32_t k = score_key(__ldcg(sc + i));
-        c += ((k >> 21) == tb && k >= mid) ? 1 : 0;
-      }
-      int tot;
-      block_excl_scan(c, red, &tot);
-      if (tot >= kb) lo = mid;
-      else hi = mid - 1u;
-    }
-    const uint32_t T = lo;
-    int gt = 0;
-    for (int i = tid; i < M; i += nthr) {
-      const uint32_t k = score_key(__ldcg(sc + i));
-      if ((k >> 21) == tb && k > T) {
-        ++gt;
-        atomicOr(sbm + (i >> 5), 1u << (i & 31));
-      }
-    }
-    int gtot;
-    block_excl_scan(gt, red, &gtot);
-    const int need = kb - gtot;
-    int taken = 0;
-    for (int base = 0; base < M && taken < need; base += nthr) {  // ascending ids
-      const int i = base + tid;
-      const bool eq = i < M && score_key(__ldcg(sc + i)) == T;
-      int tot;
-      const int ex = block_excl_scan(eq ? 1 : 0, red, &tot);
-      if (eq && taken + ex < need) atomicOr(sbm + (i >> 5), 1u << (i & 31));
-      taken += tot;
-    }
-  }
-  __syncthreads();
-}
-
-static __device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
+__device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
                                    uint32_t* sbm, uint32_t* sk, int32_t* si, int cap, int* red,
                                    uint64_t* tr = nullptr, const float* stage = nullptr,
                                    uint64_t* stage_bar = nullptr, int dbg_copy_only = 0) {
-  __shared__ int s_tb, s_kb, s_nc;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  __shared__ int s_tb, s_kb, s_nc, s_gt, s_eq;
+  __shared__ uint32_t s_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
   const int W = (M + 31) >> 5;
   for (int w = tid; w < W; w += nthr) sbm[w] = 0u;
   if (tid == 0) {
@@ -253,7 +175,71 @@ static __device__ void select_topk_shared(const float* __restrict__ sc, int M, c
   }
   __syncthreads();
   sel_stamp(tr, 1);
-  resolve_threshold_bin(sc, M, tb, s_kb, sbm, sk, si, s_nc, cap, red, tr);
+  const int nc = s_nc, kb = s_kb;
+  if (nc <= cap) {
+    {
+      __shared__ int khist[128];
+      uint32_t T0;
+      int gt, eq;
+      block_kth_key([&](int i) { return sk[i]; }, nc, tb << 21, kb, khist, red, &T0, &gt, &eq);
+      if (tid == 0) {
+        s_T = T0;
+        s_gt = gt;
+        s_eq = eq;
+      }
+    }
+    __syncthreads();
+    sel_stamp(tr, 2);
+    const uint32_t T = s_T;
+    const int need = kb - s_gt;
+    const bool all_ties = need == s_eq;
+    for (int i = tid; i < nc; i += nthr) {
+      const uint32_t k = sk[i];
+      bool take = k > T || (all_ties && k == T);
+      if (!take && k == T) {  // the `need` lowest ids among the ties
+        int rank = 0;
+        for (int j = 0; j < nc; ++j) rank += (sk[j] == T && si[j] < si[i]) ? 1 : 0;
+        take = rank < need;
+      }
+      if (take) atomicOr(sbm + (si[i] >> 5), 1u << (si[i] & 31));
+    }
+  } else {
+    // overflow: the same bisection block-wide over every score of the bin
+    uint32_t lo = tb << 21, hi = lo | 0x1fffffu;
+    while (lo < hi) {
+      const uint32_t mid = lo + ((hi - lo + 1u) >> 1);
+      int c = 0;
+      for (int i = tid; i < M; i += nthr) {
+        const uint32_t k = score_key(__ldcg(sc + i));
+        c += ((k >> 21) == tb && k >= mid) ? 1 : 0;
+      }
+      int tot;
+      block_excl_scan(c, red, &tot);
+      if (tot >= kb) lo = mid;
+      else hi = mid - 1u;
+    }
+    const uint32_t T = lo;
+    int gt = 0;
+    for (int i = tid; i < M; i += nthr) {
+      const uint32_t k = score_key(__ldcg(sc + i));
+      if ((k >> 21) == tb && k > T) {
+        ++gt;
+        atomicOr(sbm + (i >> 5), 1u << (i & 31));
+      }
+    }
+    int gtot;
+    block_excl_scan(gt, red, &gtot);
+    const int need = kb - gtot;
+    int taken = 0;
+    for (int base = 0; base < M && taken < need; base += nthr) {  // ascending ids
+      const int i = base + tid;
+      const bool eq = i < M && score_key(__ldcg(sc + i)) == T;
+      int tot;
+      const int ex = block_excl_scan(eq ? 1 : 0, red, &tot);
+      if (eq && taken + ex < need) atomicOr(sbm + (i >> 5), 1u << (i & 31));
+      taken += tot;
+    }
+  }
   __syncthreads();
   sel_stamp(tr, 3);
   if (tr && threadIdx.x == 0) tr[7] = (uint64_t)s_nc;  // candidates in the threshold bin

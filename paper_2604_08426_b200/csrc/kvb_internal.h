@@ -37,10 +37,6 @@ struct kvb_store {
   // by K2b after use (no memset nodes in the decode step). One decode step per
   // store at a time (the store's side stream and events are per store too).
   uint32_t* k2_hist = nullptr;     // [B][2048] top-11-bit key histogram
-  // pipelined layer (kvb_pipe.cu) scratch, zero between steps (re-zeroed by the merge)
-  int* pipe_ctr = nullptr;         // [3][B]: scan_done, sel_done, cand_cnt
-  uint32_t* pipe_bm = nullptr;     // [B][Wc] winner bitmaps
-  uint64_t* pipe_cand = nullptr;   // [B][kPipeCandCap] threshold-bin candidates
   int32_t* k2_meta = nullptr;      // [B][4] threshold bin / counts
   int32_t* k2_overflow = nullptr;  // [B]
   bool k2_dirty = false;           // a failed launch may have left scratch dirty
@@ -85,7 +81,6 @@ int resident_ctas(const void* func, int threads, size_t smem);
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, uint32_t* hist, cudaStream_t st, bool pdl = false);
 constexpr int kTopHistBins = 2048;
-constexpr int kPipeCandCap = 4096;  // threshold-bin candidates per sequence (pipelined layer)
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);
 bool higgs_tc_supported(const kvb_store* s);
@@ -136,6 +131,9 @@ cudaError_t launch_union_sorted(const kvb_store* s, const int32_t* chunk_ids, in
 // while its predecessor drains; it must griddepcontrol.wait before reading
 // the predecessor's output.
 bool pdl_enabled();
+// Slow-tier (resident_exact: tiered) K/V rows of a token list -> float32 (kvb_tier.cu).
+cudaError_t launch_gather_kv(const kvb_store* s, int b, const int32_t* tok, int n,
+                             int resident_exact, float* k_out, float* v_out, cudaStream_t st);
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        void** args);
 
@@ -195,28 +193,10 @@ struct BulkLaunch {
   int32_t* tok_out = nullptr;   // mode 1: sorted token union output [B][tcap]
   int32_t* ntok_out = nullptr;  // [B]
   int tcap = 0;
-  // pipelined layer (kvb_pipe.cu): attention co-resident with k1_stream,
-  // per-sequence split counts, cooperative selection through store scratch
-  int pipe = 0;
-  int s_main = 0, s_tail = 0, n_main = 0;
-  size_t smem_cap = 0;
-  const int* scan_done = nullptr;
-  int n_scan = 0;
-  int slay = 0;  // split stride of the partials (0: splits)
 };
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K = 0);
 int attend_bulk_splits(const kvb_store* s, int positions_cap);
 cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStream_t st);
-// pipelined dense layer (kvb_pipe.cu): prep -> k1_stream -> k5_attend_pipe -> merge
-bool pipe_supported(const kvb_store* s, int G, int K);
-bool attend_pipe_fits(const kvb_store* s, int G, int K, int splits, size_t smem_cap);
-cudaError_t launch_pipe_layer(const kvb_store* s, const struct AttendLaunch& a, int K, float* scores,
-                              int32_t* chunk_out, cudaStream_t st);
-bool stream_scan_supported(const kvb_store* s);
-size_t stream_scan_smem(int E, int nst);
-int stream_scan_ctas();
-cudaError_t launch_stream_scan(const kvb_store* s, const float* q, int G, float* scores,
-                               uint32_t* hist, int* done, int nst, cudaStream_t st);
 // decode-step attention over residents + selected chunks (chunk ids [B][K])
 cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, const int32_t* chunk_ids,
                                  int K, cudaStream_t st, const float* sel_scores = nullptr,

@@ -294,6 +294,21 @@ class DeviceStore:
                 "kvb_residuals_dequantized")
         return out
 
+    def gather_kv(self, seq: int, token_ids: torch.Tensor, resident_exact: bool = True):
+        """Tier read of an explicit token list of sequence ``seq``: float32
+        K and V [n, Hkv, D] (kvstore.py:281-291 gather_kv with
+        ``resident_exact``; kvstore.py:257-279 load_chunks' slow-tier rows
+        without)."""
+        if token_ids.dtype != torch.int32 or not token_ids.is_cuda:
+            raise ValueError("token_ids must be a CUDA int32 tensor")
+        tok = token_ids.contiguous()
+        n = int(tok.numel())
+        k = torch.empty((n, self.heads, self.dim), dtype=torch.float32, device="cuda")
+        v = torch.empty_like(k)
+        L.check(self.lib.kvb_gather_kv(self.h, seq, _ptr(tok), n, int(resident_exact), _ptr(k),
+                                       _ptr(v), _stream()), "kvb_gather_kv")
+        return k, v
+
     # ----------------------------------------------------------------- decode
     def score(self, q: torch.Tensor, aggregation: str = "sum", out: torch.Tensor | None = None):
         """Landmark scores [B, C] float32 (selection.py:83-84)."""

@@ -223,7 +223,101 @@ def needle_case():
     save("needles", **arr)
 
 
+def tier_io_case():
+    """load_chunks / gather_kv rows (kvstore.py:257-291) of a per-head SVD
+    store and of an exact store, and KVT1 byte streams written by kvlab's
+    write_kvt (numerics.py:151-162) with the reader's error cases."""
+    import tempfile
+    attention, kvstore, numerics, quantization, selection, workload = _kvlab()
+    B = kvstore.BudgetConfig
+    arr = {}
+    k = rand((2, 203, 16), 40, 0.5)
+    v = rand((2, 203, 16), 41, 0.5)
+    arr["keys"], arr["values"] = k, v
+    chunks = np.asarray([0, 5, 7, 25, 3], dtype=np.int64)
+    arr["chunks"] = chunks
+    arr["tokens"] = np.asarray([0, 1, 9, 40, 41, 100, 190, 199, 202], dtype=np.int64)
+    for tag, slow in (("svd", quantization.scheme_svd(6, 16)), ("none", quantization.scheme_none())):
+        st = kvstore.build_store(k, v, 8, quantization.scheme_none(), budget=B(0.1, 24, 8),
+                                 slow_tier_scheme=slow)
+        lk, lv, tr = st.load_chunks(chunks)
+        arr[f"{tag}_load_k"], arr[f"{tag}_load_v"] = lk, lv
+        arr[f"{tag}_loaded"] = np.int64(tr.tokens_loaded_from_slow_tier)
+        arr[f"{tag}_resident_bits"] = np.asarray(
+            [tr.fast_tier_resident_bits.numerator, tr.fast_tier_resident_bits.denominator])
+        gk, gv = st.gather_kv(arr["tokens"])
+        arr[f"{tag}_gather_k"], arr[f"{tag}_gather_v"] = gk, gv
+        arr[f"{tag}_resident"] = st.resident_token_ids.astype(np.int64)
+        if tag == "svd":
+            for h in range(2):
+                blk = quantization.quantize(k[h], slow)
+                halves = blk.codes.view(np.float16)
+                arr[f"left16_{h}"] = halves[: 203 * 6].reshape(203, 6).copy()
+                arr[f"right16_{h}"] = halves[203 * 6:].reshape(6, 16).copy()
+    with tempfile.TemporaryDirectory() as td:
+        for i, x in enumerate([rand((3, 5, 4), 42), rand((7,), 43), np.float32(2.5)]):
+            path = os.path.join(td, f"t{i}.kvt")
+            numerics.write_kvt(path, x)
+            with open(path, "rb") as f:
+                arr[f"kvt_bytes_{i}"] = np.frombuffer(f.read(), dtype=np.uint8).copy()
+            arr[f"kvt_array_{i}"] = np.asarray(x, dtype=np.float32)
+        good = arr["kvt_bytes_0"].tobytes()
+        bad = {"magic": b"KVT2" + good[4:], "short_header": good[:6],
+               "short_extents": good[:12], "payload": good[:-4], "extra": good + b"\0\0\0\0"}
+        for name, blob in bad.items():
+            path = os.path.join(td, f"bad_{name}.kvt")
+            with open(path, "wb") as f:
+                f.write(blob)
+            try:
+                numerics.read_kvt(path)
+                arr[f"kvtbad_{name}_raises"] = np.int64(0)
+            except numerics.KvtFormatError:
+                arr[f"kvtbad_{name}_raises"] = np.int64(1)
+            arr[f"kvtbad_{name}"] = np.frombuffer(blob, dtype=np.uint8).copy()
+    save("tier_io", **arr)
+
+
+def harness_case():
+    """kvlab's own harness.run_grid_point (harness.py:96-135) rows on small
+    planted-needle workloads: the numbers the patched shim must reproduce."""
+    attention, kvstore, numerics, quantization, selection, workload = _kvlab()
+    from kvlab import harness
+    B = kvstore.BudgetConfig
+    q = quantization
+    spec = workload.WorkloadSpec(n_tokens=8192, kv_heads=2, query_heads_per_group=2, head_dim=64,
+                                 n_needles=16, decode_steps=2, seed=0)
+    schemes = {
+        "none_c8": harness.SchemeSpec("none_c8", q.scheme_none(), 8, None, q.scheme_none()),
+        "higgs2_c1": harness.SchemeSpec("higgs2_c1", q.scheme_higgs(2), 1, None, q.scheme_none()),
+        "higgs4_c2": harness.SchemeSpec("higgs4_c2", q.scheme_higgs(4), 2, None, q.scheme_none()),
+        "svd32_c8": harness.SchemeSpec("svd32_c8", q.scheme_none(), 8, None, q.scheme_svd(32, 64)),
+        "res_c8": harness.SchemeSpec("res_c8", q.scheme_higgs(4), 8, q.scheme_higgs(1),
+                                     q.scheme_none()),
+    }
+    cases = [("landmark", "none_c8", B(0.02, 64, 32)), ("landmark", "higgs2_c1", B(0.01, 0, 0)),
+             ("landmark", "higgs4_c2", B(0.01, 0, 0)), ("landmark", "svd32_c8", B(0.02, 64, 32)),
+             ("residual-topk", "res_c8", B(0.01, 0, 0)), ("oracle", "none_c8", B(0.01, 0, 0))]
+    wl = workload.generate(spec)
+    arr = {"keys_sum": np.float64(wl.keys.astype(np.float64).sum()),
+           "n_cases": np.int64(len(cases))}
+    for i, (policy, sid, bud) in enumerate(cases):
+        cfg = harness.ExperimentConfig(workload=spec, schemes=(schemes[sid],), budgets=(bud,),
+                                       policy=policy, seeds=(0,))
+        r, e, f = harness.run_grid_point(cfg, schemes[sid], bud, wl)
+        arr[f"c{i}_policy"] = np.str_(policy)
+        arr[f"c{i}_scheme"] = np.str_(sid)
+        arr[f"c{i}_budget"] = np.asarray([bud.sparse_fraction, bud.outlier_tokens, bud.local_window])
+        arr[f"c{i}_recall"] = np.asarray(r)
+        arr[f"c{i}_rel"] = np.asarray(e)
+        arr[f"c{i}_frac"] = np.asarray(f)
+    save("harness_rows", **arr)
+
+
 def main():
+    if len(sys.argv) > 1:  # regenerate the named cases only
+        for name in sys.argv[1:]:
+            globals()[name]()
+        return
     attention, kvstore, numerics, quantization, selection, workload = _kvlab()
     B = kvstore.BudgetConfig
     none, higgs = quantization.scheme_none, quantization.scheme_higgs
@@ -247,6 +341,8 @@ def main():
     shadowkv_case("shadowkv_concat", heads=4, n=1024, d=64, g=4, cs=8, rank=48,
                   budget=B(128 / 1024, 64, 32), seed=18)
     needle_case()
+    tier_io_case()
+    harness_case()
 
 
 if __name__ == "__main__":

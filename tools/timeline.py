@@ -1,6 +1,6 @@
 """In-graph kernel timeline of the decode step (CUPTI via torch.profiler).
 
-usage: python tools/timeline.py [--variant shadowkv|higgs2c1] [--layers 4] [--graph]
+usage: python tools/timeline.py [--variant shadowkv|higgs2c1] [--layers 4] [--eager]
 
 Builds `layers` layers like bench.py, captures one decode step (all layers) in
 a CUDA graph (or runs it eagerly), replays it under torch.profiler and prints
@@ -28,8 +28,6 @@ def main():
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--budget", type=int, default=2048)
     ap.add_argument("--eager", action="store_true")
-    ap.add_argument("--microbatches", type=int, default=1)
-    ap.add_argument("--overlap-sms", type=int, default=0)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     stores, (H, G, D) = bench.build_layers(a, 0)
@@ -37,30 +35,9 @@ def main():
     plans = [st.decode_plan(G, K) for st in stores]
     q = torch.randn((a.layers, a.batch, H, G, D), device="cuda")
     out = torch.empty_like(q)
-    mb = a.microbatches
-    Bm = a.batch // mb
-    mstreams = [torch.cuda.Stream() for _ in range(mb)]
-    if mb > 1 and a.overlap_sms:
-        astreams = [torch.cuda.Stream(priority=-1) for _ in range(mb)]
-        for l in range(a.layers):
-            for m in range(mb):
-                stores[l * mb + m].set_overlap(astreams[m], a.overlap_sms)
-
     def step():
-        if mb == 1:
-            for l in range(a.layers):
-                plans[l].run(q[l], out[l])
-            return
-        cur = torch.cuda.current_stream()
-        for s_ in mstreams:
-            s_.wait_stream(cur)
         for l in range(a.layers):
-            for m, s_ in enumerate(mstreams):
-                with torch.cuda.stream(s_):
-                    sl = slice(m * Bm, (m + 1) * Bm)
-                    plans[l * mb + m].run(q[l, sl], out[l, sl])
-        for s_ in mstreams:
-            cur.wait_stream(s_)
+            plans[l].run(q[l], out[l])
 
     step()
     torch.cuda.synchronize()
