@@ -94,6 +94,8 @@ typedef struct kvb_store_desc {
   int32_t svd_groups;  /* 1 = head-concatenated (ShadowKV), kv_heads = per head */
   int32_t offload_tier;  /* kvb_tier                                         */
   int32_t max_resident;  /* capacity of the fast tier, tokens per sequence   */
+  int32_t capacity_tokens; /* >= n_tokens: room for kvb_store_append (batch 1);
+                              0 = n_tokens (no appends)                      */
 } kvb_store_desc;
 
 typedef struct kvb_store kvb_store; /* opaque; owns device + pinned memory  */
@@ -180,6 +182,31 @@ kvb_status kvb_residuals_dequantized(kvb_store* store, float* out, void* stream)
  * (kvstore.py:281-291) -- resident tokens exact from the fast tier.        */
 kvb_status kvb_gather_kv(kvb_store* store, int32_t seq, const int32_t* token_ids, int32_t n,
                          int32_t resident_exact, float* k_out, float* v_out, void* stream);
+
+/* Decode-time append of one token (kvstore.py:295-305 ChunkedKVStore.append;
+ * SPEC.md:262): the token joins the growing tail chunk, the local window
+ * rolls, and the derived state is brought to exactly what a rebuild over the
+ * n+1 tokens gives -- incrementally on the device: the offload-tier row, the
+ * tail chunk's landmark (dense) or the trailing HIGGS landmark groups, the
+ * residual groups of the chunks whose landmark changed, the outlier cosines
+ * of those chunks followed by the greedy outlier choice over all chunks
+ * (kvstore.py:160-190), and the fast tier (outliers U local window).
+ * Batch-1 stores created with capacity_tokens > n_tokens.
+ * keys/values: device [1][n+1][kv_heads][head_dim] kv_dtype, the caller's
+ * K/V including the new token at position n (the fast tier copies exact
+ * rows from them). left16_row (SVD stores): device fp16 [svd_groups][r]
+ * factor row of the new token, or NULL when the caller re-factors and calls
+ * kvb_store_set_svd (the reference re-factors on every append).
+ * outliers_out (HOST, may be NULL, capacity n_chunks after the append)
+ * receives the new sorted outlier chunk ids, *n_outliers their count.
+ * Synchronises the stream (the greedy outlier choice runs on the host).    */
+typedef struct kvb_append_args {
+  int32_t outlier_tokens;   /* BudgetConfig.outlier_tokens (kvstore.py:36-38) */
+  int32_t local_window;     /* BudgetConfig.local_window                     */
+} kvb_append_args;
+kvb_status kvb_store_append(kvb_store* store, const void* keys, const void* values,
+                            const kvb_append_args* args, const void* left16_row,
+                            int32_t* outliers_out, int32_t* n_outliers, void* stream);
 
 /* ---- decode ------------------------------------------------------------- */
 

@@ -28,7 +28,8 @@ class StoreDesc(C.Structure):
                 ("landmark_kind", C.c_int32), ("landmark_higgs", HiggsDesc),
                 ("has_residual", C.c_int32), ("residual_higgs", HiggsDesc),
                 ("slow_kind", C.c_int32), ("svd_rank", C.c_int32), ("svd_groups", C.c_int32),
-                ("offload_tier", C.c_int32), ("max_resident", C.c_int32)]
+                ("offload_tier", C.c_int32), ("max_resident", C.c_int32),
+                ("capacity_tokens", C.c_int32)]
 
 
 class StoreInfo(C.Structure):
@@ -47,6 +48,10 @@ class ResidualArgs(C.Structure):
     _fields_ = [("queries_per_head", C.c_int32), ("k_tokens", C.c_int32),
                 ("n_candidates", C.c_int32), ("token_capacity", C.c_int32),
                 ("exact_scores", C.c_int32)]
+
+
+class AppendArgs(C.Structure):
+    _fields_ = [("outlier_tokens", C.c_int32), ("local_window", C.c_int32)]
 
 
 class AttendArgs(C.Structure):
@@ -81,6 +86,7 @@ SIGNATURES = [
     ("kvb_store_set_residuals_higgs", _I32, [_P, _P, _P, _P]),
     ("kvb_landmarks_dequantized", _I32, [_P, _P, _P]),
     ("kvb_residuals_dequantized", _I32, [_P, _P, _P]),
+    ("kvb_store_append", _I32, [_P, _P, _P, C.POINTER(AppendArgs), _P, _P, _P, _P]),
     ("kvb_gather_kv", _I32, [_P, _I32, _P, _I32, _I32, _P, _P, _P]),
     ("kvb_select", _I32, [_P, _P, C.POINTER(SelectArgs), _P, _P, _P, _P, _P, _I64, _P]),
     ("kvb_score_landmarks", _I32, [_P, _P, _I32, _I32, _P, _P]),

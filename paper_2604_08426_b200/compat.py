@@ -131,7 +131,7 @@ class ChunkedKVStore:
         self.offload = offload
         self._build()
 
-    def _build(self):
+    def _build(self, capacity: int | None = None):
         h, n, d = self.keys.shape
         slow = self.slow_tier_scheme
         groups = 1
@@ -142,10 +142,16 @@ class ChunkedKVStore:
                                landmark=self.landmark_scheme, residual=self.residual_scheme,
                                slow=slow, svd_groups=groups,
                                outlier_tokens=self.budget.outlier_tokens,
-                               local_window=self.budget.local_window, offload=self.offload)
-        self._k_dev = _to_dev_tokens(self.keys, self.dtype)
-        v_dev = _to_dev_tokens(self.values, self.dtype)
-        self.dev.build(self._k_dev, v_dev)
+                               local_window=self.budget.local_window, offload=self.offload,
+                               capacity=capacity)
+        cap = self.dev.capacity
+        # device K/V with room for appends (the fast tier and outlier scoring read them)
+        self._k_buf = torch.empty((1, cap, h, d), dtype=self.dtype, device="cuda")
+        self._v_buf = torch.empty_like(self._k_buf)
+        self._k_buf[:, :n] = _to_dev_tokens(self.keys, self.dtype)
+        self._v_buf[:, :n] = _to_dev_tokens(self.values, self.dtype)
+        self._k_dev = self._k_buf[:, :n]
+        self.dev.build(self._k_dev, self._v_buf[:, :n])
         torch.cuda.synchronize()
 
     # -- geometry (kvstore.py:98-123)
@@ -276,14 +282,28 @@ class ChunkedKVStore:
                 f.write(f"{key} = {val}\n")
 
     def append(self, new_keys, new_values) -> None:
-        """kvstore.py:295-305: one token per head joins the tail chunk; the
-        derived state is rebuilt on the device."""
+        """kvstore.py:295-305: one token per head joins the tail chunk. The
+        device store is updated in place (kvb_store_append: tail landmark or
+        trailing HIGGS groups, residuals, outliers, local window); an SVD slow
+        tier is re-factored over all n+1 keys as the reference does. The
+        device buffers double when full (amortised O(1) appends)."""
         nk = as_f32(new_keys, "new_keys").reshape(self.n_heads, 1, self.head_dim)
         nv = as_f32(new_values, "new_values").reshape(self.n_heads, 1, self.head_dim)
         self.keys = np.concatenate([self.keys, nk], axis=1)
         self.values = np.concatenate([self.values, nv], axis=1)
-        self.dev.close()
-        self._build()
+        n = self.keys.shape[1]
+        if n > self.dev.capacity:
+            self.dev.close()
+            self._build(capacity=2 * n)
+            return
+        self._k_buf[0, n - 1] = torch.from_numpy(nk[:, 0]).to("cuda", self.dtype)
+        self._v_buf[0, n - 1] = torch.from_numpy(nv[:, 0]).to("cuda", self.dtype)
+        self._k_dev = self._k_buf[:, :n]
+        kd, vd = self._k_dev.contiguous(), self._v_buf[:, :n].contiguous()
+        self.dev.append(kd, vd)
+        if self.slow_tier_scheme.kind == SVD:
+            self.dev.import_svd(*self.dev.svd_factors(kd))
+        torch.cuda.synchronize()
 
 
 def load_store(directory, **kwargs) -> ChunkedKVStore:

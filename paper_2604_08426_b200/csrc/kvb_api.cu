@@ -153,8 +153,8 @@ kvb_status dalloc(T** p, size_t count, const char* what) {
   return KVB_OK;
 }
 
-kvb_status setup_higgs(kvb_store* s, const kvb_higgs_desc& hd, int rows, kvb_higgs_dev* out,
-                       const char* which) {
+kvb_status setup_higgs(kvb_store* s, const kvb_higgs_desc& hd, int rows, int cap_rows,
+                       kvb_higgs_dev* out, const char* which) {
   const int D = s->d.head_dim;
   if (hd.d != 1 && hd.d != 2 && hd.d != 4)
     KVB_FAIL(KVB_EINVAL, std::string(which) + ": sub-vector dimension must be 1, 2 or 4");
@@ -179,7 +179,8 @@ kvb_status setup_higgs(kvb_store* s, const kvb_higgs_desc& hd, int rows, kvb_hig
   out->rows = hd.group / D;
   out->groups = (int)(((int64_t)rows * D + hd.group - 1) / hd.group);
   out->group_bytes = (hd.group / hd.d) * bits / 8;
-  const size_t G = (size_t)s->d.batch * s->d.kv_heads * out->groups;
+  const int cap_groups = (int)(((int64_t)cap_rows * D + hd.group - 1) / hd.group);
+  const size_t G = (size_t)s->d.batch * s->d.kv_heads * cap_groups;
   kvb_status st;
   if ((st = dalloc(&out->codebook, (size_t)hd.n * hd.d, "codebook")) != KVB_OK) return st;
   if ((st = dalloc(&out->signs, (size_t)hd.group, "signs")) != KVB_OK) return st;
@@ -271,6 +272,52 @@ kvb_status check_attend_shape(const kvb_store* s) {
 
 }  // namespace
 
+namespace {
+
+// kvstore.py:181-190 greedy fill over a per-chunk cosine array (shared by
+// kvb_choose_outliers and the append path).
+std::vector<int32_t> greedy_outliers(const double* per_chunk, int32_t C, int64_t n, int32_t cs,
+                                     int64_t budget) {
+  std::vector<int32_t> chosen;
+  if (budget <= 0 || C < 1) return chosen;  // kvstore.py:164-165
+  std::vector<int32_t> order(C);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return per_chunk[a] < per_chunk[b]; });
+  std::vector<int32_t> seq;
+  seq.reserve(C);
+  seq.push_back(0);
+  for (int32_t c : order)
+    if (c != 0) seq.push_back(c);
+  int64_t used = 0;
+  for (int32_t c : seq) {
+    const int64_t size = std::min<int64_t>(cs, n - (int64_t)c * cs);
+    if (used + size > budget) continue;  // skip, not stop (kvstore.py:186-187)
+    chosen.push_back(c);
+    used += size;
+  }
+  std::sort(chosen.begin(), chosen.end());
+  return chosen;
+}
+
+// device scratch released on every exit path
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  cudaError_t get(T** p, size_t count) {
+    cudaError_t e = cudaMallocAsync((void**)p, std::max<size_t>(count, 1) * sizeof(T), st);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+}  // namespace
+
 extern "C" {
 
 const char* kvb_last_error(void) { return g_err.c_str(); }
@@ -301,35 +348,44 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   } else if (d.slow_kind != KVB_SLOW_NONE) {
     KVB_FAIL(KVB_EUNSUPPORTED, "slow tier must be none or svd");
   }
-  if ((int64_t)d.n_tokens > (1ll << 26)) KVB_FAIL(KVB_EUNSUPPORTED, "n_tokens too large");
+  if ((int64_t)d.n_tokens > (1ll << 26) || (int64_t)d.capacity_tokens > (1ll << 26))
+    KVB_FAIL(KVB_EUNSUPPORTED, "n_tokens too large");
+  if (d.capacity_tokens != 0 && d.capacity_tokens < d.n_tokens)
+    KVB_FAIL(KVB_EINVAL, "capacity_tokens must be 0 or >= n_tokens");
+  if (d.capacity_tokens > d.n_tokens && d.batch != 1)
+    KVB_FAIL(KVB_EUNSUPPORTED, "append capacity needs a batch-1 store");
   auto* s = new kvb_store();
   s->d = d;
+  s->cap_n = std::max(d.n_tokens, d.capacity_tokens);
   s->C = (d.n_tokens + d.chunk_size - 1) / d.chunk_size;
   s->E = d.kv_heads * d.head_dim;
   s->W = (d.n_tokens + 31) / 32;
   s->esz = d.kv_dtype == KVB_BF16 ? 2 : 4;
-  const size_t B = d.batch, E = s->E, n = d.n_tokens;
+  // allocations are sized for the capacity (batch 1 when it exceeds n_tokens,
+  // so the per-sequence strides never matter)
+  const size_t B = d.batch, E = s->E, n = s->cap_n;
+  const int Ccap = (s->cap_n + d.chunk_size - 1) / d.chunk_size, Wcap = (s->cap_n + 31) / 32;
   kvb_status st = KVB_OK;
   auto bail = [&](kvb_status code) {
     free_store(s);
     return code;
   };
   if (d.landmark_kind == KVB_LM_DENSE) {
-    if ((st = dalloc((char**)&s->lm_dense, B * s->C * E * s->esz, "landmarks")) != KVB_OK) return bail(st);
+    if ((st = dalloc((char**)&s->lm_dense, B * Ccap * E * s->esz, "landmarks")) != KVB_OK) return bail(st);
   } else if (d.landmark_kind == KVB_LM_HIGGS) {
-    if ((st = setup_higgs(s, d.landmark_higgs, s->C, &s->lm_h, "landmark")) != KVB_OK) return bail(st);
+    if ((st = setup_higgs(s, d.landmark_higgs, s->C, Ccap, &s->lm_h, "landmark")) != KVB_OK) return bail(st);
   } else {
     return bail((set_error("unknown landmark kind"), KVB_EINVAL));
   }
   if (d.has_residual) {
-    if ((st = setup_higgs(s, d.residual_higgs, d.n_tokens, &s->res_h, "residual")) != KVB_OK)
+    if ((st = setup_higgs(s, d.residual_higgs, d.n_tokens, s->cap_n, &s->res_h, "residual")) != KVB_OK)
       return bail(st);
   }
   const size_t R = d.max_resident;
   if ((st = dalloc(&s->res_ids, B * R, "resident ids")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->res_count, B, "resident counts")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->res_bitmap, B * s->W, "resident bitmap")) != KVB_OK) return bail(st);
-  if ((st = dalloc(&s->res_prefix, B * s->W, "resident prefix")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->res_bitmap, B * Wcap, "resident bitmap")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->res_prefix, B * Wcap, "resident prefix")) != KVB_OK) return bail(st);
   if ((st = dalloc((char**)&s->res_k, B * R * E * s->esz, "resident K")) != KVB_OK) return bail(st);
   if ((st = dalloc((char**)&s->res_v, B * R * E * s->esz, "resident V")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_hist, B * kTopHistBins, "K2 histogram")) != KVB_OK) return bail(st);
@@ -339,8 +395,8 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   cudaMemset(s->k2_hist, 0, B * kTopHistBins * sizeof(uint32_t));
   cudaMemset(s->k2_meta, 0, B * 4 * sizeof(int32_t));
   cudaMemset(s->res_count, 0, B * sizeof(int32_t));
-  cudaMemset(s->res_bitmap, 0, B * s->W * sizeof(uint32_t));
-  cudaMemset(s->res_prefix, 0, B * s->W * sizeof(int32_t));
+  cudaMemset(s->res_bitmap, 0, B * Wcap * sizeof(uint32_t));
+  cudaMemset(s->res_prefix, 0, B * Wcap * sizeof(int32_t));
   const size_t off_bytes = B * n * E * s->esz;
   const bool need_k = d.slow_kind == KVB_SLOW_NONE;
   if (d.offload_tier == KVB_TIER_HOST_MAPPED) {
@@ -481,24 +537,7 @@ kvb_status kvb_choose_outliers(const double* per_chunk, int32_t C, int32_t n, in
   *out_count = 0;
   if (budget <= 0) return KVB_OK;  // kvstore.py:164-165
   if (!per_chunk || !out_chunks || C < 1 || cs < 1) KVB_FAIL(KVB_EINVAL, "bad outlier arguments");
-  std::vector<int32_t> order(C);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t a, int32_t b) { return per_chunk[a] < per_chunk[b]; });
-  std::vector<int32_t> seq;
-  seq.reserve(C);
-  seq.push_back(0);
-  for (int32_t c : order)
-    if (c != 0) seq.push_back(c);
-  std::vector<int32_t> chosen;
-  int64_t used = 0;
-  for (int32_t c : seq) {
-    const int64_t size = std::min<int64_t>(cs, (int64_t)n - (int64_t)c * cs);
-    if (used + size > budget) continue;  // skip, not stop (kvstore.py:186-187)
-    chosen.push_back(c);
-    used += size;
-  }
-  std::sort(chosen.begin(), chosen.end());
+  const std::vector<int32_t> chosen = greedy_outliers(per_chunk, C, n, cs, budget);
   for (size_t i = 0; i < chosen.size(); ++i) out_chunks[i] = chosen[i];
   *out_count = (int32_t)chosen.size();
   return KVB_OK;
@@ -536,6 +575,123 @@ kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* val
     if (!keys) KVB_FAIL(KVB_EINVAL, "slow tier 'none' needs keys");
     KVB_CUDA(cudaMemcpyAsync(s->off_k_dev, keys, bytes, cudaMemcpyDefault, st), "offload K");
   }
+  return KVB_OK;
+}
+
+kvb_status kvb_store_append(kvb_store* s, const void* keys, const void* values,
+                            const kvb_append_args* a, const void* left16_row,
+                            int32_t* outliers_out, int32_t* n_outliers, void* stream) {
+  if (!s || !keys || !values || !a) KVB_FAIL(KVB_EINVAL, "null argument");
+  if (s->d.batch != 1) KVB_FAIL(KVB_EUNSUPPORTED, "append needs a batch-1 store");
+  if (s->d.n_tokens + 1 > s->cap_n) KVB_FAIL(KVB_EINVAL, "store capacity exhausted (capacity_tokens)");
+  if (a->outlier_tokens < 0 || a->local_window < 0)
+    KVB_FAIL(KVB_EINVAL, "outlier_tokens and local_window must be >= 0");
+  if (a->outlier_tokens > 0 && s->d.chunk_size > 64)
+    KVB_FAIL(KVB_EUNSUPPORTED, "outlier scoring needs chunk_size <= 64");
+  cudaStream_t st = as_stream(stream);
+  const int cs = s->d.chunk_size, D = s->d.head_dim, H = s->d.kv_heads;
+  const size_t E = s->E, esz = s->esz;
+  const int n0 = s->d.n_tokens, n1 = n0 + 1;
+  const int C0 = s->C, C1 = (n1 + cs - 1) / cs;
+  // new geometry (every launcher below reads it)
+  s->d.n_tokens = n1;
+  s->C = C1;
+  s->W = (n1 + 31) / 32;
+  s->Wc = (C1 + 31) / 32;
+  Scratch sc(st);
+  // offload tier row (and the SVD factor row when given)
+  const char* kb = static_cast<const char*>(keys);
+  const char* vb = static_cast<const char*>(values);
+  KVB_CUDA(cudaMemcpyAsync(static_cast<char*>(s->off_v_dev) + (size_t)n0 * E * esz,
+                           vb + (size_t)n0 * E * esz, E * esz, cudaMemcpyDefault, st), "append V row");
+  if (s->off_k)
+    KVB_CUDA(cudaMemcpyAsync(static_cast<char*>(s->off_k_dev) + (size_t)n0 * E * esz,
+                             kb + (size_t)n0 * E * esz, E * esz, cudaMemcpyDefault, st), "append K row");
+  if (s->svd_left && left16_row) {
+    const size_t gr = (size_t)s->d.svd_groups * s->d.svd_rank;
+    KVB_CUDA(cudaMemcpyAsync(s->svd_left + (size_t)n0 * gr, left16_row, gr * 2, cudaMemcpyDefault, st),
+             "append factor row");
+  }
+  // landmarks: the tail chunk (dense) or the trailing HIGGS groups it falls in
+  int c_lo = C1 - 1;  // first chunk whose dequantised landmark changed
+  if (s->d.landmark_kind == KVB_LM_DENSE) {
+    KVB_CUDA(launch_chunk_means(s, keys, s->lm_dense, nullptr, st, c_lo), "tail landmark");
+  } else {
+    kvb_higgs_dev& h = s->lm_h;
+    const int g_old = h.groups, g_new = (int)(((int64_t)C1 * D + h.group - 1) / h.group);
+    if (g_new != g_old) {
+      KVB_CUDA(launch_higgs_relayout(s, h, g_old, g_new, st), "landmark relayout");
+      h.groups = g_new;
+    }
+    const int g0 = c_lo / h.rows;
+    c_lo = g0 * h.rows;
+    float* means = nullptr;
+    KVB_CUDA(sc.get(&means, (size_t)H * C1 * D), "append scratch");
+    KVB_CUDA(launch_chunk_means(s, keys, nullptr, means, st, c_lo), "tail landmark means");
+    KVB_CUDA(launch_higgs_quantize(s, h, means, C1, st, g0), "tail landmark quantize");
+  }
+  // dequantised landmarks [C1][H][D] from chunk c_lo on (residuals, cosines)
+  float* lm = nullptr;
+  const bool need_lm = s->d.has_residual || a->outlier_tokens > 0;
+  if (need_lm) {
+    KVB_CUDA(sc.get(&lm, (size_t)C1 * E), "append scratch");
+    if (s->d.landmark_kind == KVB_LM_DENSE)
+      KVB_CUDA(launch_dense_to_f32(s, lm, st), "landmark widen");
+    else
+      KVB_CUDA(launch_higgs_dequant(s, s->lm_h, C1, lm, st, c_lo / s->lm_h.rows), "landmark dequant");
+  }
+  // residuals of every token whose landmark changed (kvstore.py:133-140)
+  if (s->d.has_residual) {
+    kvb_higgs_dev& h = s->res_h;
+    const int g_old = h.groups, g_new = (int)(((int64_t)n1 * D + h.group - 1) / h.group);
+    if (g_new != g_old) {
+      KVB_CUDA(launch_higgs_relayout(s, h, g_old, g_new, st), "residual relayout");
+      h.groups = g_new;
+    }
+    const int g0 = (c_lo * cs) / h.rows;
+    float* src = nullptr;
+    KVB_CUDA(sc.get(&src, (size_t)H * n1 * D), "append scratch");
+    KVB_CUDA(launch_residual_source(s, keys, lm, src, st, g0 * h.rows), "residual source");
+    KVB_CUDA(launch_higgs_quantize(s, h, src, n1, st, g0), "residual quantize");
+  }
+  // outliers: cosines of the changed chunks (every chunk the first time),
+  // greedy choice over all chunks on the host mirror
+  std::vector<int32_t> outl;
+  if (a->outlier_tokens > 0) {
+    const int cc = (int)s->pc_host.size() == C0 && C0 > 0 ? std::min(c_lo, C0) : 0;
+    double* pcd = nullptr;
+    KVB_CUDA(sc.get(&pcd, (size_t)C1), "append scratch");
+    if (cc == 0 && s->d.landmark_kind != KVB_LM_DENSE && c_lo > 0) {
+      // first append of a HIGGS store: every landmark group is needed
+      KVB_CUDA(launch_higgs_dequant(s, s->lm_h, C1, lm, st, 0), "landmark dequant");
+    }
+    KVB_CUDA(launch_chunk_cosine(s, keys, lm, pcd, st, cc), "append cosine");
+    s->pc_host.resize(C1);
+    KVB_CUDA(cudaMemcpyAsync(s->pc_host.data() + cc, pcd + cc, sizeof(double) * (C1 - cc),
+                             cudaMemcpyDeviceToHost, st), "cosine readback");
+    KVB_CUDA(cudaStreamSynchronize(st), "append sync");
+    outl = greedy_outliers(s->pc_host.data(), C1, n1, cs, a->outlier_tokens);
+  }
+  s->outliers = outl;
+  // fast tier: outlier-chunk tokens U local window (kvstore.py:230-240)
+  std::vector<int32_t> ids;
+  for (int32_t c : outl)
+    for (int t = c * cs; t < std::min(n1, (c + 1) * cs); ++t) ids.push_back(t);
+  const int w = std::min(a->local_window, n1);
+  for (int t = n1 - w; t < n1; ++t) ids.push_back(t);
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  if ((int)ids.size() > s->d.max_resident)
+    KVB_FAIL(KVB_EINVAL, "resident set exceeds max_resident (outlier_tokens + local_window)");
+  const int32_t cnt = (int32_t)ids.size();
+  if (cnt) KVB_CUDA(cudaMemcpyAsync(s->res_ids, ids.data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, st),
+                    "resident ids");
+  KVB_CUDA(cudaMemcpyAsync(s->res_count, &cnt, sizeof(int32_t), cudaMemcpyHostToDevice, st), "resident count");
+  KVB_CUDA(launch_residency(s, keys, values, st), "residency");
+  KVB_CUDA(cudaStreamSynchronize(st), "append sync");  // host ids / count above
+  if (n_outliers) *n_outliers = (int32_t)outl.size();
+  if (outliers_out)
+    for (size_t i = 0; i < outl.size(); ++i) outliers_out[i] = outl[i];
   return KVB_OK;
 }
 

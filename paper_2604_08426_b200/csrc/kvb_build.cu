@@ -60,15 +60,16 @@ __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) {
 template <typename T>
 __global__ void k_chunk_means(const T* __restrict__ keys, T* __restrict__ out_dense,
                               float* __restrict__ out_f32, int B, int n, int H, int D, int cs,
-                              int C) {
-  const int E = H * D;
-  const size_t total = (size_t)B * C * E;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int e = idx % E;
-    const size_t bc = idx / E;
-    const int c = bc % C;
-    const int b = bc / C;
+                              int C, int c0) {
+  const int E = H * D, Cr = C - c0;  // chunks [c0, C) (append: the changed tail)
+  const size_t total = (size_t)B * Cr * E;
+  for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < total;
+       j += (size_t)gridDim.x * blockDim.x) {
+    const int e = j % E;
+    const size_t bc = j / E;
+    const int c = c0 + (int)(bc % Cr);
+    const int b = bc / Cr;
+    const size_t idx = ((size_t)b * C + c) * E + e;
     const int t0 = c * cs, t1 = min(t0 + cs, n);
     const T* k = keys + ((size_t)b * n + t0) * E + e;
     double s = (double)to_f32(k[0]);
@@ -95,14 +96,16 @@ __global__ void k_higgs_quantize(const float* __restrict__ src, int rows, int D,
                                  int GS, float root, const float* __restrict__ cb,
                                  const float* __restrict__ signs, int d, int ncb, int bits,
                                  int ngroups, int gbytes, uint8_t* __restrict__ codes,
-                                 float* __restrict__ scales, int B) {
+                                 float* __restrict__ scales, int B, int g0) {
   extern __shared__ float sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const size_t gid = (size_t)blockIdx.x * nw + warp;
-  if (gid >= (size_t)B * H * ngroups) return;
+  const size_t wid = (size_t)blockIdx.x * nw + warp;  // groups [g0, ngroups) of every (b, h)
+  const int gr = ngroups - g0;
+  if (wid >= (size_t)B * H * gr) return;
   float* xs = sm + (size_t)warp * GS;
-  const int gi = gid % ngroups;
-  const size_t bh = gid / ngroups;
+  const int gi = g0 + (int)(wid % gr);
+  const size_t bh = wid / gr;
+  const size_t gid = bh * ngroups + gi;
   const float* base = src + bh * (size_t)rows * D;
   const size_t limit = (size_t)rows * D;
   for (int i = lane; i < GS; i += 32) {
@@ -187,14 +190,16 @@ __global__ void k_higgs_factor(const uint8_t* __restrict__ codes, const float* _
 __global__ void k_higgs_dequant(const uint8_t* __restrict__ codes, const float* __restrict__ factor,
                                 const float* __restrict__ cb, const float* __restrict__ signs,
                                 int d, int bits, int GS, float root, int gbytes, int ngroups,
-                                int rows, int H, int D, int B, float* __restrict__ out) {
+                                int rows, int H, int D, int B, float* __restrict__ out, int g0) {
   extern __shared__ float sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const size_t gid = (size_t)blockIdx.x * nw + warp;
-  if (gid >= (size_t)B * H * ngroups) return;
+  const size_t wid = (size_t)blockIdx.x * nw + warp;
+  const int gr = ngroups - g0;
+  if (wid >= (size_t)B * H * gr) return;
   float* xs = sm + (size_t)warp * GS;
-  const int gi = gid % ngroups;
-  const size_t bh = gid / ngroups;
+  const int gi = g0 + (int)(wid % gr);
+  const size_t bh = wid / gr;
+  const size_t gid = bh * ngroups + gi;
   const int h = bh % H;
   const int b = bh / H;
   const uint8_t* gc = codes + gid * gbytes;
@@ -228,15 +233,16 @@ __global__ void k_higgs_dequant(const uint8_t* __restrict__ codes, const float* 
 template <typename T>
 __global__ void k_residual_source(const T* __restrict__ keys, const float* __restrict__ lm_dq,
                                   float* __restrict__ out, int B, int n, int H, int D, int cs,
-                                  int C) {
-  const int E = H * D;
-  const size_t total = (size_t)B * n * E;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int e = idx % E;
-    const size_t bt = idx / E;
-    const int t = bt % n;
-    const int b = bt / n;
+                                  int C, int t0) {
+  const int E = H * D, nr = n - t0;  // tokens [t0, n)
+  const size_t total = (size_t)B * nr * E;
+  for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < total;
+       j += (size_t)gridDim.x * blockDim.x) {
+    const int e = j % E;
+    const size_t bt = j / E;
+    const int t = t0 + (int)(bt % nr);
+    const int b = bt / nr;
+    const size_t idx = ((size_t)b * n + t) * E + e;
     const int h = e / D, dd = e - h * D;
     const float k = to_f32(keys[idx]);
     const float l = lm_dq[(((size_t)b * C + t / cs) * H + h) * D + dd];
@@ -248,11 +254,14 @@ __global__ void k_residual_source(const T* __restrict__ keys, const float* __res
 // One thread per (b, chunk) -- prefill only.
 template <typename T>
 __global__ void k_chunk_cosine(const T* __restrict__ keys, const float* __restrict__ lm_dq,
-                               double* __restrict__ out, int B, int n, int H, int D, int cs, int C) {
-  const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (idx >= (size_t)B * C) return;
-  const int c = idx % C;
-  const int b = idx / C;
+                               double* __restrict__ out, int B, int n, int H, int D, int cs, int C,
+                               int c0) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const int Cr = C - c0;  // chunks [c0, C)
+  if (j >= (size_t)B * Cr) return;
+  const int c = c0 + (int)(j % Cr);
+  const int b = j / Cr;
+  const size_t idx = (size_t)b * C + c;
   const int E = H * D;
   float tok[64];
   const int t0 = c * cs;
@@ -315,6 +324,27 @@ __global__ void k_residency(const int32_t* __restrict__ ids, const int32_t* __re
   }
 }
 
+// HIGGS state of a batch-1 store whose group count per head grew from g_old
+// to g_new (append): head h moves from h*g_old to h*g_new (new trailing
+// groups left for the quantizer). Reads `src` (a copy), writes `dst`.
+__global__ void k_higgs_relayout(const uint8_t* __restrict__ src_codes, const float* __restrict__ src_sc,
+                                 const float* __restrict__ src_fac, uint8_t* __restrict__ codes,
+                                 float* __restrict__ sc, float* __restrict__ fac, int H, int g_old,
+                                 int g_new, int gbytes) {
+  const size_t total = (size_t)H * g_old * gbytes;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t gi = i / gbytes, byte = i % gbytes;
+    const int h = gi / g_old, g = gi % g_old;
+    const size_t dst = (size_t)h * g_new + g;
+    codes[dst * gbytes + byte] = src_codes[i];
+    if (byte == 0) {
+      sc[dst] = src_sc[gi];
+      fac[dst] = src_fac[gi];
+    }
+  }
+}
+
 template <typename T>
 __global__ void k_to_f32(const T* __restrict__ x, float* __restrict__ y, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
@@ -331,30 +361,31 @@ int grid_for(size_t total, int threads) {
 }  // namespace
 
 cudaError_t launch_chunk_means(const kvb_store* s, const void* keys, void* out_dense,
-                               float* out_f32, cudaStream_t st) {
-  const size_t total = (size_t)s->d.batch * s->C * s->E;
+                               float* out_f32, cudaStream_t st, int c0) {
+  const size_t total = (size_t)s->d.batch * (s->C - c0) * s->E;
   count_launch();
   if (s->d.kv_dtype == KVB_BF16)
     k_chunk_means<__nv_bfloat16><<<grid_for(total, 256), 256, 0, st>>>(
         (const __nv_bfloat16*)keys, (__nv_bfloat16*)out_dense, out_f32, s->d.batch,
-        s->d.n_tokens, s->d.kv_heads, s->d.head_dim, s->d.chunk_size, s->C);
+        s->d.n_tokens, s->d.kv_heads, s->d.head_dim, s->d.chunk_size, s->C, c0);
   else
     k_chunk_means<float><<<grid_for(total, 256), 256, 0, st>>>(
         (const float*)keys, (float*)out_dense, out_f32, s->d.batch, s->d.n_tokens,
-        s->d.kv_heads, s->d.head_dim, s->d.chunk_size, s->C);
+        s->d.kv_heads, s->d.head_dim, s->d.chunk_size, s->C, c0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_higgs_quantize(const kvb_store* s, const kvb_higgs_dev& h, const float* src,
-                                  int rows, cudaStream_t st) {
+                                  int rows, cudaStream_t st, int g0) {
   const int warps = 4;
   const size_t groups = (size_t)s->d.batch * s->d.kv_heads * h.groups;
+  const size_t qgroups = (size_t)s->d.batch * s->d.kv_heads * (h.groups - g0);
   const size_t smem = (size_t)warps * h.group * sizeof(float);
   ensure_smem((const void*)k_higgs_quantize, smem);
   count_launch(2);
-  k_higgs_quantize<<<(unsigned)((groups + warps - 1) / warps), warps * 32, smem, st>>>(
+  k_higgs_quantize<<<(unsigned)((qgroups + warps - 1) / warps), warps * 32, smem, st>>>(
       src, rows, s->d.head_dim, s->d.kv_heads, h.group, (float)sqrt((double)h.group), h.codebook,
-      h.signs, h.d, h.n, h.bits, h.groups, h.group_bytes, h.codes, h.scales, s->d.batch);
+      h.signs, h.d, h.n, h.bits, h.groups, h.group_bytes, h.codes, h.scales, s->d.batch, g0);
   k_higgs_factor<<<(unsigned)((groups + 127) / 128), 128, 0, st>>>(
       h.codes, h.scales, h.codebook, h.d, h.bits, h.group, h.group_bytes, groups, h.factor);
   return cudaGetLastError();
@@ -369,45 +400,45 @@ cudaError_t launch_higgs_factor(const kvb_store* s, const kvb_higgs_dev& h, cuda
 }
 
 cudaError_t launch_higgs_dequant(const kvb_store* s, const kvb_higgs_dev& h, int rows, float* out,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int g0) {
   const int warps = 4;
-  const size_t groups = (size_t)s->d.batch * s->d.kv_heads * h.groups;
+  const size_t groups = (size_t)s->d.batch * s->d.kv_heads * (h.groups - g0);
   const size_t smem = (size_t)warps * h.group * sizeof(float);
   ensure_smem((const void*)k_higgs_dequant, smem);
   count_launch();
   k_higgs_dequant<<<(unsigned)((groups + warps - 1) / warps), warps * 32, smem, st>>>(
       h.codes, h.factor, h.codebook, h.signs, h.d, h.bits, h.group, (float)sqrt((double)h.group),
-      h.group_bytes, h.groups, rows, s->d.kv_heads, s->d.head_dim, s->d.batch, out);
+      h.group_bytes, h.groups, rows, s->d.kv_heads, s->d.head_dim, s->d.batch, out, g0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_residual_source(const kvb_store* s, const void* keys, const float* lm_dq,
-                                   float* out, cudaStream_t st) {
-  const size_t total = (size_t)s->d.batch * s->d.n_tokens * s->E;
+                                   float* out, cudaStream_t st, int t0) {
+  const size_t total = (size_t)s->d.batch * (s->d.n_tokens - t0) * s->E;
   count_launch();
   if (s->d.kv_dtype == KVB_BF16)
     k_residual_source<__nv_bfloat16><<<grid_for(total, 256), 256, 0, st>>>(
         (const __nv_bfloat16*)keys, lm_dq, out, s->d.batch, s->d.n_tokens, s->d.kv_heads,
-        s->d.head_dim, s->d.chunk_size, s->C);
+        s->d.head_dim, s->d.chunk_size, s->C, t0);
   else
     k_residual_source<float><<<grid_for(total, 256), 256, 0, st>>>(
         (const float*)keys, lm_dq, out, s->d.batch, s->d.n_tokens, s->d.kv_heads, s->d.head_dim,
-        s->d.chunk_size, s->C);
+        s->d.chunk_size, s->C, t0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chunk_cosine(const kvb_store* s, const void* keys, const float* lm_dq,
-                                double* out, cudaStream_t st) {
-  const size_t total = (size_t)s->d.batch * s->C;
+                                double* out, cudaStream_t st, int c0) {
+  const size_t total = (size_t)s->d.batch * (s->C - c0);
   count_launch();
   if (s->d.kv_dtype == KVB_BF16)
     k_chunk_cosine<__nv_bfloat16><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
         (const __nv_bfloat16*)keys, lm_dq, out, s->d.batch, s->d.n_tokens, s->d.kv_heads,
-        s->d.head_dim, s->d.chunk_size, s->C);
+        s->d.head_dim, s->d.chunk_size, s->C, c0);
   else
     k_chunk_cosine<float><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
         (const float*)keys, lm_dq, out, s->d.batch, s->d.n_tokens, s->d.kv_heads, s->d.head_dim,
-        s->d.chunk_size, s->C);
+        s->d.chunk_size, s->C, c0);
   return cudaGetLastError();
 }
 
@@ -425,6 +456,29 @@ cudaError_t launch_residency(const kvb_store* s, const void* keys, const void* v
         (const float*)keys, (const float*)values, (float*)s->res_k, (float*)s->res_v,
         s->d.n_tokens, s->E);
   return cudaGetLastError();
+}
+
+cudaError_t launch_higgs_relayout(const kvb_store* s, kvb_higgs_dev& h, int g_old, int g_new,
+                                  cudaStream_t st) {
+  const size_t H = s->d.kv_heads, nb = H * g_old * h.group_bytes;
+  uint8_t* tmp = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&tmp, ((nb + 15) & ~size_t(15)) + 2 * H * g_old * sizeof(float), st);
+  if (e != cudaSuccess) return e;
+  float* tsc2 = reinterpret_cast<float*>(tmp + ((nb + 15) & ~size_t(15)));
+  e = cudaMemcpyAsync(tmp, h.codes, nb, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(tsc2, h.scales, H * g_old * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(tsc2 + H * g_old, h.factor, H * g_old * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) {
+    count_launch();
+    k_higgs_relayout<<<grid_for(nb, 256), 256, 0, st>>>(tmp, tsc2, tsc2 + H * g_old, h.codes,
+                                                         h.scales, h.factor, (int)H, g_old, g_new,
+                                                         h.group_bytes);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(tmp, st);
+  return e;
 }
 
 cudaError_t launch_dense_to_f32(const kvb_store* s, float* out, cudaStream_t st) {

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/kvb.h"
 
@@ -22,6 +23,9 @@ struct kvb_higgs_dev {
 
 struct kvb_store {
   kvb_store_desc d{};
+  int cap_n = 0;      // token capacity (batch-1 append; == d.n_tokens otherwise)
+  std::vector<double> pc_host;  // per-chunk outlier cosine mirror (append), empty until used
+  std::vector<int32_t> outliers;  // current outlier chunks (append bookkeeping)
   int C = 0;          // chunks per sequence
   int E = 0;          // kv_heads * head_dim
   int W = 0;          // resident bitmap words per sequence
@@ -221,19 +225,25 @@ cudaError_t launch_recon_logits(const kvb_store* s, const float* q, int G, const
                                 int K, float* logits, cudaStream_t st);
 
 // ---- build ---------------------------------------------------------------
+// The trailing range arguments restrict a launcher to the part of the store an
+// append changed: chunks [c0, C), HIGGS groups [g0, groups) of every head,
+// tokens [t0, n). 0 = the whole store (prefill).
 cudaError_t launch_chunk_means(const kvb_store* s, const void* keys, void* out_dense,
-                               float* out_f32_headmajor, cudaStream_t st);
+                               float* out_f32_headmajor, cudaStream_t st, int c0 = 0);
 cudaError_t launch_higgs_quantize(const kvb_store* s, const kvb_higgs_dev& h, const float* src,
-                                  int rows_per_head, cudaStream_t st);
+                                  int rows_per_head, cudaStream_t st, int g0 = 0);
 cudaError_t launch_higgs_factor(const kvb_store* s, const kvb_higgs_dev& h, cudaStream_t st);
 cudaError_t launch_higgs_dequant(const kvb_store* s, const kvb_higgs_dev& h, int rows_per_head,
-                                 float* out_rowmajor, cudaStream_t st);
+                                 float* out_rowmajor, cudaStream_t st, int g0 = 0);
 cudaError_t launch_residual_source(const kvb_store* s, const void* keys, const float* lm_dq,
-                                   float* out_headmajor, cudaStream_t st);
+                                   float* out_headmajor, cudaStream_t st, int t0 = 0);
 cudaError_t launch_chunk_cosine(const kvb_store* s, const void* keys, const float* lm_dq,
-                                double* out, cudaStream_t st);
+                                double* out, cudaStream_t st, int c0 = 0);
 cudaError_t launch_residency(const kvb_store* s, const void* keys, const void* values,
                              cudaStream_t st);
+// batch-1 append: a HIGGS state's per-head group count grew g_old -> g_new
+cudaError_t launch_higgs_relayout(const kvb_store* s, kvb_higgs_dev& h, int g_old, int g_new,
+                                  cudaStream_t st);
 cudaError_t launch_dense_to_f32(const kvb_store* s, float* out, cudaStream_t st);
 
 }  // namespace kvb

@@ -62,7 +62,8 @@ class DeviceStore:
                  chunk_size: int, dtype=torch.float32,
                  landmark: SchemeDescriptor, residual: SchemeDescriptor | None = None,
                  slow: SchemeDescriptor | None = None, svd_groups: int = 1,
-                 outlier_tokens: int = 384, local_window: int = 32, offload: str = "hbm"):
+                 outlier_tokens: int = 384, local_window: int = 32, offload: str = "hbm",
+                 capacity: int | None = None):
         self.lib = L.load()
         slow = slow or SchemeDescriptor(kind=NONE)
         if landmark.kind not in (NONE, HIGGS):
@@ -100,6 +101,8 @@ class DeviceStore:
             d.slow_kind = L.KVB_SLOW_NONE
         d.offload_tier = L.KVB_TIER_HOST_MAPPED if offload == "host" else L.KVB_TIER_HBM
         d.max_resident = self.max_resident
+        self.capacity = max(n_tokens, capacity or 0)
+        d.capacity_tokens = self.capacity if self.capacity > n_tokens else 0
         h = C.c_void_p()
         L.check(self.lib.kvb_store_create(C.byref(d), C.byref(h)), "kvb_store_create")
         self._keep.clear()
@@ -254,6 +257,38 @@ class DeviceStore:
                                                  _ptr(values), _stream()),
                 "kvb_store_set_residency")
         self.residency = Residency([tuple(o) for o in outliers], res)
+
+    def append(self, keys: torch.Tensor, values: torch.Tensor, left_row: torch.Tensor | None = None):
+        """Decode-time append of one token (kvstore.py:295-305), batch-1
+        stores with ``capacity`` > n: ``keys`` / ``values`` are the full
+        [1, n+1, Hkv, D] device K/V including the new token. The device
+        state becomes what a fresh build over n+1 tokens gives (tail
+        landmark / trailing HIGGS groups, residuals, outliers, local window).
+        SVD stores: ``left_row`` fp16 [Gs, r] is the new token's factor row,
+        or None when the caller re-factors (``import_svd``) afterwards."""
+        want = (1, self.n + 1, self.heads, self.dim)
+        for t, nm in ((keys, "keys"), (values, "values")):
+            if tuple(t.shape) != want or t.dtype != self.dtype or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{nm} must be a contiguous CUDA {self.dtype} tensor {want}")
+        a = L.AppendArgs(self.outlier_tokens, self.local_window)
+        C1 = -(-(self.n + 1) // self.cs)
+        out = np.zeros(max(1, C1), dtype=np.int32)
+        cnt = C.c_int32()
+        if left_row is not None:
+            left_row = left_row.to(torch.float16).contiguous()
+        L.check(self.lib.kvb_store_append(self.h, _ptr(keys), _ptr(values), C.byref(a), _ptr(left_row),
+                                          out.ctypes.data_as(C.c_void_p), C.byref(cnt), _stream()),
+                "kvb_store_append")
+        self.n += 1
+        self.C = C1
+        outl = tuple(int(c) for c in out[: cnt.value])
+        w = min(self.local_window, self.n)
+        parts = [np.arange(c * self.cs, min((c + 1) * self.cs, self.n)) for c in outl]
+        parts.append(np.arange(self.n - w, self.n))
+        self.residency = Residency([outl], [np.unique(np.concatenate(parts)).astype(np.int64)])
+        info = L.StoreInfo()
+        L.check(self.lib.kvb_store_get_info(self.h, C.byref(info)), "kvb_store_get_info")
+        self.info = info
 
     # ----------------------------------------------------------------- import
     def import_dense_landmarks(self, lm: torch.Tensor):
