@@ -471,3 +471,86 @@ class DecodePlan:
                                       _ptr(self.tok), _ptr(self.ntok), _ptr(dst), _ptr(self.lse),
                                       _ptr(self.ws), self.ws.numel(), _stream()), "kvb_decode_step")
         return dst
+
+
+class HeadSplitStore:
+    """Per-KV-head selection: every KV head of every sequence ranks its own
+    chunks and attends to its own top-K (BASELINE north_star kernel (2)).
+
+    kvlab ranks ONE global sum over heads (selection.py:46-52,83-84); the
+    per-head variant's reference semantics are kvlab applied to single-head
+    stores, ``build_store(K[h:h+1])`` + ``select_by_landmarks(store_h,
+    q[h:h+1])`` (SURVEY 8c restatement (4)) -- per-head landmarks, outliers,
+    local window, slow tier and selection. That is exactly a device store
+    whose sequences are the (sequence, head) pairs with one KV head each:
+    the same scan / top-K / gather / attention kernels then run per head,
+    with the G grouped queries of a head scored and attended together.
+
+    Layout: K/V [B*Hkv][n][1][D] (one 256-byte bf16 row per token and head).
+    Queries [B, Hkv, G, D] are a free view of the inner [B*Hkv, 1, G, D]."""
+
+    def __init__(self, *, batch: int, n_tokens: int, kv_heads: int, head_dim: int, chunk_size: int,
+                 dtype=torch.float32, landmark: SchemeDescriptor, residual=None, slow=None,
+                 outlier_tokens: int = 384, local_window: int = 32, offload: str = "hbm"):
+        if slow is not None and slow.kind == SVD and slow.dim not in (0, head_dim):
+            raise ValueError("per-head SVD slow tier factors one head: dim must equal head_dim")
+        self.batch, self.heads = batch, kv_heads
+        self.inner = DeviceStore(batch=batch * kv_heads, n_tokens=n_tokens, kv_heads=1,
+                                 head_dim=head_dim, chunk_size=chunk_size, dtype=dtype,
+                                 landmark=landmark, residual=residual, slow=slow, svd_groups=1,
+                                 outlier_tokens=outlier_tokens, local_window=local_window,
+                                 offload=offload)
+        self.n, self.dim, self.cs, self.C = n_tokens, head_dim, chunk_size, self.inner.C
+
+    def close(self):
+        self.inner.close()
+
+    def _split(self, t: torch.Tensor) -> torch.Tensor:
+        B, n, H, D = t.shape
+        if B != self.batch or H != self.heads:
+            raise ValueError(f"expected [B={self.batch}, n, Hkv={self.heads}, D], got {tuple(t.shape)}")
+        return t.permute(0, 2, 1, 3).reshape(B * H, n, 1, D).contiguous()
+
+    def _q(self, q: torch.Tensor) -> torch.Tensor:
+        if q.dim() != 4 or q.shape[0] != self.batch or q.shape[1] != self.heads:
+            raise ValueError(f"queries must be [B={self.batch}, Hkv={self.heads}, G, D]")
+        return q.contiguous().view(self.batch * self.heads, 1, q.shape[2], q.shape[3])
+
+    def build(self, keys: torch.Tensor, values: torch.Tensor):
+        self.inner.build(self._split(keys), self._split(values))
+        return self
+
+    @property
+    def residency(self):
+        return self.inner.residency
+
+    def n_select(self, sparse_fraction: float) -> int:
+        return self.inner.n_select(sparse_fraction)
+
+    def select(self, q: torch.Tensor, n_select: int, rank_order: bool = True):
+        """Per-head selection: chunk_ids [B, Hkv, K], scores [B, Hkv, C],
+        token_ids [B, Hkv, cap] ascending, n_tokens [B, Hkv]."""
+        cid, sc, tok, ntok = self.inner.select(self._q(q), n_select, rank_order=rank_order)
+        B, H = self.batch, self.heads
+        return (cid.view(B, H, -1), sc.view(B, H, -1), tok.view(B, H, -1), ntok.view(B, H))
+
+    def attend(self, q: torch.Tensor, token_ids: torch.Tensor, n_tokens: torch.Tensor):
+        """out [B, Hkv, G, D]: head h attends to its own token list."""
+        B, H = self.batch, self.heads
+        out, _ = self.inner.attend(self._q(q), token_ids.reshape(B * H, -1).contiguous(),
+                                   n_tokens.reshape(B * H).contiguous())
+        return out.view(B, H, q.shape[2], self.dim)
+
+    def decode_plan(self, G: int, n_select: int):
+        return _HeadSplitPlan(self, self.inner.decode_plan(G, n_select))
+
+
+class _HeadSplitPlan:
+    def __init__(self, store: HeadSplitStore, plan: DecodePlan):
+        self.store, self.plan = store, plan
+
+    def run(self, q: torch.Tensor, out: torch.Tensor | None = None):
+        s = self.store
+        dst = None if out is None else out.view(s.batch * s.heads, 1, q.shape[2], s.dim)
+        r = self.plan.run(s._q(q), dst)
+        return r.view(s.batch, s.heads, q.shape[2], s.dim)
