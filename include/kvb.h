@@ -55,7 +55,11 @@ typedef enum kvb_landmark_kind {
 /* Slow-tier key representation (kvstore.py:142-148). */
 typedef enum kvb_slow_kind {
   KVB_SLOW_NONE = 0, /* exact keys in the offload tier                      */
-  KVB_SLOW_SVD = 1   /* fp16 low-rank factors left[n,r] x right[r, Dg]       */
+  KVB_SLOW_SVD = 1,  /* fp16 low-rank factors left[n,r] x right[r, Dg]       */
+  KVB_SLOW_FP8 = 2,  /* K and V as E4M3 + fp32 scale per (token, head)
+                        (quantization.py:341-371 fp8_e4m3_quantize)          */
+  KVB_SLOW_NVFP4 = 3 /* K and V as E2M1 + E4M3 scale per 16 values
+                        (quantization.py:374-412 nvfp4_quantize)             */
 } kvb_slow_kind;
 
 /* Where the offload tier (V, and K when slow_kind == NONE) lives. */
@@ -153,7 +157,8 @@ kvb_status kvb_choose_outliers(const double* per_chunk_host, int32_t n_chunks,
 kvb_status kvb_store_set_residency(kvb_store* store, const int32_t* resident_host,
                                    const int32_t* counts_host, const void* keys,
                                    const void* values, void* stream);
-/* Offload tier: exact V, and exact K when slow_kind == NONE (device src).   */
+/* Offload tier: exact V, and exact K when slow_kind == NONE (device src);
+ * FP8 / NVFP4 slow tiers encode both K and V on the device.                */
 kvb_status kvb_store_set_offload(kvb_store* store, const void* keys, const void* values,
                                  void* stream);
 /* SVD slow tier (quantization.py:490-513): device fp16 factors

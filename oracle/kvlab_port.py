@@ -242,9 +242,71 @@ def svd16_reconstruct(left16: np.ndarray, right16: np.ndarray) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
+# ---------------------------------------------------------------------------
+# FP8 E4M3 / NVFP4 slow-tier codecs (quantization.py:36-76, 341-412)
+# ---------------------------------------------------------------------------
+
+
+def _e4m3_grid() -> np.ndarray:
+    """quantization.py:38-45: magnitude of linear index i (exponent i // 8,
+    mantissa i % 8, bias 7), i < 127 (no inf / nan)."""
+    i = np.arange(127)
+    e, m = i // 8, i % 8
+    return np.where(e == 0, m * 2.0 ** -9, (1.0 + m / 8.0) * 2.0 ** (e - 7))
+
+
+E4M3 = _e4m3_grid()
+E4M3_MID = (E4M3[:-1] + E4M3[1:]) / 2.0
+E2M1 = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+E2M1_MID = (E2M1[:-1] + E2M1[1:]) / 2.0
+
+
+def grid_round(mags: np.ndarray, mids: np.ndarray, top: int) -> np.ndarray:
+    """quantization.py:55-66: nearest grid index, exact midpoints to the
+    even index (IEEE round-to-nearest-even on these layouts)."""
+    idx = np.minimum(np.searchsorted(mids, mags, side="right"), top)
+    low = np.maximum(idx - 1, 0)
+    tie = (idx > 0) & (mags == mids[low])
+    return np.where(tie & (low % 2 == 0), low, idx)
+
+
+def fp8_roundtrip(x2d: np.ndarray) -> np.ndarray:
+    """fp8_e4m3_quantize + _fp8_dequantize (quantization.py:341-371) with one
+    fp32 scale per row (scale_axis = -1)."""
+    x = f32(x2d)
+    mx = np.abs(x).max(axis=-1, keepdims=True).astype(np.float32)
+    sc = (mx / np.float32(448.0)).astype(np.float32)
+    sc = np.where(mx == 0, np.float32(1.0), sc)
+    y = (x / sc).astype(np.float32)
+    idx = grid_round(np.minimum(np.abs(y).astype(np.float64), 448.0), E4M3_MID, 126)
+    sign = np.where(np.signbit(y), -1.0, 1.0)
+    return ((E4M3[idx] * sign).astype(np.float32) * sc).astype(np.float32)
+
+
+def nvfp4_roundtrip(x2d: np.ndarray) -> np.ndarray:
+    """nvfp4_quantize + _nvfp4_dequantize (quantization.py:374-412): blocks of
+    16 of the flattened tensor, E4M3 block scale nearest to max|x| / 6."""
+    x = f32(x2d)
+    flat = x.ravel().astype(np.float64)
+    pad = (-len(flat)) % 16
+    if pad:
+        flat = np.concatenate([flat, np.zeros(pad)])
+    blocks = flat.reshape(-1, 16)
+    mx = np.abs(blocks).max(axis=1)
+    qs = E4M3[grid_round(np.minimum(mx / 6.0, 448.0), E4M3_MID, 126)]
+    qs = np.where(qs == 0.0, E4M3[1], qs)
+    qs = np.where(mx == 0.0, 1.0, qs)
+    y = (blocks.astype(np.float32) / qs[:, None].astype(np.float32)).astype(np.float32)
+    idx = grid_round(np.minimum(np.abs(y).astype(np.float64), 6.0), E2M1_MID, 7)
+    sign = np.where(np.signbit(y), -1.0, 1.0)
+    vals = (E2M1[idx] * sign).astype(np.float32)
+    out = (vals * qs[:, None].astype(np.float32)).astype(np.float32).ravel()
+    return out[: x.size].reshape(x.shape)
+
+
 @dataclass(frozen=True)
 class Scheme:
-    kind: str            # "none" | "higgs" | "svd"
+    kind: str            # "none" | "higgs" | "svd" | "fp8_e4m3" | "nvfp4"
     d: int = 0
     n: int = 0
     group: int = 0
@@ -263,6 +325,14 @@ class Scheme:
     def svd(rank: int):
         return Scheme("svd", rank=rank)
 
+    @staticmethod
+    def fp8():
+        return Scheme("fp8_e4m3")
+
+    @staticmethod
+    def nvfp4():
+        return Scheme("nvfp4")
+
 
 def lossy_roundtrip(x2d: np.ndarray, s: Scheme):
     """quantize+dequantize of one [rows, D] tensor (quantization.py:516-553).
@@ -275,6 +345,10 @@ def lossy_roundtrip(x2d: np.ndarray, s: Scheme):
     if s.kind == "svd":
         l16, r16 = svd16(x2d, s.rank)
         return svd16_reconstruct(l16, r16), (l16, r16)
+    if s.kind == "fp8_e4m3":
+        return fp8_roundtrip(x2d), None
+    if s.kind == "nvfp4":
+        return nvfp4_roundtrip(x2d), None
     raise ValueError(f"scheme {s.kind!r} is outside the decode hot path")
 
 
@@ -450,9 +524,12 @@ def build(keys, values, cs: int, landmark: Scheme, residual: Scheme | None = Non
             facs.append(st)
         slow_k = np.stack(sk)
         codec["slow"] = ("per_head", facs) if slow.kind == "svd" else None
-        # values stay exact under SVD (kvstore.py:142-144); only "none" and
-        # "svd" slow tiers are on the decode hot path
-        slow_v = v.copy()
+        # values stay exact under SVD, otherwise they take the slow-tier
+        # scheme too (kvstore.py:142-148)
+        if slow.kind in ("fp8_e4m3", "nvfp4"):
+            slow_v = np.stack([lossy_roundtrip(v[i], slow)[0] for i in range(h)])
+        else:
+            slow_v = v.copy()
     outl = outlier_chunks(k, lm_dq, cs, budget.outlier_tokens)
     return PortStore(keys=k, values=v, cs=cs, budget=budget, lm_dq=lm_dq, res_dq=res_dq,
                      slow_k=slow_k, slow_v=slow_v, outliers=outl, codec=codec)

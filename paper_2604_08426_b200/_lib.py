@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(_PKG, "libkvb.so")
 KVB_OK, KVB_EINVAL, KVB_ECUDA, KVB_ENOMEM, KVB_ENCCL, KVB_EUNSUPPORTED = range(6)
 KVB_F32, KVB_BF16 = 0, 1
 KVB_LM_DENSE, KVB_LM_HIGGS = 0, 1
-KVB_SLOW_NONE, KVB_SLOW_SVD = 0, 1
+KVB_SLOW_NONE, KVB_SLOW_SVD, KVB_SLOW_FP8, KVB_SLOW_NVFP4 = 0, 1, 2, 3
 KVB_TIER_HBM, KVB_TIER_HOST_MAPPED = 0, 1
 KVB_AGG_SUM, KVB_AGG_MAX = 0, 1
 

@@ -225,12 +225,10 @@ void free_store(kvb_store* s) {
   cudaFree(s->svd_left);
   cudaFree(s->svd_right);
   cudaFree(s->svd_rightT);
-  if (s->off_host) {
-    cudaFreeHost(s->off_k);
-    cudaFreeHost(s->off_v);
-  } else {
-    cudaFree(s->off_k);
-    cudaFree(s->off_v);
+  for (void* p : {s->off_k, s->off_v, s->off_ks, s->off_vs}) {
+    if (!p) continue;
+    if (s->off_host) cudaFreeHost(p);
+    else cudaFree(p);
   }
   delete s;
 }
@@ -345,8 +343,10 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
     if (d.svd_rank < 1) KVB_FAIL(KVB_EINVAL, "svd rank must be >= 1");
     if (d.svd_groups < 1 || d.kv_heads % d.svd_groups)
       KVB_FAIL(KVB_EINVAL, "svd_groups must divide kv_heads");
+  } else if (d.slow_kind == KVB_SLOW_FP8 || d.slow_kind == KVB_SLOW_NVFP4) {
+    if (d.head_dim % 16) KVB_FAIL(KVB_EUNSUPPORTED, "quantized slow tiers need head_dim % 16 == 0");
   } else if (d.slow_kind != KVB_SLOW_NONE) {
-    KVB_FAIL(KVB_EUNSUPPORTED, "slow tier must be none or svd");
+    KVB_FAIL(KVB_EINVAL, "unknown slow tier");
   }
   if ((int64_t)d.n_tokens > (1ll << 26) || (int64_t)d.capacity_tokens > (1ll << 26))
     KVB_FAIL(KVB_EUNSUPPORTED, "n_tokens too large");
@@ -397,28 +397,30 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   cudaMemset(s->res_count, 0, B * sizeof(int32_t));
   cudaMemset(s->res_bitmap, 0, B * Wcap * sizeof(uint32_t));
   cudaMemset(s->res_prefix, 0, B * Wcap * sizeof(int32_t));
-  const size_t off_bytes = B * n * E * s->esz;
-  const bool need_k = d.slow_kind == KVB_SLOW_NONE;
-  if (d.offload_tier == KVB_TIER_HOST_MAPPED) {
-    s->off_host = true;
-    cudaError_t e = cudaHostAlloc(&s->off_v, off_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e != cudaSuccess) return bail(cuda_status(e, "pinned V"));
-    cudaHostGetDevicePointer(&s->off_v_dev, s->off_v, 0);
-    if (need_k) {
-      e = cudaHostAlloc(&s->off_k, off_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
-      if (e != cudaSuccess) return bail(cuda_status(e, "pinned K"));
-      cudaHostGetDevicePointer(&s->off_k_dev, s->off_k, 0);
-    }
-  } else if (d.offload_tier == KVB_TIER_HBM) {
-    if ((st = dalloc((char**)&s->off_v, off_bytes, "offload V")) != KVB_OK) return bail(st);
-    s->off_v_dev = s->off_v;
-    if (need_k) {
-      if ((st = dalloc((char**)&s->off_k, off_bytes, "offload K")) != KVB_OK) return bail(st);
-      s->off_k_dev = s->off_k;
-    }
-  } else {
+  // offload tier: exact rows, or FP8 / NVFP4 codes + scales (K and V)
+  const int qk = slow_qkind(s);
+  const size_t off_bytes = qk == 1 ? B * n * E : qk == 2 ? B * n * E / 2 : B * n * E * s->esz;
+  const size_t sc_bytes = qk == 1 ? B * n * d.kv_heads * sizeof(float) : qk == 2 ? B * n * E / 16 : 0;
+  const bool need_k = d.slow_kind != KVB_SLOW_SVD;
+  if (d.offload_tier != KVB_TIER_HOST_MAPPED && d.offload_tier != KVB_TIER_HBM)
     return bail((set_error("unknown offload tier"), KVB_EINVAL));
-  }
+  s->off_host = d.offload_tier == KVB_TIER_HOST_MAPPED;
+  auto tier_alloc = [&](void** p, void** pdev, size_t bytes, const char* what) -> kvb_status {
+    if (!bytes) return KVB_OK;
+    if (s->off_host) {
+      cudaError_t e = cudaHostAlloc(p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_status(e, what);
+      cudaHostGetDevicePointer(pdev, *p, 0);
+      return KVB_OK;
+    }
+    kvb_status r = dalloc((char**)p, bytes, what);
+    *pdev = *p;
+    return r;
+  };
+  if ((st = tier_alloc(&s->off_v, &s->off_v_dev, off_bytes, "offload V")) != KVB_OK) return bail(st);
+  if (need_k && (st = tier_alloc(&s->off_k, &s->off_k_dev, off_bytes, "offload K")) != KVB_OK) return bail(st);
+  if ((st = tier_alloc(&s->off_vs, &s->off_vs_dev, sc_bytes, "offload V scales")) != KVB_OK) return bail(st);
+  if ((st = tier_alloc(&s->off_ks, &s->off_ks_dev, sc_bytes, "offload K scales")) != KVB_OK) return bail(st);
   if (d.slow_kind == KVB_SLOW_SVD) {
     const size_t r = d.svd_rank, g = d.svd_groups, Dg = E / g;
     if ((st = dalloc(&s->svd_left, B * n * g * r, "svd left")) != KVB_OK) return bail(st);
@@ -448,7 +450,9 @@ kvb_status kvb_store_get_info(const kvb_store* s, kvb_store_info* info) {
   if (s->svd_left)
     fast += (int64_t)B * (n * s->d.svd_groups * s->d.svd_rank + (size_t)s->d.svd_rank * E) * 2;
   info->bytes_fast_tier = fast;
-  info->bytes_offload_tier = (int64_t)B * n * E * s->esz * (s->off_k ? 2 : 1);
+  const int qk = slow_qkind(s);
+  const int64_t row = qk == 1 ? E + 4 * s->d.kv_heads : qk == 2 ? E / 2 + E / 16 : E * s->esz;
+  info->bytes_offload_tier = (int64_t)B * n * row * (s->off_k ? 2 : 1);
   return KVB_OK;
 }
 
@@ -570,6 +574,12 @@ kvb_status kvb_store_set_offload(kvb_store* s, const void* keys, const void* val
   if (!s || !values) KVB_FAIL(KVB_EINVAL, "null argument");
   const size_t bytes = (size_t)s->d.batch * s->d.n_tokens * s->E * s->esz;
   cudaStream_t st = as_stream(stream);
+  if (slow_qkind(s)) {  // quantization.py:341-412, encoded on the device
+    if (!keys) KVB_FAIL(KVB_EINVAL, "quantized slow tier needs keys");
+    KVB_CUDA(launch_quantize_tier(s, keys, true, st), "slow-tier K encode");
+    KVB_CUDA(launch_quantize_tier(s, values, false, st), "slow-tier V encode");
+    return KVB_OK;
+  }
   KVB_CUDA(cudaMemcpyAsync(s->off_v_dev, values, bytes, cudaMemcpyDefault, st), "offload V");
   if (s->off_k) {
     if (!keys) KVB_FAIL(KVB_EINVAL, "slow tier 'none' needs keys");
@@ -602,9 +612,14 @@ kvb_status kvb_store_append(kvb_store* s, const void* keys, const void* values,
   // offload tier row (and the SVD factor row when given)
   const char* kb = static_cast<const char*>(keys);
   const char* vb = static_cast<const char*>(values);
-  KVB_CUDA(cudaMemcpyAsync(static_cast<char*>(s->off_v_dev) + (size_t)n0 * E * esz,
-                           vb + (size_t)n0 * E * esz, E * esz, cudaMemcpyDefault, st), "append V row");
-  if (s->off_k)
+  if (slow_qkind(s)) {
+    KVB_CUDA(launch_quantize_tier(s, keys, true, st, n0), "append K encode");
+    KVB_CUDA(launch_quantize_tier(s, values, false, st, n0), "append V encode");
+  } else {
+    KVB_CUDA(cudaMemcpyAsync(static_cast<char*>(s->off_v_dev) + (size_t)n0 * E * esz,
+                             vb + (size_t)n0 * E * esz, E * esz, cudaMemcpyDefault, st), "append V row");
+  }
+  if (s->off_k && !slow_qkind(s))
     KVB_CUDA(cudaMemcpyAsync(static_cast<char*>(s->off_k_dev) + (size_t)n0 * E * esz,
                              kb + (size_t)n0 * E * esz, E * esz, cudaMemcpyDefault, st), "append K row");
   if (s->svd_left && left16_row) {

@@ -59,6 +59,14 @@ struct AttParams {
   int* counters;         // [B] split tickets (zeroed per call)
   float* out;            // [B][H][G][D]
   float* lse;            // [B][H][G] (may be null)
+  // quantized slow tier (kvb_tier.cu): codes + scales of K and V, decoded
+  // into fp32 shared-memory rows; residents are kv-dtype rows (res_bf16)
+  int slow_q;
+  const uint8_t* qk;
+  const uint8_t* qv;
+  const void* qks;
+  const void* qvs;
+  int res_bf16;
   // shared-memory geometry (bytes)
   int krow, kpad_head, lrow, vrow;
   int off_qt, off_lg, off_alpha, off_tok, off_buf, buf_bytes, boff_l, boff_v;
@@ -223,6 +231,41 @@ __device__ __forceinline__ void stage_rows(const AttParams& p, int b, const int*
   }
 }
 
+// Quantized slow tier: warp per token, lanes over the row's E values; decoded
+// (or widened resident) values are stored as fp32 rows in the layout the
+// fp32 kernel reads (head-padded K rows, V rows). Synchronous: these tiers are
+// about fidelity and host-link bytes, not the HBM hot path.
+__device__ void stage_rows_q(const AttParams& p, int b, const int* tok_s, const int* slot_s, int i0,
+                             int ns, unsigned char* buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int H = p.H, D = p.D, E = H * D;
+  for (int j = warp; j < ns; j += nwarp) {
+    const int slot = slot_s[i0 + j];
+    const size_t tr = (size_t)b * p.n + tok_s[i0 + j];
+    unsigned char* krow = buf + (size_t)j * p.krow;
+    float* vrow = reinterpret_cast<float*>(buf + p.boff_v + (size_t)j * p.vrow);
+    const size_t rb = ((size_t)b * p.Rcap + (slot < 0 ? 0 : slot)) * E;
+    for (int e = lane; e < E; e += 32) {
+      float kv, vv;
+      if (slot >= 0) {
+        if (p.res_bf16) {
+          kv = __bfloat162float(static_cast<const __nv_bfloat16*>(p.res_k)[rb + e]);
+          vv = __bfloat162float(static_cast<const __nv_bfloat16*>(p.res_v)[rb + e]);
+        } else {
+          kv = static_cast<const float*>(p.res_k)[rb + e];
+          vv = static_cast<const float*>(p.res_v)[rb + e];
+        }
+      } else {
+        kv = qdecode(p.slow_q, p.qk, p.qks, tr, e, E, H, D);
+        vv = qdecode(p.slow_q, p.qv, p.qvs, tr, e, E, H, D);
+      }
+      const int h = e / D;
+      reinterpret_cast<float*>(krow + (size_t)h * p.kpad_head)[e - h * D] = kv;
+      vrow[e] = vv;
+    }
+  }
+}
+
 template <typename T, int TT>
 __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -265,7 +308,10 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
   __syncthreads();
 
   const int nsub = (cnt + TT - 1) / TT;
-  if (nsub > 0) stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
+  if (nsub > 0) {
+    if (p.slow_q) stage_rows_q(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
+    else stage_rows<T>(p, b, tok_s, slot_s, 0, min(TT, cnt), bufs);
+  }
   cp_commit();
 
   // SVD logits on tensor cores: warps 0..3 own n-tile (8 hg) w. A = the
@@ -329,8 +375,12 @@ __global__ void __launch_bounds__(kAttThreads, 1) k5_attend(AttParams p) {
     const int ns = min(TT, cnt - i0);
     unsigned char* buf = bufs + (size_t)(st & 1) * p.buf_bytes;
     if (st + 1 < nsub) {
-      stage_rows<T>(p, b, tok_s, slot_s, i0 + TT, min(TT, cnt - i0 - TT),
-                    bufs + (size_t)((st + 1) & 1) * p.buf_bytes);
+      if (p.slow_q)
+        stage_rows_q(p, b, tok_s, slot_s, i0 + TT, min(TT, cnt - i0 - TT),
+                     bufs + (size_t)((st + 1) & 1) * p.buf_bytes);
+      else
+        stage_rows<T>(p, b, tok_s, slot_s, i0 + TT, min(TT, cnt - i0 - TT),
+                      bufs + (size_t)((st + 1) & 1) * p.buf_bytes);
       cp_commit();
       cp_wait<1>();
     } else {
@@ -671,7 +721,7 @@ AttGeom attend_geometry(const kvb_store* s, int G, int cap) {
   AttGeom a{};
   AttParams& p = a.p;
   const int H = s->d.kv_heads, D = s->d.head_dim, E = H * D;
-  const int esz = (int)s->esz;
+  const int esz = slow_qkind(s) ? 4 : (int)s->esz;  // quantized tiers run the fp32 kernel
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
   const int HG = H * G;
@@ -837,8 +887,14 @@ cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaSt
   p.counters = w.counters;
   p.out = a.out;
   p.lse = a.lse;
+  p.slow_q = slow_qkind(s);
+  p.qk = static_cast<const uint8_t*>(s->off_k_dev);
+  p.qv = static_cast<const uint8_t*>(s->off_v_dev);
+  p.qks = s->off_ks_dev;
+  p.qvs = s->off_vs_dev;
+  p.res_bf16 = s->d.kv_dtype == KVB_BF16 ? 1 : 0;
   count_launch(1);
-  if (s->d.kv_dtype == KVB_BF16) {
+  if (s->d.kv_dtype == KVB_BF16 && !p.slow_q) {
     ensure_smem((const void*)k5_attend<__nv_bfloat16, 16>, geo.smem);
     k5_attend<__nv_bfloat16, 16><<<dim3(w.splits, B), kAttThreads, geo.smem, st>>>(p);
   } else {

@@ -924,6 +924,7 @@ BulkGeom bulk_geometry(const kvb_store* s, int positions_cap, int K = 0) {
 }  // namespace
 
 bool attend_bulk_supported(const kvb_store* s, int G, int positions_cap, int K) {
+  if (slow_qkind(s)) return false;  // FP8 / NVFP4 tiers: the token kernel decodes them
   if (s->d.kv_dtype != KVB_BF16 || s->d.head_dim != kBD || s->d.kv_heads > 8 || G > 8 || G < 1)
     return false;
   // host-mapped offload tier: cp.async.bulk reads the pinned, device-mapped

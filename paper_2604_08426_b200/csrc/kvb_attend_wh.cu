@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(128) k5_merge_splits(const float* __restrict__
 }  // namespace
 
 bool attend_wh_supported(const kvb_store* s, int G) {
-  return s->d.kv_dtype == KVB_BF16 && s->d.head_dim == kWhD && s->d.kv_heads <= kWhWarps &&
+  return !slow_qkind(s) && s->d.kv_dtype == KVB_BF16 && s->d.head_dim == kWhD && s->d.kv_heads <= kWhWarps &&
          G <= 8 && (s->d.slow_kind != KVB_SLOW_SVD ||
                     (s->d.svd_rank % 8 == 0 && s->d.svd_rank <= 16 * kWhMaxKsSvd));
 }

@@ -37,6 +37,32 @@ template <> struct Vec<__nv_bfloat16> {
   }
 };
 
+// ---- quantized slow tiers (quantization.py:36-49) ------------------------------
+// E4M3 magnitude of linear index i (exponent i / 8, mantissa i % 8, bias 7).
+__host__ __device__ __forceinline__ double e4m3_value(int i) {
+  const int e = i >> 3, m = i & 7;
+  return e == 0 ? m * 0.001953125 /* 2^-9 */ : (1.0 + m / 8.0) * ldexp(1.0, e - 7);
+}
+__device__ __forceinline__ float e4m3_f32(int i) { return (float)e4m3_value(i); }
+__device__ __forceinline__ float e2m1_f32(int i) {
+  const float t[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+  return t[i];
+}
+// Decoded element e (of E = H*D) of token row `tr` of a quantized tier:
+// kind 1 = FP8 (fp32 scale per (token, head)), 2 = NVFP4 (E4M3 byte per 16).
+__device__ __forceinline__ float qdecode(int kind, const uint8_t* codes, const void* scales,
+                                         size_t tr, int e, int E, int H, int D) {
+  if (kind == 1) {
+    const uint8_t c = codes[tr * E + e];
+    const float v = (c & 0x80) ? -e4m3_f32(c & 0x7f) : e4m3_f32(c & 0x7f);
+    return v * static_cast<const float*>(scales)[tr * H + e / D];
+  }
+  const uint8_t b = codes[tr * (E / 2) + e / 2];
+  const int c = (e & 1) ? (b >> 4) : (b & 15);
+  const float v = (c & 8) ? -e2m1_f32(c & 7) : e2m1_f32(c & 7);
+  return v * e4m3_f32(static_cast<const uint8_t*>(scales)[tr * (E / 16) + e / 16]);
+}
+
 // Streaming 16-byte load that does not allocate in L1 (landmark scan).
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 r;

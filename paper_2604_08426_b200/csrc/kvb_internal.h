@@ -56,6 +56,12 @@ struct kvb_store {
   void* off_v = nullptr;         // [B][n][E]
   void* off_k_dev = nullptr;     // device alias when host-mapped
   void* off_v_dev = nullptr;
+  // quantized slow tiers (FP8 / NVFP4): off_k/off_v hold the codes, these the
+  // scales (fp32 [B][n][Hkv] for FP8, E4M3 bytes [B][n][E/16] for NVFP4)
+  void* off_ks = nullptr;
+  void* off_vs = nullptr;
+  void* off_ks_dev = nullptr;
+  void* off_vs_dev = nullptr;
   bool off_host = false;
   // side stream + events for the fork/join of decode-step work (prep || scan)
   cudaStream_t side = nullptr;
@@ -63,6 +69,11 @@ struct kvb_store {
 };
 
 namespace kvb {
+
+// 0: slow tier none / svd; 1: FP8 E4M3; 2: NVFP4 (kvb_tier.cu)
+inline int slow_qkind(const kvb_store* s) {
+  return s->d.slow_kind == KVB_SLOW_FP8 ? 1 : s->d.slow_kind == KVB_SLOW_NVFP4 ? 2 : 0;
+}
 
 void set_error(const std::string& msg);
 kvb_status cuda_status(cudaError_t e, const char* what);
@@ -135,6 +146,10 @@ cudaError_t launch_union_sorted(const kvb_store* s, const int32_t* chunk_ids, in
 // while its predecessor drains; it must griddepcontrol.wait before reading
 // the predecessor's output.
 bool pdl_enabled();
+// Encode K (keys = true) or V of the whole store into its FP8 / NVFP4 tier.
+// t0 > 0 (batch-1 append): only tokens [t0, n).
+cudaError_t launch_quantize_tier(const kvb_store* s, const void* src, bool keys, cudaStream_t st,
+                                 int t0 = 0);
 // Slow-tier (resident_exact: tiered) K/V rows of a token list -> float32 (kvb_tier.cu).
 cudaError_t launch_gather_kv(const kvb_store* s, int b, const int32_t* tok, int n,
                              int resident_exact, float* k_out, float* v_out, cudaStream_t st);

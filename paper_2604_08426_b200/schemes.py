@@ -3,9 +3,9 @@
 Mirrors the reference's scheme vocabulary (quantization.py:81-169, 556-623)
 so kvlab configuration strings (``higgs2``, ``higgs:d=2,n=256,group=1024,
 seed=0``, ``svd:rank=160,dim=1024``) select the same codecs here. The
-decode path consumes only ``none`` / ``higgs`` landmarks and residuals and
-``none`` / ``svd`` slow tiers; FP8/NVFP4 parse but are rejected by the store
-(outside this hot path).
+decode path consumes ``none`` / ``higgs`` landmarks and residuals and
+``none`` / ``svd`` / ``fp8_e4m3`` / ``nvfp4`` slow tiers (the FP8 / NVFP4
+tiers encode K and V in the offload tier, quantization.py:341-412).
 
 The HIGGS codebook is a constant table (k-means over seeded Gaussian samples,
 quantization.py:207-266). It is computed once on the host with the same

@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .schemes import HIGGS, NONE, SVD, SchemeDescriptor, hadamard_signs, higgs_codebook
+from .schemes import (FP8_E4M3, HIGGS, NONE, NVFP4, SVD, SchemeDescriptor, hadamard_signs,
+                      higgs_codebook)
 
 
 def _ptr(t) -> C.c_void_p:
@@ -70,7 +71,7 @@ class DeviceStore:
             raise NotImplementedError(f"landmark scheme {landmark.kind!r} is outside the decode path")
         if residual is not None and residual.kind != HIGGS:
             raise NotImplementedError("residuals must be HIGGS-coded on the decode path")
-        if slow.kind not in (NONE, SVD):
+        if slow.kind not in (NONE, SVD, FP8_E4M3, NVFP4):
             raise NotImplementedError(f"slow tier {slow.kind!r} is outside the decode path")
         self.batch, self.n, self.heads, self.dim = batch, n_tokens, kv_heads, head_dim
         self.cs = chunk_size
@@ -97,8 +98,9 @@ class DeviceStore:
             d.slow_kind = L.KVB_SLOW_SVD
             d.svd_rank = slow.rank
             d.svd_groups = self.svd_groups
-        else:
-            d.slow_kind = L.KVB_SLOW_NONE
+        else:  # none / FP8 E4M3 / NVFP4 (quantization.py:341-412): K and V in the offload tier
+            d.slow_kind = {NONE: L.KVB_SLOW_NONE, FP8_E4M3: L.KVB_SLOW_FP8,
+                           NVFP4: L.KVB_SLOW_NVFP4}[slow.kind]
         d.offload_tier = L.KVB_TIER_HOST_MAPPED if offload == "host" else L.KVB_TIER_HBM
         d.max_resident = self.max_resident
         self.capacity = max(n_tokens, capacity or 0)

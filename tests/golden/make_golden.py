@@ -277,6 +277,40 @@ def tier_io_case():
     save("tier_io", **arr)
 
 
+def lowbit_case():
+    """FP8 E4M3 / NVFP4 slow tiers (quantization.py:341-412): codec round
+    trips on edge-case rows (zeros, ties, huge and subnormal magnitudes) and a
+    store whose slow tier is each of them (gather_kv + selection + attention)."""
+    attention, kvstore, numerics, quantization, selection, workload = _kvlab()
+    arr = {}
+    x = rand((24, 64), 50)
+    x[0] = 0.0                                   # all-zero row / blocks
+    x[1, :16] = 0.0
+    x[2] *= 1e-30                                # subnormal E4M3 block scales
+    x[3] *= 1e6
+    x[4, :8] = np.float32(448.0) * np.arange(8, dtype=np.float32) / 7
+    x[5] = np.round(x[5] * 4) / 4               # many exact grid midpoints
+    x[6, 3] = -0.0
+    arr["x"] = x
+    for name, fn in (("fp8", quantization.scheme_fp8()), ("nvfp4", quantization.scheme_nvfp4())):
+        arr[f"{name}_dq"] = quantization.dequantize(quantization.quantize(x, fn))
+    k = rand((2, 203, 32), 51, 0.5)
+    v = rand((2, 203, 32), 52, 0.5)
+    q = rand((2, 2, 32), 53)
+    arr["keys"], arr["values"], arr["queries"] = k, v, q
+    toks = np.arange(0, 203, 3, dtype=np.int64)
+    arr["tokens"] = toks
+    b = kvstore.BudgetConfig(0.1, 24, 8)
+    for name, fn in (("fp8", quantization.scheme_fp8()), ("nvfp4", quantization.scheme_nvfp4())):
+        st = kvstore.build_store(k, v, 8, quantization.scheme_none(), budget=b, slow_tier_scheme=fn)
+        gk, gv = st.gather_kv(toks)
+        arr[f"{name}_gather_k"], arr[f"{name}_gather_v"] = gk, gv
+        sel = selection.select_by_landmarks(st, q, b)
+        arr[f"{name}_token_ids"] = sel.token_ids.astype(np.int64)
+        arr[f"{name}_sparse_out"] = attention.sparse_attention(q, st, sel).output
+    save("lowbit", **arr)
+
+
 def harness_case():
     """kvlab's own harness.run_grid_point (harness.py:96-135) rows on small
     planted-needle workloads: the numbers the patched shim must reproduce."""
@@ -343,6 +377,7 @@ def main():
     needle_case()
     tier_io_case()
     harness_case()
+    lowbit_case()
 
 
 if __name__ == "__main__":

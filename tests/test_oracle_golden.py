@@ -167,3 +167,21 @@ def test_errors_match_reference_conditions():
     with pytest.raises(ValueError):
         P.Budget(0.0, 0, 0)
     assert math.isclose(P.n_select(st, 0.5), 1)
+
+
+def test_lowbit_slow_tiers():
+    """FP8 E4M3 / NVFP4 restatement (quantization.py:341-412) == kvlab: codec
+    round trips on edge-case rows and whole stores (gather, selection,
+    attention) bit for bit."""
+    z = golden("lowbit")
+    assert np.array_equal(P.fp8_roundtrip(z["x"]), z["fp8_dq"])
+    assert np.array_equal(P.nvfp4_roundtrip(z["x"]), z["nvfp4_dq"])
+    b = P.Budget(0.1, 24, 8)
+    for name, sch in (("fp8", P.Scheme.fp8()), ("nvfp4", P.Scheme.nvfp4())):
+        st = P.build(z["keys"], z["values"], 8, P.Scheme.none(), budget=b, slow=sch)
+        gk, gv = st.gather(z["tokens"])
+        assert np.array_equal(gk, z[f"{name}_gather_k"]) and np.array_equal(gv, z[f"{name}_gather_v"])
+        sel = P.select_by_landmarks(st, z["queries"], b)
+        assert np.array_equal(sel.token_ids, z[f"{name}_token_ids"])
+        o, _, _ = P.sparse_attention(z["queries"], st, sel.token_ids)
+        np.testing.assert_allclose(o, z[f"{name}_sparse_out"], rtol=0, atol=1e-6)
