@@ -7,7 +7,9 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libkvb.so")
+# KVB_LIB_TAG selects an experiment build libkvb_<tag>.so (build.py, same tag)
+_TAG = os.environ.get("KVB_LIB_TAG", "")
+LIB_PATH = os.path.join(_PKG, f"libkvb_{_TAG}.so" if _TAG else "libkvb.so")
 
 KVB_OK, KVB_EINVAL, KVB_ECUDA, KVB_ENOMEM, KVB_ENCCL, KVB_EUNSUPPORTED = range(6)
 KVB_F32, KVB_BF16 = 0, 1

@@ -17,8 +17,13 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libkvb.so")
+# Experiment builds (A/B runs in one GPU session): KVB_LIB_TAG=<tag> with
+# KVB_DEFS="-DNAME=VALUE ..." writes libkvb_<tag>.so from _build_<tag>/; the
+# product library is the untagged libkvb.so.
+TAG = os.environ.get("KVB_LIB_TAG", "")
+DEFS = os.environ.get("KVB_DEFS", "").split() if TAG else []
+OBJ = os.path.join(PKG, f"_build_{TAG}" if TAG else "_build")
+LIB = os.path.join(PKG, f"libkvb_{TAG}.so" if TAG else "libkvb.so")
 SOURCES = ["kvb_api.cu", "kvb_score.cu", "kvb_select.cu", "kvb_attend.cu", "kvb_build.cu",
            "kvb_higgs_tc.cu", "kvb_attend_wh.cu", "kvb_attend_bulk.cu", "kvb_recon.cu", "kvb_tier.cu"]
 HEADERS = ["kvb_common.cuh", "kvb_internal.h", "kvb_fuse.cuh"]
@@ -68,7 +73,7 @@ def _compile(src: str, force: bool) -> tuple[str, str, str]:
     source must not be reused)."""
     s = os.path.join(CSRC, src)
     o = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+    cmd = [_nvcc(), *ARCH, *FLAGS, *DEFS, "-c", s, "-o", o]
     digest = _digest([s, *_deps()], " ".join(cmd[1:]))
     if not force and _fresh(o, digest):
         return o, "", digest

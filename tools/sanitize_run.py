@@ -1,7 +1,8 @@
 """Small-shape driver of every decode-path kernel family, for
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
-usage: compute-sanitizer --tool racecheck python tools/sanitize_run.py
+usage: compute-sanitizer --tool racecheck python tools/sanitize_run.py [N]
+(N = context length, default 4096; racecheck runs use a shorter one)
 
 Runs, on tiny stores (n = 4096, batch 2): the C2-style decode step
 (k5_prep + k1_dense_sum + k5_attend_bulk with the prologue top-K +
@@ -25,7 +26,7 @@ from paper_2604_08426_b200.store import DeviceStore  # noqa: E402
 def main():
     torch.cuda.set_device(0)
     g = torch.Generator(device="cuda").manual_seed(0)
-    B, n, H, G, D = 2, 4096, 8, 4, 128
+    B, n, H, G, D = 2, int(sys.argv[1]) if len(sys.argv) > 1 else 4096, 8, 4, 128
     k = torch.randn((B, n, H, D), generator=g, device="cuda").bfloat16()
     v = torch.randn((B, n, H, D), generator=g, device="cuda").bfloat16()
     q = torch.randn((B, H, G, D), generator=g, device="cuda")
@@ -34,7 +35,7 @@ def main():
                      landmark=S.scheme_none(), slow=S.scheme_svd(160, H * D), svd_groups=1,
                      outlier_tokens=64, local_window=32)
     st.build(k, v)
-    K = st.n_select(256 / n)
+    K = st.n_select(min(256, n // 16) / n)
     for kp in (0, 2):
         plan = st.decode_plan(G, K, k_path=kp)
         plan.run(q)
@@ -46,7 +47,7 @@ def main():
     st = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=1, dtype=torch.bfloat16,
                      landmark=S.scheme_higgs(2), outlier_tokens=0, local_window=32)
     st.build(k, v)
-    plan = st.decode_plan(G, st.n_select(256 / n))
+    plan = st.decode_plan(G, st.n_select(min(256, n // 16) / n))
     plan.run(q)
     st.close()
     # Appendix E: 4-bit @ 8 landmarks + 1-bit residuals, both stages
@@ -55,7 +56,7 @@ def main():
                      local_window=32)
     st.build(k, v)
     for exact in (True, False):
-        st.select_residual(q, 256, 4, exact=exact)
+        st.select_residual(q, min(256, n // 16), 4, exact=exact)
     st.close()
     # FP8 slow tier (token kernel decode path)
     st = DeviceStore(batch=B, n_tokens=n, kv_heads=H, head_dim=D, chunk_size=8, dtype=torch.bfloat16,
