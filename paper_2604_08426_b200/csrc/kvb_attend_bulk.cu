@@ -319,6 +319,10 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
                             : make_float2(0.f, 0.f);
       }
   }
+  // prologue top-K: the selected-chunk bitmap and its per-word prefix counts
+  // (rank of a chunk among the selected ones in O(1)); null otherwise
+  const uint32_t* sel_bm = nullptr;
+  int32_t* wpre = nullptr;
   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
     // top-K from the scan's scores + histogram into a bitmap in the (not yet
     // used) ring, then ascending ids: each thread owns a run of words, one scan
@@ -332,8 +336,12 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     // stage the sequence's scores in the ring's tail by bulk copies (overlaps
     // the threshold search) when they fit beside >= 4096 candidate slots
     const size_t sbytes = (size_t)p.C * 4;
+#ifdef KVB_NO_STAGE
+    const bool staged = false;
+#else
     const bool staged = (sbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(scs) & 15) == 0) &&
                         used + sbytes + 4096 * 8 <= ring_bytes;
+#endif
     __shared__ __align__(8) uint64_t stage_bar;
     float* stage = staged ? reinterpret_cast<float*>(pro + ring_bytes - sbytes) : nullptr;
     if (staged && tid == 0) {
@@ -348,10 +356,10 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     const int cap = (int)((ring_bytes - used - (staged ? sbytes : 0)) / 8);
     select_topk_shared(scs, p.C,
                        p.sel_hist + (size_t)b * kFuseHistBins,
-                       p.Kb, wb, sk, reinterpret_cast<int32_t*>(sk + cap), cap, red,
+                       p.Kb, wb, reinterpret_cast<uint64_t*>(sk), cap, red,
                        p.trace ? p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8
                                : nullptr,
-                       stage, staged ? &stage_bar : nullptr, 0);
+                       stage, staged ? &stage_bar : nullptr);
     if (staged && tid == 0)  // all threads waited on it inside (and synced after)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(saddr(&stage_bar)) : "memory");
     const int per = (p.Wc + nthr - 1) / nthr;
@@ -360,6 +368,13 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     for (int w = w0; w < w1; ++w) cnt += __popc(wb[w]);
     int tot;
     int pos = block_excl_scan(cnt, red, &tot);
+    // wpre[w]: selected chunks below word w (the candidate list is dead now)
+    wpre = reinterpret_cast<int32_t*>(sk);
+    for (int w = w0, q = pos; w < w1; ++w) {
+      wpre[w] = q;
+      q += __popc(wb[w]);
+    }
+    sel_bm = wb;
     for (int w = w0; w < w1; ++w) {
       uint32_t bits = wb[w];
       while (bits) {
@@ -386,8 +401,12 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       int f = 0;
       if (i < nres) {
         const int c = ur[i] / p.cs;
-        const int lb = lower_bound_i(uc, p.Kb, c);
-        f = (lb < p.Kb && uc[lb] == c) ? 1 : 0;
+        if (sel_bm) {
+          f = (sel_bm[c >> 5] >> (c & 31)) & 1;
+        } else {
+          const int lb = lower_bound_i(uc, p.Kb, c);
+          f = (lb < p.Kb && uc[lb] == c) ? 1 : 0;
+        }
       }
       int tot;
       const int ex = block_excl_scan(f, red, &tot);
@@ -427,8 +446,16 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
         kind = 0;
         if (p.tok_out) {
           const int r = ur[gi], c = r / p.cs;
-          const int lb = lower_bound_i(uc, p.Kb, c);
-          const bool inA = lb < p.Kb && uc[lb] == c;
+          int lb;
+          bool inA;
+          if (sel_bm) {
+            const uint32_t wv = sel_bm[c >> 5], bit = 1u << (c & 31);
+            lb = wpre[c >> 5] + __popc(wv & (bit - 1u));
+            inA = (wv & bit) != 0u;
+          } else {
+            lb = lower_bound_i(uc, p.Kb, c);
+            inA = lb < p.Kb && uc[lb] == c;
+          }
           const int pos = gi + lb * p.cs + (inA ? r - c * p.cs : 0) - ud[gi];
           if (pos < p.tcap) p.tok_out[(size_t)b * p.tcap + pos] = r;
         }

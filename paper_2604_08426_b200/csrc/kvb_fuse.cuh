@@ -6,15 +6,20 @@
 // any inter-CTA communication:
 //   1. derives the threshold bin tb and the count kb to take inside it from
 //      the histogram (bins scanned from the top);
-//   2. streams the sequence's scores once (L2-resident, 64 KiB at C2):
-//      keys with bin > tb go straight into a shared-memory bitmap, keys in the
-//      threshold bin are appended to a shared candidate list;
-//   3. one warp bisects the candidates' low 21 bits for the K-th key T and
-//      marks the winners: keys above T, then the lowest ids among the ties --
-//      exactly the set of np.argsort(-s, kind="stable")[:K] (ties to the
-//      lowest id, -0 == +0 through score_key). With more candidates than the
-//      shared list holds, the same bisection runs block-wide over all scores
-//      (slow, exact; pathological ties only).
+//   2. streams the sequence's scores once (staged in shared memory by bulk
+//      copies, 64 KiB at C2), each thread over its own run of bitmap words,
+//      comparing with the bin boundaries in the float domain: "bin > tb" bits
+//      become whole bitmap words, threshold-bin scores are appended to a
+//      shared candidate list as 64-bit composites (key << 32 | ~id) at
+//      offsets from one block scan of the per-thread counts;
+//   3. the winners of the threshold bin are the kb largest composites, i.e.
+//      larger key first, then lower id -- exactly the members of
+//      np.argsort(-s, kind="stable")[:K] (ties to the lowest id, -0 == +0
+//      through score_key): one 8-bit radix round over the next key bits
+//      finds the crossing sub-bin, whose few candidates are ranked among
+//      themselves. Beyond kRankMax candidates a block-wide 3x7-bit radix
+//      k-th key; with more candidates than the shared list holds, an exact
+//      bisection over all scores (pathological ties).
 // The bitmap then yields the ascending id list by one block scan. The merge
 // kernel that follows the attention re-zeroes the histogram.
 
@@ -30,7 +35,7 @@ constexpr int kFuseHistBins = 2048;
 __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
                                                int* s_kb) {
   const int tid = threadIdx.x;
-  constexpr int kMaxPer = 64;  // blockDim.x >= 32
+  constexpr int kMaxPer = 16;  // blockDim.x >= 128
   const int per = kFuseHistBins / blockDim.x;
   int hv[kMaxPer];
   int loc = 0;
@@ -81,10 +86,12 @@ __device__ __forceinline__ void fuse_mbar_wait0(uint64_t* b) {
       : "memory");
 }
 
+constexpr int kRankMax = 2048;  // threshold-bin candidates resolved by direct ranking
+
 __device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
-                                   uint32_t* sbm, uint32_t* sk, int32_t* si, int cap, int* red,
+                                   uint32_t* sbm, uint64_t* cd, int cap, int* red,
                                    uint64_t* tr = nullptr, const float* stage = nullptr,
-                                   uint64_t* stage_bar = nullptr, int dbg_copy_only = 0) {
+                                   uint64_t* stage_bar = nullptr) {
   __shared__ int s_tb, s_kb, s_nc, s_gt, s_eq;
   __shared__ uint32_t s_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
@@ -99,89 +106,143 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
   fuse_threshold(hb, K, red, &s_tb, &s_kb);
   const uint32_t tb = (uint32_t)s_tb;
   sel_stamp(tr, 0);
-  auto visit = [&](int i, float v) {
-    const uint32_t key = score_key(v), bin = key >> 21;
-    if (bin > tb) {
-      atomicOr(sbm + (i >> 5), 1u << (i & 31));
-    } else if (bin == tb) {
-      const int pos = atomicAdd(&s_nc, 1);
-      if (pos < cap) {
-        sk[pos] = key;
-        si[pos] = i;
-      }
-    }
-  };
-  if (stage) {
+  // Bin tests in the float domain: score_key is a monotone bijection on
+  // non-NaN scores (-0 == +0), so key >= b << 21 <=> s >= key_score(b << 21)
+  // whenever that boundary is an ordinary float (bins 4..2043; finite scores
+  // live in bins 3..2044). Outside that range: the per-score key path below.
+  const bool fbins = tb >= 4u && tb <= 2042u;
+  const float lo_f = key_score(tb << 21), hi_f = key_score((tb + 1u) << 21);
+  // Thread t owns bitmap words [t*segw, (t+1)*segw) of the scores: the
+  // bin > tb bits are built in registers and stored as whole words, the
+  // threshold-bin bits kept as a mask; one block scan of the per-thread
+  // counts places every thread's candidates (no atomics, every load
+  // independent). Float4 j of a word is read in lane-rotated order
+  // ((j + lane) & 7): 8 lanes of a phase hit 8 distinct 16-B bank groups.
+  constexpr int kMaxSegW = 4;  // words per thread: M <= 32768 at 256 threads
+  const int segw = (W + nthr - 1) / nthr;
+  if (fbins && stage && segw <= kMaxSegW) {
     fuse_mbar_wait0(stage_bar);
-    if (dbg_copy_only) {  // profiling: the staging copy alone (empty selection)
-      __syncthreads();
-      sel_stamp(tr, 1);
-      return;
-    }
-    // 4 scores per LDS.128 and 4 independent loads per iteration: at 8 warps
-    // per SM a serial per-score chain is latency-bound (~10 us at C2); keys at
-    // or above the threshold bin (~3% of them) take the rare branch
-    const float4* s4 = reinterpret_cast<const float4*>(stage);
-    const int M4 = M >> 2;  // staged => M % 4 == 0
-#pragma unroll 4
-    for (int j = tid; j < M4; j += nthr) {
-      const float4 v = s4[j];
-      const uint32_t k0 = score_key(v.x), k1 = score_key(v.y), k2 = score_key(v.z), k3 = score_key(v.w);
-      const uint32_t kmax = max(max(k0, k1), max(k2, k3));
-      if ((kmax >> 21) >= tb) {
-        const uint32_t kk[4] = {k0, k1, k2, k3};
-        uint32_t wm = 0u;
+    sel_stamp(tr, 6);
+    const int wlo = min(W, tid * segw), whi = min(W, wlo + segw);
+    uint32_t em[kMaxSegW];
+    int cnt = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t bin = kk[e] >> 21;
-          if (bin > tb) wm |= 1u << e;
-          if (bin == tb) {
-            const int pos = atomicAdd(&s_nc, 1);
-            if (pos < cap) {
-              sk[pos] = kk[e];
-              si[pos] = 4 * j + e;
-            }
-          }
+    for (int q = 0; q < kMaxSegW; ++q) {
+      em[q] = 0u;
+      const int w = wlo + q;
+      if (w < whi) {
+        uint32_t g = 0u, e = 0u;
+#pragma unroll
+        for (int j0 = 0; j0 < 8; ++j0) {
+          const int j = (j0 + lane) & 7;
+          const int i = 32 * w + 4 * j;  // staged => M % 4 == 0: all or none of the 4 are < M
+          const float4 v = i < M ? *reinterpret_cast<const float4*>(stage + i)
+                                 : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+          const uint32_t gb = (v.x >= hi_f ? 1u : 0u) | (v.y >= hi_f ? 2u : 0u) | (v.z >= hi_f ? 4u : 0u) |
+                              (v.w >= hi_f ? 8u : 0u);
+          const uint32_t ge = (v.x >= lo_f ? 1u : 0u) | (v.y >= lo_f ? 2u : 0u) | (v.z >= lo_f ? 4u : 0u) |
+                              (v.w >= lo_f ? 8u : 0u);
+          g |= gb << (4 * j);
+          e |= (ge & ~gb) << (4 * j);
         }
-        if (wm) atomicOr(sbm + ((4 * j) >> 5), wm << ((4 * j) & 31));
+        sbm[w] = g;
+        em[q] = e;
+        cnt += __popc(e);
       }
     }
-  } else if ((M & 3) == 0 && ((reinterpret_cast<uintptr_t>(sc) & 15) == 0)) {
-    // U float4 loads in flight per thread per round (the shared-memory atomics
-    // in visit() would otherwise serialise one L2 round trip per load)
-    constexpr int U = 16;
-    const float4* s4 = reinterpret_cast<const float4*>(sc);
-    const int M4 = M >> 2;
-    for (int i0 = tid; i0 < M4; i0 += nthr * U) {
-      float4 v[U];
+    int tot;
+    int pos = block_excl_scan(cnt, red, &tot);
+    if (tid == 0) s_nc = tot;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nthr;
-        v[u] = i < M4 ? __ldcg(s4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nthr;
-        if (i < M4) {
-          visit(4 * i, v[u].x);
-          visit(4 * i + 1, v[u].y);
-          visit(4 * i + 2, v[u].z);
-          visit(4 * i + 3, v[u].w);
-        }
+    for (int q = 0; q < kMaxSegW; ++q) {
+      uint32_t e = em[q];
+      while (e) {
+        const int bit = __ffs(e) - 1;
+        e &= e - 1u;
+        const uint32_t id = (uint32_t)(32 * (wlo + q) + bit);
+        if (pos < cap) cd[pos] = ((uint64_t)score_key(stage[id]) << 32) | (uint64_t)(~id);
+        ++pos;
       }
     }
   } else {
-    for (int i = tid; i < M; i += nthr) visit(i, __ldcg(sc + i));
+    if (stage) fuse_mbar_wait0(stage_bar);
+    // unstaged scores or extreme threshold bins: per-score keys, shared atomics
+    for (int i = tid; i < M; i += nthr) {
+      const uint32_t key = score_key(__ldcg(sc + i)), bin = key >> 21;
+      if (bin > tb) {
+        atomicOr(sbm + (i >> 5), 1u << (i & 31));
+      } else if (bin == tb) {
+        const int pos = atomicAdd(&s_nc, 1);
+        if (pos < cap) cd[pos] = ((uint64_t)key << 32) | (uint64_t)(~(uint32_t)i);
+      }
+    }
   }
   __syncthreads();
   sel_stamp(tr, 1);
   const int nc = s_nc, kb = s_kb;
-  if (nc <= cap) {
+  if (nc <= kRankMax && 2 * nc <= cap) {
+    // one 8-bit radix round over key bits 20..13 (shared histogram), then the
+    // few candidates of the crossing sub-bin ranked among themselves
+    __shared__ int h8[256];
+    __shared__ int s_sb, s_kb2, s_n3;
+    for (int i = tid; i < 256; i += nthr) h8[i] = 0;
+    if (tid == 0) s_n3 = 0;
+    __syncthreads();
+    for (int i = tid; i < nc; i += nthr) atomicAdd(&h8[(uint32_t)(cd[i] >> 45) & 255u], 1);
+    __syncthreads();
+    if (tid < 32) {  // lane l owns sub-bins 255-8l .. 248-8l (descending)
+      int c[8], loc = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c[q] = h8[255 - 8 * lane - q];
+        loc += c[q];
+      }
+      const int inc = warp_incl_scan(loc, lane);
+      int above = inc - loc;
+      if (above < kb && kb <= inc) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (above + c[q] >= kb) {
+            s_sb = 255 - 8 * lane - q;
+            s_kb2 = kb - above;
+            break;
+          }
+          above += c[q];
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t sb = (uint32_t)s_sb;
+    uint64_t* c3 = cd + nc;  // the crossing sub-bin's candidates
+    for (int i = tid; i < nc; i += nthr) {
+      const uint64_t me = cd[i];
+      const uint32_t b8 = (uint32_t)(me >> 45) & 255u;
+      if (b8 > sb) {
+        const uint32_t id = ~(uint32_t)me;
+        atomicOr(sbm + (id >> 5), 1u << (id & 31));
+      } else if (b8 == sb) {
+        c3[atomicAdd(&s_n3, 1)] = me;
+      }
+    }
+    __syncthreads();
+    const int n3 = s_n3, kb2 = s_kb2;
+    for (int i = tid; i < n3; i += nthr) {
+      const uint64_t me = c3[i];
+      int r = 0;
+      for (int q = 0; q < n3; ++q) r += c3[q] > me ? 1 : 0;
+      if (r < kb2) {
+        const uint32_t id = ~(uint32_t)me;
+        atomicOr(sbm + (id >> 5), 1u << (id & 31));
+      }
+    }
+    sel_stamp(tr, 2);
+  } else if (nc <= cap) {
     {
       __shared__ int khist[128];
       uint32_t T0;
       int gt, eq;
-      block_kth_key([&](int i) { return sk[i]; }, nc, tb << 21, kb, khist, red, &T0, &gt, &eq);
+      block_kth_key([&](int i) { return (uint32_t)(cd[i] >> 32); }, nc, tb << 21, kb, khist, red, &T0,
+                    &gt, &eq);
       if (tid == 0) {
         s_T = T0;
         s_gt = gt;
@@ -194,14 +255,15 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
     const int need = kb - s_gt;
     const bool all_ties = need == s_eq;
     for (int i = tid; i < nc; i += nthr) {
-      const uint32_t k = sk[i];
+      const uint32_t k = (uint32_t)(cd[i] >> 32), id = ~(uint32_t)cd[i];
       bool take = k > T || (all_ties && k == T);
       if (!take && k == T) {  // the `need` lowest ids among the ties
         int rank = 0;
-        for (int j = 0; j < nc; ++j) rank += (sk[j] == T && si[j] < si[i]) ? 1 : 0;
+        for (int j = 0; j < nc; ++j)
+          rank += ((uint32_t)(cd[j] >> 32) == T && ~(uint32_t)cd[j] < id) ? 1 : 0;
         take = rank < need;
       }
-      if (take) atomicOr(sbm + (si[i] >> 5), 1u << (si[i] & 31));
+      if (take) atomicOr(sbm + (id >> 5), 1u << (id & 31));
     }
   } else {
     // overflow: the same bisection block-wide over every score of the bin

@@ -45,7 +45,7 @@ def report(tag, lib, B, S):
         ncand = sub[:, 7]
         if (ncand > 0).any():
             print(f"    threshold-bin candidates per CTA: min {ncand.min():.0f} med {np.median(ncand):.0f} max {ncand.max():.0f}")
-        names = ["threshold", "scan", "bisect", "winners", "id list", "union prefix"]
+        names = ["threshold", "scan", "bisect", "winners", "id list", "union prefix", "scores staged"]
         w = ph[:, 6]
         for i, nm in enumerate(names):
             col = sub[:, i]
