@@ -9,6 +9,7 @@ python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 for t in "$@"; do
   if [ "$t" = base ]; then unset KVB_LIB_TAG; else export KVB_LIB_TAG=$t; fi
   timeout 300 python tools/trace_attend.py > $O/trace_$t.txt 2>&1
+  timeout 300 python tools/timeline.py --layers 4 > $O/tl_$t.txt 2>&1
   timeout 600 python bench.py --steps 20 --warmup 3 --also "" ${BENCH_ARGS:-} > $O/bench_$t.json 2> $O/bench_$t.err
   python - "$O/bench_$t.json" "$t" <<'PY'
 import json, sys
