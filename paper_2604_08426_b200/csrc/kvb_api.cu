@@ -37,6 +37,12 @@ cudaError_t ensure_smem(const void* func, size_t bytes) {
     size_t v = 0;
     if (cudaFuncGetAttributes(&attr, func) == cudaSuccess) v = attr.sharedSizeBytes;
     sb = static_bytes.emplace(func, v).first;
+    // one L1/shared split for every kernel: CTAs of the PDL-overlapped decode
+    // kernels then share an SM without waiting for it to drain and re-split
+#ifndef KVB_EXP_NOCARVE
+    cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+#endif
   }
   if (bytes + sb->second <= 48 * 1024) return cudaSuccess;
   auto it = done.find(func);

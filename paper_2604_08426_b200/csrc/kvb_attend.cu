@@ -650,12 +650,23 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                const uint16_t* __restrict__ right,
                                                float* __restrict__ q2, float* __restrict__ qt2,
                                                int H, int G, int D, int r, int sgroups,
-                                               int* __restrict__ counters) {
+                                               int* __restrict__ counters, uint64_t* tr) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
+  // profiling (kvb_trace_enable): per-CTA entry / PDL wait passed / exit
+  if (tr) tr += kTracePrep + 4 * (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      tr[k] = t;
+    }
+  };
+  stamp(0);
   // decode step: PDL-launched behind the previous layer -- wait for it before
   // touching q, then let the PDL-launched scan start beside this kernel
   pdl_wait();
+  stamp(1);
   pdl_trigger();
   // split tickets of the attention that follows (self-resetting; zeroed here
   // so a fresh caller workspace needs no memset)
@@ -709,6 +720,7 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
     for (int d = 0; d < D; ++d) acc = fmaf(rw[d], qq[d], acc);
     qt2[(size_t)b * HG * r + ((size_t)(rr >> 1) * HG + h * G + g) * 2 + (rr & 1)] = acc;
   }
+  stamp(2);
 }
 
 struct AttGeom {
@@ -822,8 +834,9 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   float* qt2 = w.qt2;
   int Hh = H, Gg = G, Dd = D, rr = r, sg = svd ? s->d.svd_groups : 1;
   int* ctr = w.counters;
+  uint64_t* tr = trace_buffer();
   void* args[] = {(void*)&q, (void*)&right, (void*)&q2, (void*)&qt2, (void*)&Hh, (void*)&Gg,
-                  (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr};
+                  (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr, (void*)&tr};
   const dim3 grid(H, B, svd ? 4 : 1);
   if (pdl) return launch_pdl((const void*)k5_prep, grid, dim3(256), fs, st, args);
   return cudaLaunchKernel((const void*)k5_prep, grid, dim3(256), args, fs, st);

@@ -854,6 +854,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(saddr(full + tid)) : "memory");
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(saddr(empty + tid)) : "memory");
   }
+  if (p.trace && tid == 0) p.trace[kTraceAttExit + (size_t)b * S + split] = gtimer();
 }
 
 template <int QW, int NKS, int VAR>

@@ -83,6 +83,9 @@ bool trace_enable(int on);
 uint64_t* trace_buffer();  // null when disabled
 int64_t trace_read(uint64_t* host, int64_t max_words);
 constexpr int64_t kTraceWords = 1 << 16;
+constexpr int64_t kTraceK1 = 8192;     // dense scan: [CTA][4] entry / scan end / exit
+constexpr int64_t kTracePrep = 12288;  // decode prep: [CTA][4] entry / waited / exit
+constexpr int64_t kTraceAttExit = 16384;  // bulk attention: [CTA] exit
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
 cudaError_t ensure_smem(const void* func, size_t bytes);

@@ -51,11 +51,21 @@ constexpr int kHistBins = 2048;
 template <typename T, int VW, int NV>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
-             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist) {
+             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist, uint64_t* __restrict__ tr) {
   extern __shared__ float qbar[];
   __shared__ uint32_t shist[kHistBins];
   const int E = Hkv * D;
   const int b = blockIdx.y;
+  // profiling (kvb_trace_enable): per-CTA entry / scan end / exit %globaltimer
+  if (tr) tr += 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x);
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      tr[k] = t;
+    }
+  };
+  stamp(0);
   pdl_trigger();  // the next kernel may launch now; it waits for this grid
   load_qbar(q + (size_t)b * Hkv * G * D, Hkv, G, D, qbar);
   if (hist)
@@ -184,6 +194,7 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
     }
   }
   }
+  stamp(1);
   if (hist) {
     __syncthreads();
     uint32_t* gh = hist + (size_t)b * kHistBins;
@@ -193,13 +204,15 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
   // PDL-launched behind k5_prep (decode step): this grid's completion then
   // implies the prep's, for the attention that waits on this grid
   pdl_wait();
+  stamp(2);
 }
 
 // Generic fallback for very wide rows: identical order, q_bar read from smem.
 template <typename T, int VW>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
-                  float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist) {
+                  float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist,
+                  uint64_t*) {
   extern __shared__ float qbar[];
   const int E = Hkv * D;
   const int b = blockIdx.y;
@@ -461,8 +474,11 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   ensure_smem(fn, smem);
   dim3 grid(score_grid_x(C, B, fn, smem), B);
   count_launch();
+  uint64_t* tr = trace_buffer();
+  if (tr && (size_t)grid.x * grid.y * 4 <= 4096) tr += kTraceK1;
+  else tr = nullptr;
   void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D,
-                  (void*)&hist};
+                  (void*)&hist, (void*)&tr};
   if (pdl) return launch_pdl(fn, grid, dim3(kScoreThreads), smem, st, args);
   return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
