@@ -283,7 +283,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     pre_done = min(min(2, n_rloc / ett), nst - 1);
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
-      if (k % H != warp) continue;
+      if (warp != H) continue;  // the producer warp
       unsigned char* st = ring + (size_t)k * p.stage_bytes;
       const int j = lane & 15;
       uint32_t bytes = lane < 16 && j < ett ? (uint32_t)(2 * vbytes0) : 0u;
@@ -503,24 +503,21 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   const int vrow = p.vrow;
   const int vbytes = H * kBD * 2;
 
-  // ---- production: tile k is staged by warp k % H (one lane per token) ---------------
-  // Issued by a consumer warp just before it consumes tile k - (stages - 1);
-  // the slot's previous tile k - stages has then been released by this warp,
-  // so the wait is only for slower warps. 8 warps = 2 per SM sub-partition,
-  // which leaves the consumers up to 255 registers.
+  // ---- production: a dedicated producer warp (warp H) stages every tile ---------------
+  // (one lane per token), as soon as the slot's previous tile has been
+  // released by all H consumer warps -- the consumers never issue copies or
+  // wait on each other's releases.
   const int lbytes = p.sgroups * p.r * 2;
   // called for k = 0, 1, 2, ... in order by every warp (slot / round / owner
   // tracked incrementally: no integer division in the loop)
-  int pk_stg = 0, pk_rnd = 0, pk_own = 0;
+  int pk_stg = 0, pk_rnd = 0;
   auto produce = [&](int k) {
     const int stg = pk_stg, rnd = pk_rnd;
-    const bool mine = pk_own == warp;
     if (++pk_stg == nst) {
       pk_stg = 0;
       ++pk_rnd;
     }
-    if (++pk_own == H) pk_own = 0;
-    if (k >= ntiles || !mine || k < pre_done) return;  // k < pre_done: staged before the wait
+    if (k >= ntiles || k < pre_done) return;  // k < pre_done: staged before the wait
     if (rnd > 0) mbar_wait(empty + stg, (rnd - 1) & 1);
     const bool sv = k >= t_ex;
     const int tt = sv ? kBT : ett;
@@ -565,7 +562,9 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       else bulk_g2s(st + tt * vrow + j * krow, ksrc, kb, full + stg);
     }
   };
-  for (int k = 0; k < nst - 1; ++k) produce(k);
+  if (warp == H) {
+    for (int k = 0; k < ntiles; ++k) produce(k);
+  } else {
   int c_stg = 0, c_rnd = 0;  // consumer ring position
   auto next_slot = [&](int& stg, int& par) {
     stg = c_stg;
@@ -705,7 +704,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       }
     }
     for (int k = 0; k < t_ex; ++k) {
-      produce(k + nst - 1);
       int stg, par;
       next_slot(stg, par);
       mbar_wait(full + stg, par);
@@ -749,7 +747,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     // K3 (kvb_recon.cu) already produced q.k of the reconstructed keys: the
     // staged row of token j holds logits[(h, g)] for every head
     for (int k = t_ex; k < ntiles; ++k) {
-      produce(k + nst - 1);
       int stg, par;
       next_slot(stg, par);
       mbar_wait(full + stg, par);
@@ -787,7 +784,6 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       }
     const int hgrp = h / (H / p.sgroups);
     for (int k = t_ex; k < ntiles; ++k) {
-      produce(k + nst - 1);
       int stg, par;
       next_slot(stg, par);
       mbar_wait(full + stg, par);
@@ -847,6 +843,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       const int q = qa + (e & 1);
       if (writer && q < G) p.po[(pb + q) * kBD + mt * 16 + g4 + 8 * (e >> 1)] = v;
     }
+  }  // consumers
   KVB_STAMP(5);
   // the ring barriers are re-initialised by the next item of a persistent CTA
   __syncthreads();
@@ -858,7 +855,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
 }
 
 template <int QW, int NKS, int VAR>
-__global__ void __maxnreg__(232) k5_attend_bulk(const __grid_constant__ BulkParams p) {
+__global__ void __maxnreg__(168) k5_attend_bulk(const __grid_constant__ BulkParams p) {
   extern __shared__ __align__(128) unsigned char sm[];
   attend_item<QW, NKS, VAR>(p, blockIdx.y, blockIdx.x, gridDim.x, sm);
 }
@@ -1062,7 +1059,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
-  cudaError_t le = launch_pdl(fn, grid, dim3(H * 32), g.smem, st, args);
+  // H consumer warps (one per KV head) + one producer warp
+  cudaError_t le = launch_pdl(fn, grid, dim3(H * 32 + 32), g.smem, st, args);
   if (le != cudaSuccess) return le;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -31,26 +31,29 @@ namespace kvb {
 
 constexpr int kFuseHistBins = 2048;
 
-// Threshold bin: bins in descending order; blockDim.x must divide 2048.
+// Threshold bin: bins in descending order, a run of `per` bins per thread
+// (threads past bin 2047 hold none); blockDim.x >= 128.
 __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
                                                int* s_kb) {
   const int tid = threadIdx.x;
-  constexpr int kMaxPer = 16;  // blockDim.x >= 128
-  const int per = kFuseHistBins / blockDim.x;
+  constexpr int kMaxPer = 16;
+  const int per = (kFuseHistBins + blockDim.x - 1) / blockDim.x;
   int hv[kMaxPer];
   int loc = 0;
 #pragma unroll
-  for (int j = 0; j < kMaxPer; ++j)
-    if (j < per) {
+  for (int j = 0; j < kMaxPer; ++j) {
+    hv[j] = 0;
+    if (j < per && tid * per + j < kFuseHistBins) {
       hv[j] = (int)__ldcg(hb + kFuseHistBins - 1 - (tid * per + j));
       loc += hv[j];
     }
+  }
   int tot;
   int above = block_excl_scan(loc, red, &tot);
   if (above < K && K <= above + loc) {
 #pragma unroll
     for (int j = 0; j < kMaxPer; ++j) {
-      if (j >= per) break;
+      if (j >= per || tid * per + j >= kFuseHistBins) break;
       const int bin = kFuseHistBins - 1 - (tid * per + j);
       const int c = hv[j];
       if (above + c >= K) {
