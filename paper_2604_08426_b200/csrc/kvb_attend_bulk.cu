@@ -49,6 +49,14 @@ constexpr int kBT = 16;       // tokens per tile
 constexpr int kBMaxKs = 10;   // SVD rank <= 160
 constexpr int kBMaxStages = 8;
 constexpr float kLazy = 8.f;  // rescale threshold (natural-log units)
+#ifndef KVB_BULK_PRODUCERS
+#define KVB_BULK_PRODUCERS 2
+#endif
+// producer warps: each bulk copy is issued through a uniform-register
+// waterfall (~40 instructions), so one warp issues ~1 tile per us -- the
+// consumers' pace; two or more keep the ring ahead of them. Warps per CTA:
+// H consumers + producers <= 12 (3 per SM sub-partition at <= 168 registers).
+constexpr int kBProducers = KVB_BULK_PRODUCERS;
 
 struct BulkParams {
   // work stream
@@ -283,7 +291,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     pre_done = min(min(2, n_rloc / ett), nst - 1);
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
-      if (warp != H) continue;  // the producer warp
+      if (warp != H + k % kBProducers) continue;  // tile k's producer warp
       unsigned char* st = ring + (size_t)k * p.stage_bytes;
       const int j = lane & 15;
       uint32_t bytes = lane < 16 && j < ett ? (uint32_t)(2 * vbytes0) : 0u;
@@ -510,13 +518,8 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   const int lbytes = p.sgroups * p.r * 2;
   // called for k = 0, 1, 2, ... in order by every warp (slot / round / owner
   // tracked incrementally: no integer division in the loop)
-  int pk_stg = 0, pk_rnd = 0;
   auto produce = [&](int k) {
-    const int stg = pk_stg, rnd = pk_rnd;
-    if (++pk_stg == nst) {
-      pk_stg = 0;
-      ++pk_rnd;
-    }
+    const int rnd = k / nst, stg = k - rnd * nst;
     if (k >= ntiles || k < pre_done) return;  // k < pre_done: staged before the wait
     if (rnd > 0) mbar_wait(empty + stg, (rnd - 1) & 1);
     const bool sv = k >= t_ex;
@@ -562,8 +565,8 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       else bulk_g2s(st + tt * vrow + j * krow, ksrc, kb, full + stg);
     }
   };
-  if (warp == H) {
-    for (int k = 0; k < ntiles; ++k) produce(k);
+  if (warp >= H) {  // producer warps take tiles round-robin (copy issue rate)
+    for (int k = warp - H; k < ntiles; k += kBProducers) produce(k);
   } else {
   int c_stg = 0, c_rnd = 0;  // consumer ring position
   auto next_slot = [&](int& stg, int& par) {
@@ -1059,8 +1062,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
-  // H consumer warps (one per KV head) + one producer warp
-  cudaError_t le = launch_pdl(fn, grid, dim3(H * 32 + 32), g.smem, st, args);
+  // H consumer warps (one per KV head) + the producer warps
+  cudaError_t le = launch_pdl(fn, grid, dim3(H * 32 + 32 * kBProducers), g.smem, st, args);
   if (le != cudaSuccess) return le;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -117,6 +117,15 @@ def main():
     for i, nm in enumerate(["start", "setup", "prologue", "first_tile", "loop_end", "partials out"]):
         stats(nm, rel(att[:, i]))
     stats("pdl_waited", rel(att[:, 6]))
+    sel = block(n_att * 8 + 64, n_att, 8)
+    for i, nm in enumerate(["sel threshold", "sel scan", "sel rank", "sel winners", "sel id list",
+                            "sel union prefix", "sel scores staged"]):
+        stats(nm, rel(sel[:, i]))
+    sel2 = block(AEXIT + 4096, n_att, 8)
+    if np.isfinite(sel2[:, 0]).any():
+        print(" second selection pass (KVB_EXP_SELTWICE)")
+        for i, nm in enumerate(["sel threshold", "sel scan", "sel rank", "sel winners"]):
+            stats(nm, rel(sel2[:, i]))
     stats("exit (after merge)", rel(ax))
     print(f" layer: scan entry -> last attention exit {np.nanmax(rel(ax)):.2f} us")
 
