@@ -221,6 +221,7 @@ void free_store(kvb_store* s) {
   cudaFree(s->res_ids);
   cudaFree(s->res_count);
   cudaFree(s->k2_hist);
+  cudaFree(s->scan_done);
 
   cudaFree(s->k2_meta);
   cudaFree(s->k2_overflow);
@@ -395,6 +396,8 @@ kvb_status kvb_store_create(const kvb_store_desc* desc, kvb_store** out) {
   if ((st = dalloc((char**)&s->res_k, B * R * E * s->esz, "resident K")) != KVB_OK) return bail(st);
   if ((st = dalloc((char**)&s->res_v, B * R * E * s->esz, "resident V")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_hist, B * kTopHistBins, "K2 histogram")) != KVB_OK) return bail(st);
+  if ((st = dalloc(&s->scan_done, B, "scan done counters")) != KVB_OK) return bail(st);
+  cudaMemset(s->scan_done, 0, B * sizeof(int32_t));
   if ((st = dalloc(&s->k2_meta, B * 4, "K2 meta")) != KVB_OK) return bail(st);
   if ((st = dalloc(&s->k2_overflow, B, "K2 overflow")) != KVB_OK) return bail(st);
   s->Wc = (s->C + 31) / 32;
@@ -957,6 +960,7 @@ kvb_status kvb_select_residual(kvb_store* s, const float* q, const kvb_residual_
     // finish with the rank-order sort (K2b); store-owned self-cleaning scratch
     if (s->k2_dirty) {
       KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * B * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->scan_done, 0, sizeof(int32_t) * s->d.batch, st), "scan counter reset");
       KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * B * 4, st), "meta reset");
     }
     s->k2_dirty = true;
@@ -1144,14 +1148,17 @@ kvb_status kvb_decode_step(kvb_store* s, const float* q, const kvb_select_args* 
     void* tcws = sv.take<char>(higgs_tc_ws_bytes(s));
     if (s->k2_dirty) {  // a previous chain aborted part-way: histogram and K2 counters
       KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+      KVB_CUDA(cudaMemsetAsync(s->scan_done, 0, sizeof(int32_t) * s->d.batch, st), "scan counter reset");
       KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * s->d.batch * 4, st), "meta reset");
       s->k2_dirty = false;
     }
     s->k2_dirty = true;
+    s->scan_ctas = 0;
     if (tc_scan)
       KVB_CUDA(launch_score_higgs_tc(s, q, L.G, sc, tcws, s->k2_hist, st), "HIGGS tensor-core scoring");
     else
-      KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, inline_prep),
+      KVB_CUDA(launch_score_dense(s, q, L.G, KVB_AGG_SUM, sc, s->k2_hist, st, inline_prep,
+                                  inline_prep ? s->scan_done : nullptr, &s->scan_ctas),
                "landmark scoring");
     if (!inline_prep) KVB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0), "join wait");
     KVB_CUDA(launch_attend_chunks(s, L, nullptr, K, st, sc, s->k2_hist, chunk_ids), "sparse attention");
@@ -1208,6 +1215,7 @@ kvb_status kvb_select_candidates(kvb_store* s, const float* q, int32_t G, int32_
   const bool use_hist = agg == KVB_AGG_SUM && s->d.landmark_kind == KVB_LM_DENSE;
   if (use_hist && s->k2_dirty) {
     KVB_CUDA(cudaMemsetAsync(s->k2_hist, 0, sizeof(uint32_t) * s->d.batch * kTopHistBins, st), "hist reset");
+    KVB_CUDA(cudaMemsetAsync(s->scan_done, 0, sizeof(int32_t) * s->d.batch, st), "scan counter reset");
     KVB_CUDA(cudaMemsetAsync(s->k2_meta, 0, sizeof(int32_t) * s->d.batch * 4, st), "meta reset");
     s->k2_dirty = false;
   }

@@ -102,6 +102,8 @@ struct BulkParams {
   // geometry
   int maxper, vrow, krow_ex, krow_sv, stage_bytes, off_tab, off_bar, off_stage;
   int nB;                     // batch (grid y of the split-K launch)
+  const int32_t* scan_done;   // decode step: finished scan CTAs per sequence (spin instead of PDL wait)
+  int scan_ctas;              // scan CTAs per sequence
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -305,7 +307,26 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
       }
     }
   }
-  pdl_wait();  // the selection (token / chunk list) of the previous kernel
+  if (VAR == 2 && p.scan_done) {
+    // decode step: this sequence's scan CTAs have published their scores,
+    // histogram and (through their own PDL wait) the prep's q~ -- no need to
+    // wait for the whole scan grid to retire and flush
+    __shared__ int s_go;
+    if (tid == 0) {
+      const int* cnt = p.scan_done + b;
+      for (long long it = 0;; ++it) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+        if (v >= p.scan_ctas) break;
+        if (it > (1ll << 24)) __trap();  // a lost count must fail the launch, not hang
+        __nanosleep(20);
+      }
+      s_go = 1;
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();  // the selection (token / chunk list) of the previous kernel
+  }
   KVB_STAMP(6);
   if (p.mode == 0) {  // token mode: the list length comes from the selection kernel
     const int P = p.nitems[b];
@@ -863,16 +884,20 @@ __global__ void __maxnreg__(168) k5_attend_bulk(const __grid_constant__ BulkPara
   attend_item<QW, NKS, VAR>(p, blockIdx.y, blockIdx.x, gridDim.x, sm);
 }
 
+#ifndef KVB_MERGE_MINB
+#define KVB_MERGE_MINB 4
+#endif
 // Exact LSE merge of the split partials: one CTA per (row = h*G + g, sequence),
 // thread d. Launched with programmatic stream serialization right behind
 // k5_attend_bulk (which triggers its dependents at entry), so its CTAs are
 // resident before the attention drains; griddepcontrol.wait then orders the
 // reads after the attention grid has completed and flushed.
-__global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict__ pm,
+__global__ void __launch_bounds__(128, KVB_MERGE_MINB) k5_merge_rows(const float* __restrict__ pm,
                                                      const float* __restrict__ pl,
                                                      const float* __restrict__ po, int S, int HG,
                                                      float* __restrict__ out, float* __restrict__ lse,
-                                                     uint32_t* __restrict__ hist_clear) {
+                                                     uint32_t* __restrict__ hist_clear,
+                                                     int32_t* __restrict__ done_clear) {
   const int row = blockIdx.x, b = blockIdx.y, d = threadIdx.x, lane = d & 31;
   // the next layer's (PDL-launched, waiting) prep may become resident now
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -880,14 +905,19 @@ __global__ void __launch_bounds__(128, 4) k5_merge_rows(const float* __restrict_
   // the attention (complete) was the last reader of the scan's histogram
   if (hist_clear && row == 0)
     for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
+  if (done_clear && row == 0 && d == 0) done_clear[b] = 0;  // every attention CTA has passed its spin
   const size_t base = (size_t)b * S * HG + row;
   float m = -INFINITY, acc = 0.f, L = 0.f;
-  constexpr int CH = 32;  // splits per round: one round for S <= 32, every load in flight
+#ifndef KVB_MERGE_CH
+#define KVB_MERGE_CH 32
+#endif
+  constexpr int CH = KVB_MERGE_CH;  // splits per round: one round for S <= CH, every load in flight
   for (int s0 = 0; s0 < S; s0 += CH) {
     // split (s0 + lane)'s (m, l) in lane registers; this thread's o column for all CH splits
     const int sl = s0 + lane;
-    const float ml = sl < S ? __ldcg(pm + base + (size_t)sl * HG) : -INFINITY;
-    const float ll = sl < S ? __ldcg(pl + base + (size_t)sl * HG) : 0.f;
+    const bool inr = lane < CH && sl < S;  // this round's splits only
+    const float ml = inr ? __ldcg(pm + base + (size_t)sl * HG) : -INFINITY;
+    const float ll = inr ? __ldcg(pl + base + (size_t)sl * HG) : 0.f;
     float ov[CH];
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
@@ -1059,6 +1089,12 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
 #undef KVB_BULK_VAR
   dim3 grid(g.splits, B);
   p.nB = B;
+#ifndef KVB_EXP_NOSPIN
+  p.scan_done = (var == 2 && s->scan_ctas > 0) ? s->scan_done : nullptr;
+#else
+  p.scan_done = nullptr;
+#endif
+  p.scan_ctas = s->scan_ctas;
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};
@@ -1079,7 +1115,8 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k5_merge_rows, (const float*)p.pm, (const float*)p.pl,
                             (const float*)p.po, g.splits, H * a.G, p.out, p.lse,
-                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr);
+                            p.sel_scores ? const_cast<uint32_t*>(p.sel_hist) : (uint32_t*)nullptr,
+                            const_cast<int32_t*>(p.scan_done));
   return cudaGetLastError();
 }
 

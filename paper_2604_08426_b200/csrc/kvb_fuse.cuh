@@ -32,32 +32,22 @@ namespace kvb {
 constexpr int kFuseHistBins = 2048;
 
 // Threshold bin: bins in descending order, a run of `per` bins per thread
-// (threads past bin 2047 hold none); blockDim.x >= 128.
+// (threads past bin 2047 hold none); any block size.
 __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
                                                int* s_kb) {
   const int tid = threadIdx.x;
-  constexpr int kMaxPer = 16;
   const int per = (kFuseHistBins + blockDim.x - 1) / blockDim.x;
-  int hv[kMaxPer];
+  const int i0 = tid * per, i1 = min(kFuseHistBins, i0 + per);
   int loc = 0;
-#pragma unroll
-  for (int j = 0; j < kMaxPer; ++j) {
-    hv[j] = 0;
-    if (j < per && tid * per + j < kFuseHistBins) {
-      hv[j] = (int)__ldcg(hb + kFuseHistBins - 1 - (tid * per + j));
-      loc += hv[j];
-    }
-  }
+#pragma unroll 8
+  for (int i = i0; i < i1; ++i) loc += (int)__ldcg(hb + kFuseHistBins - 1 - i);
   int tot;
   int above = block_excl_scan(loc, red, &tot);
-  if (above < K && K <= above + loc) {
-#pragma unroll
-    for (int j = 0; j < kMaxPer; ++j) {
-      if (j >= per || tid * per + j >= kFuseHistBins) break;
-      const int bin = kFuseHistBins - 1 - (tid * per + j);
-      const int c = hv[j];
+  if (above < K && K <= above + loc) {  // this thread's run holds the K-th largest key
+    for (int i = i0; i < i1; ++i) {
+      const int c = (int)__ldcg(hb + kFuseHistBins - 1 - i);
       if (above + c >= K) {
-        *s_tb = bin;
+        *s_tb = kFuseHistBins - 1 - i;
         *s_kb = K - above;
         break;
       }

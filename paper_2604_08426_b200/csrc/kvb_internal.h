@@ -41,6 +41,8 @@ struct kvb_store {
   // by K2b after use (no memset nodes in the decode step). One decode step per
   // store at a time (the store's side stream and events are per store too).
   uint32_t* k2_hist = nullptr;     // [B][2048] top-11-bit key histogram
+  int32_t* scan_done = nullptr;    // [B] finished scan CTAs per sequence (decode step; reset by the merge)
+  int scan_ctas = 0;               // scan CTAs per sequence of the last histogram scan launch
   int32_t* k2_meta = nullptr;      // [B][4] threshold bin / counts
   int32_t* k2_overflow = nullptr;  // [B]
   bool k2_dirty = false;           // a failed launch may have left scratch dirty
@@ -96,8 +98,11 @@ int resident_ctas(const void* func, int threads, size_t smem);
 // ---- launchers (stream-ordered, return cudaGetLastError()) ------------------
 // hist (may be null): [B][2048] uint32, zeroed by the caller; receives the
 // histogram of the top 11 bits of the score keys (sum aggregation only).
+// done (may be null): per-sequence counter each scan CTA increments when its
+// scores and histogram are published (decode step: the attention waits on it)
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl = false);
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl = false,
+                               int32_t* done = nullptr, int* ctas_per_seq = nullptr);
 constexpr int kTopHistBins = 2048;
 cudaError_t launch_score_higgs(const kvb_store* s, const float* q, int G, int agg,
                                float* scores, cudaStream_t st);

@@ -51,7 +51,8 @@ constexpr int kHistBins = 2048;
 template <typename T, int VW, int NV>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __restrict__ scores,
-             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist, uint64_t* __restrict__ tr) {
+             int C, int Hkv, int G, int D, uint32_t* __restrict__ hist, uint64_t* __restrict__ tr,
+             int32_t* __restrict__ done) {
   extern __shared__ float qbar[];
   __shared__ uint32_t shist[kHistBins];
   const int E = Hkv * D;
@@ -204,6 +205,16 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
   // PDL-launched behind k5_prep (decode step): this grid's completion then
   // implies the prep's, for the attention that waits on this grid
   pdl_wait();
+  if (done) {
+    // decode step: publish this CTA's scores + histogram (and, through the
+    // wait above, the prep's q~) to the attention CTAs of sequence b, which
+    // spin on the count instead of waiting for this whole grid to retire
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(done + b, 1);
+    }
+  }
   stamp(2);
 }
 
@@ -212,7 +223,7 @@ template <typename T, int VW>
 __global__ void __launch_bounds__(kScoreThreads)
 k1_dense_sum_wide(const T* __restrict__ lm, const float* __restrict__ q,
                   float* __restrict__ scores, int C, int Hkv, int G, int D, uint32_t* hist,
-                  uint64_t*) {
+                  uint64_t*, int32_t*) {
   extern __shared__ float qbar[];
   const int E = Hkv * D;
   const int b = blockIdx.y;
@@ -454,7 +465,8 @@ int score_grid_x(int C, int B, const void* func, size_t smem) {
 
 template <typename T>
 cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, int G,
-                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl) {
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl,
+                               int32_t* done, int* ctas_per_seq) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim, E = s->E;
   constexpr int VWv = 16 / sizeof(T);
   const bool vec = (E % VWv) == 0;
@@ -477,8 +489,11 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
   uint64_t* tr = trace_buffer();
   if (tr && (size_t)grid.x * grid.y * 4 <= 4096) tr += kTraceK1;
   else tr = nullptr;
+  const bool wide = fn == (const void*)k1_dense_sum_wide<T, VWv> || fn == (const void*)k1_dense_sum_wide<T, 1>;
+  if (wide) done = nullptr;  // the wide fallback publishes only by grid completion
+  if (ctas_per_seq) *ctas_per_seq = done ? (int)grid.x : 0;
   void* args[] = {(void*)&lm, (void*)&q, (void*)&scores, (void*)&C, (void*)&H, (void*)&G, (void*)&D,
-                  (void*)&hist, (void*)&tr};
+                  (void*)&hist, (void*)&tr, (void*)&done};
   if (pdl) return launch_pdl(fn, grid, dim3(kScoreThreads), smem, st, args);
   return cudaLaunchKernel(fn, grid, dim3(kScoreThreads), args, smem, st);
   return cudaGetLastError();
@@ -487,12 +502,16 @@ cudaError_t dense_sum_dispatch(const kvb_store* s, const T* lm, const float* q, 
 }  // namespace
 
 cudaError_t launch_score_dense(const kvb_store* s, const float* q, int G, int agg,
-                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl) {
+                               float* scores, uint32_t* hist, cudaStream_t st, bool pdl,
+                               int32_t* done, int* ctas_per_seq) {
   const int B = s->d.batch, C = s->C, H = s->d.kv_heads, D = s->d.head_dim;
+  if (ctas_per_seq) *ctas_per_seq = 0;
   if (agg == KVB_AGG_SUM) {
     if (s->d.kv_dtype == KVB_BF16)
-      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st, pdl);
-    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st, pdl);
+      return dense_sum_dispatch(s, (const __nv_bfloat16*)s->lm_dense, q, G, scores, hist, st, pdl,
+                                done, ctas_per_seq);
+    return dense_sum_dispatch(s, (const float*)s->lm_dense, q, G, scores, hist, st, pdl, done,
+                              ctas_per_seq);
   }
   if (pdl) return cudaErrorInvalidValue;  // the max scan is never PDL-chained
   const size_t smem = (size_t)H * G * D * sizeof(float);
