@@ -33,19 +33,23 @@ constexpr int kFuseHistBins = 2048;
 
 // Threshold bin: bins in descending order, a run of `per` bins per thread
 // (threads past bin 2047 hold none); any block size.
+// hb_shared: the histogram lives in shared memory (else global, read via L2).
+__device__ __forceinline__ uint32_t ld_hist(const uint32_t* hb, int i, bool hb_shared) {
+  return hb_shared ? hb[i] : __ldcg(hb + i);
+}
 __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* red, int* s_tb,
-                                               int* s_kb) {
+                                               int* s_kb, bool hb_shared = false) {
   const int tid = threadIdx.x;
   const int per = (kFuseHistBins + blockDim.x - 1) / blockDim.x;
   const int i0 = tid * per, i1 = min(kFuseHistBins, i0 + per);
   int loc = 0;
 #pragma unroll 8
-  for (int i = i0; i < i1; ++i) loc += (int)__ldcg(hb + kFuseHistBins - 1 - i);
+  for (int i = i0; i < i1; ++i) loc += (int)ld_hist(hb, kFuseHistBins - 1 - i, hb_shared);
   int tot;
   int above = block_excl_scan(loc, red, &tot);
   if (above < K && K <= above + loc) {  // this thread's run holds the K-th largest key
     for (int i = i0; i < i1; ++i) {
-      const int c = (int)__ldcg(hb + kFuseHistBins - 1 - i);
+      const int c = (int)ld_hist(hb, kFuseHistBins - 1 - i, hb_shared);
       if (above + c >= K) {
         *s_tb = kFuseHistBins - 1 - i;
         *s_kb = K - above;
@@ -81,10 +85,10 @@ __device__ __forceinline__ void fuse_mbar_wait0(uint64_t* b) {
 
 constexpr int kRankMax = 2048;  // threshold-bin candidates resolved by direct ranking
 
-__device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
+static __device__ void select_topk_shared(const float* __restrict__ sc, int M, const uint32_t* hb, int K,
                                    uint32_t* sbm, uint64_t* cd, int cap, int* red,
                                    uint64_t* tr = nullptr, const float* stage = nullptr,
-                                   uint64_t* stage_bar = nullptr) {
+                                   uint64_t* stage_bar = nullptr, bool hb_shared = false) {
   __shared__ int s_tb, s_kb, s_nc, s_gt, s_eq;
   __shared__ uint32_t s_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
@@ -96,7 +100,7 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
     s_nc = 0;
   }
   __syncthreads();
-  fuse_threshold(hb, K, red, &s_tb, &s_kb);
+  fuse_threshold(hb, K, red, &s_tb, &s_kb, hb_shared);
   const uint32_t tb = (uint32_t)s_tb;
   sel_stamp(tr, 0);
   // Bin tests in the float domain: score_key is a monotone bijection on
@@ -114,7 +118,7 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
   constexpr int kMaxSegW = 4;  // words per thread: M <= 32768 at 256 threads
   const int segw = (W + nthr - 1) / nthr;
   if (fbins && stage && segw <= kMaxSegW) {
-    fuse_mbar_wait0(stage_bar);
+    if (stage_bar) fuse_mbar_wait0(stage_bar);  // null: the caller staged the scores synchronously
     sel_stamp(tr, 6);
     const int wlo = min(W, tid * segw), whi = min(W, wlo + segw);
     uint32_t em[kMaxSegW];
@@ -158,7 +162,7 @@ __device__ void select_topk_shared(const float* __restrict__ sc, int M, const ui
       }
     }
   } else {
-    if (stage) fuse_mbar_wait0(stage_bar);
+    if (stage && stage_bar) fuse_mbar_wait0(stage_bar);
     // unstaged scores or extreme threshold bins: per-score keys, shared atomics
     for (int i = tid; i < M; i += nthr) {
       const uint32_t key = score_key(__ldcg(sc + i)), bin = key >> 21;

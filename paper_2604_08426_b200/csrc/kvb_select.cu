@@ -19,6 +19,7 @@
 
 #include "kvb_common.cuh"
 #include "kvb_internal.h"
+#include "kvb_fuse.cuh"
 
 namespace kvb {
 
@@ -377,6 +378,97 @@ __device__ __noinline__ void select_body(const SelParams& p, unsigned char* smem
 __global__ void __launch_bounds__(kSelThreads) k2_select(SelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   select_body(p, smem_raw);
+}
+
+// Token top-k of the Appendix-E stage 2 (selection.py:160-162; mode 1: items
+// are positions in the ascending candidate-token list, so lowest position ==
+// lowest token id) with the attention prologue's selection (kvb_fuse.cuh):
+// the sequence's M token scores staged in shared memory once, their 2048-bin
+// key histogram built there, float-domain bitmap scan + 8-bit radix + rank
+// for the threshold bin, then the sorted union with the residents. One CTA
+// per sequence; replaces select_body's four 8-bit radix passes (35 -> ~8 us
+// at C2 Proposed-B). Layout: [scores M4][hist 2048][selected bitmap][token
+// bitmap W][candidates].
+__global__ void __launch_bounds__(kSelThreads) k2_select_fuse(SelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int red[33];
+  const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  pdl_trigger();
+  pdl_wait();
+  const int M = p.m_count ? p.m_count[b] : p.M_stride;
+  const int M4 = (M + 3) & ~3;
+  const int K = p.K < M ? p.K : M;
+  const float* sc = p.scores + (size_t)b * p.M_stride;
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  const size_t mst = (size_t)((p.M_stride + 3) & ~3);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(stage + mst);
+  uint32_t* selbm = hist + kFuseHistBins;
+  const int Wm = (p.M_stride + 31) >> 5;
+  uint32_t* tbm = selbm + ((Wm + 3) & ~3);
+  uint64_t* cd = reinterpret_cast<uint64_t*>(tbm + ((p.W + 3) & ~3));
+  for (int i = tid; i < kFuseHistBins; i += nthr) hist[i] = 0u;
+  __syncthreads();
+  for (int i = tid; i < M4; i += nthr) {
+    const float v = i < M ? __ldg(sc + i) : -INFINITY;  // pad: never selected (K <= M)
+    stage[i] = v;
+    if (i < M) atomicAdd(&hist[score_key(v) >> 21], 1u);
+  }
+  __syncthreads();
+  if (K > 0)
+    select_topk_shared(sc, M, hist, K, selbm, cd, p.cand_cap, red, nullptr, stage, nullptr, true);
+  else
+    for (int w = tid; w < (M + 31) >> 5; w += nthr) selbm[w] = 0u;
+  __syncthreads();
+  // ascending selected positions (sel_ids) and the token union with residents
+  const int Wsel = (M + 31) >> 5;
+  {
+    const int per = (Wsel + nthr - 1) / nthr;
+    const int w0 = min(Wsel, tid * per), w1 = min(Wsel, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(selbm[w]);
+    int tot;
+    int pos = block_excl_scan(cnt, red, &tot);
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = selbm[w];
+      while (bits) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (pos < K) p.sel_ids[(size_t)b * p.K + pos] = w * 32 + bit;
+        ++pos;
+      }
+    }
+  }
+  if (!p.token_ids) return;
+  const uint32_t* rb = p.res_bitmap + (size_t)b * p.W;
+  for (int w = tid; w < p.W; w += nthr) tbm[w] = p.with_residents ? rb[w] : 0u;
+  __syncthreads();
+  const int32_t* ct = p.cand_tok + (size_t)b * p.M_stride;
+  for (int i = tid; i < M; i += nthr)
+    if ((selbm[i >> 5] >> (i & 31)) & 1u) {
+      const int t = ct[i];
+      atomicOr(&tbm[t >> 5], 1u << (t & 31));
+    }
+  __syncthreads();
+  const int wpt = (p.W + nthr - 1) / nthr;
+  const int w0 = tid * wpt;
+  int cnt = 0;
+  for (int w = w0; w < w0 + wpt && w < p.W; ++w) cnt += __popc(tbm[w]);
+  int total;
+  int pos = block_excl_scan(cnt, red, &total);
+  int32_t* dst = p.token_ids + (size_t)b * p.cap;
+  for (int w = w0; w < w0 + wpt && w < p.W; ++w) {
+    uint32_t bits = tbm[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      if (pos < p.cap) dst[pos] = w * 32 + bit;
+      ++pos;
+    }
+  }
+  if (tid == 0) {
+    p.n_tokens[b] = total < p.cap ? total : p.cap;
+    if (total > p.cap && p.err_flag) atomicOr(p.err_flag, 1);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -891,6 +983,25 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
     p.cand_cap = (int)std::min<size_t>(room / 4, 16384);
     if (p.cand_cap < 256) p.hist = nullptr;
     else smem += (size_t)p.cand_cap * 4;
+  }
+  // Appendix-E token top-k (mode 1, no rank order): the fused selection
+  if (a.mode == 1 && !a.rank_order && !a.sel_scores && a.token_ids) {
+    const size_t Wm = ((size_t)(a.M_stride + 31) / 32 + 3) & ~size_t(3);
+    size_t fs = (size_t)((a.M_stride + 3) & ~3) * 4 + kFuseHistBins * 4 + Wm * 4 +
+                (size_t)((s->W + 3) & ~3) * 4;
+    fs = (fs + 15) & ~size_t(15);
+    const size_t room = 220 * 1024 > fs ? 220 * 1024 - fs : 0;
+    const int ccap = (int)std::min<size_t>(room / 8, 8192);
+#ifndef KVB_EXP_OLDSEL
+    if (ccap >= 1024) {
+      p.cand_cap = ccap;
+      fs += (size_t)ccap * 8;
+      ensure_smem((const void*)k2_select_fuse, fs);
+      count_launch();
+      void* args[] = {&p};
+      return launch_pdl((const void*)k2_select_fuse, dim3(s->d.batch), dim3(kSelThreads), fs, st, args);
+    }
+#endif
   }
   ensure_smem((const void*)k2_select, smem);
   count_launch();
