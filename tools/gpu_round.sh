@@ -23,5 +23,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1h
   -o $O/prof_pb python bench.py --variant proposed_b --profile-steps 2 --layers 2 --also "" > $O/ncu_pb.log 2>&1
 timeout 600 python bench.py --variant proposed_b --steps 10 --warmup 3 --also "" > $O/bench_pb.json 2>&1
 timeout 600 python bench.py --variant higgs4c2 --steps 10 --warmup 3 --also "" > $O/bench_h4.json 2>&1
-TOOLS=racecheck RACE_N=1024 bash tools/gpu_sanitize.sh $TAG/san > /dev/null 2>&1
+bash tools/gpu_sanitize.sh $TAG/san > $O/sanitize.log 2>&1
 ls $O
