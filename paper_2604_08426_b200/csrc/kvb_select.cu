@@ -407,12 +407,21 @@ __global__ void __launch_bounds__(kSelThreads) k2_select_fuse(SelParams p) {
   uint32_t* tbm = selbm + ((Wm + 3) & ~3);
   uint64_t* cd = reinterpret_cast<uint64_t*>(tbm + ((p.W + 3) & ~3));
   for (int i = tid; i < kFuseHistBins; i += nthr) hist[i] = 0u;
-  __syncthreads();
-  for (int i = tid; i < M4; i += nthr) {
-    const float v = i < M ? __ldg(sc + i) : -INFINITY;  // pad: never selected (K <= M)
-    stage[i] = v;
-    if (i < M) atomicAdd(&hist[score_key(v) >> 21], 1u);
+  // stage the scores with every load of a thread in flight (a load -> store ->
+  // atomic chain per score was L2-latency bound), then the histogram from smem
+  if ((reinterpret_cast<uintptr_t>(sc) & 15) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(sc);
+    float4* d4 = reinterpret_cast<float4*>(stage);
+    const int n4 = M >> 2;
+#pragma unroll 4
+    for (int i = tid; i < n4; i += nthr) d4[i] = __ldg(s4 + i);
+    for (int i = 4 * n4 + tid; i < M4; i += nthr) stage[i] = i < M ? __ldg(sc + i) : -INFINITY;
+  } else {
+#pragma unroll 4
+    for (int i = tid; i < M4; i += nthr) stage[i] = i < M ? __ldg(sc + i) : -INFINITY;
   }
+  __syncthreads();
+  for (int i = tid; i < M; i += nthr) atomicAdd(&hist[score_key(stage[i]) >> 21], 1u);
   __syncthreads();
   if (K > 0)
     select_topk_shared(sc, M, hist, K, selbm, cd, p.cand_cap, red, nullptr, stage, nullptr, true);
@@ -443,11 +452,11 @@ __global__ void __launch_bounds__(kSelThreads) k2_select_fuse(SelParams p) {
   for (int w = tid; w < p.W; w += nthr) tbm[w] = p.with_residents ? rb[w] : 0u;
   __syncthreads();
   const int32_t* ct = p.cand_tok + (size_t)b * p.M_stride;
-  for (int i = tid; i < M; i += nthr)
-    if ((selbm[i >> 5] >> (i & 31)) & 1u) {
-      const int t = ct[i];
-      atomicOr(&tbm[t >> 5], 1u << (t & 31));
-    }
+#pragma unroll 4
+  for (int i = tid; i < M; i += nthr) {
+    const int t = __ldg(ct + i);  // coalesced, independent of the selection bit
+    if ((selbm[i >> 5] >> (i & 31)) & 1u) atomicOr(&tbm[t >> 5], 1u << (t & 31));
+  }
   __syncthreads();
   const int wpt = (p.W + nthr - 1) / nthr;
   const int w0 = tid * wpt;
