@@ -650,9 +650,21 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
                                                const uint16_t* __restrict__ right,
                                                float* __restrict__ q2, float* __restrict__ qt2,
                                                int H, int G, int D, int r, int sgroups,
-                                               int* __restrict__ counters, uint64_t* tr) {
+                                               int* __restrict__ counters, uint64_t* tr,
+                                               int32_t* __restrict__ pdone) {
   extern __shared__ float fsm[];
   const int b = blockIdx.y, h = blockIdx.x;
+  // decode step: this CTA's q2 / q~ / ticket writes are visible to the
+  // attention CTAs of sequence b, which spin on the count (the scan that runs
+  // beside this kernel never waits for it)
+  auto publish = [&]() {
+    if (!pdone) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(pdone + b, 1);
+    }
+  };
   // profiling (kvb_trace_enable): per-CTA entry / PDL wait passed / exit
   if (tr) tr += kTracePrep + 4 * (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
   auto stamp = [&](int k) {
@@ -683,7 +695,10 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
       q2[(size_t)b * HG * D + ((size_t)(d >> 1) * HG + h * G + g) * 2 + (d & 1)] = v;
     }
   }
-  if (!right) return;
+  if (!right) {
+    publish();
+    return;
+  }
   const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
   float* rsm = fsm + G * D;         // [r][D+1] (rows r0..r1 used)
   const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
@@ -720,6 +735,7 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
     for (int d = 0; d < D; ++d) acc = fmaf(rw[d], qq[d], acc);
     qt2[(size_t)b * HG * r + ((size_t)(rr >> 1) * HG + h * G + g) * 2 + (rr & 1)] = acc;
   }
+  publish();
   stamp(2);
 }
 
@@ -819,14 +835,18 @@ AttWs carve_att_ws(const kvb_store* s, const AttendLaunch& a, const AttGeom& geo
 
 }  // namespace
 
-cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl) {
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl,
+                               int32_t* pdone, int* ctas_per_seq) {
   const int B = s->d.batch, H = s->d.kv_heads, D = s->d.head_dim, G = a.G;
   AttGeom geo = attend_geometry(s, G, a.cap);
   AttWs w = carve_att_ws(s, a, geo);
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
   const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
-  ensure_smem((const void*)k5_prep, fs);
+#ifndef KVB_PREP_CARVE
+#define KVB_PREP_CARVE -1
+#endif
+  ensure_smem((const void*)k5_prep, fs, KVB_PREP_CARVE);
   count_launch();
   const float* q = a.q;
   const uint16_t* right = svd ? s->svd_right : nullptr;
@@ -836,8 +856,9 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   int* ctr = w.counters;
   uint64_t* tr = trace_buffer();
   void* args[] = {(void*)&q, (void*)&right, (void*)&q2, (void*)&qt2, (void*)&Hh, (void*)&Gg,
-                  (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr, (void*)&tr};
+                  (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr, (void*)&tr, (void*)&pdone};
   const dim3 grid(H, B, svd ? 4 : 1);
+  if (ctas_per_seq) *ctas_per_seq = pdone ? (int)(grid.x * grid.z) : 0;
   if (pdl) return launch_pdl((const void*)k5_prep, grid, dim3(256), fs, st, args);
   return cudaLaunchKernel((const void*)k5_prep, grid, dim3(256), args, fs, st);
 }

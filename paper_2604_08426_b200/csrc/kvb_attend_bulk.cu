@@ -104,6 +104,7 @@ struct BulkParams {
   int nB;                     // batch (grid y of the split-K launch)
   const int32_t* scan_done;   // decode step: finished scan CTAs per sequence (spin instead of PDL wait)
   int scan_ctas;              // scan CTAs per sequence
+  int prep_ctas;              // prep CTAs per sequence counted in scan_done[nB + b] (0: none)
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -314,10 +315,12 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     __shared__ int s_go;
     if (tid == 0) {
       const int* cnt = p.scan_done + b;
+      const int* pcnt = p.scan_done + p.nB + b;
       for (long long it = 0;; ++it) {
-        int v;
+        int v, w = p.prep_ctas;
         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-        if (v >= p.scan_ctas) break;
+        if (p.prep_ctas) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(w) : "l"(pcnt) : "memory");
+        if (v >= p.scan_ctas && w >= p.prep_ctas) break;
         if (it > (1ll << 24)) __trap();  // a lost count must fail the launch, not hang
         __nanosleep(20);
       }
@@ -905,7 +908,10 @@ __global__ void __launch_bounds__(128, KVB_MERGE_MINB) k5_merge_rows(const float
   // the attention (complete) was the last reader of the scan's histogram
   if (hist_clear && row == 0)
     for (int i = d; i < kFuseHistBins; i += blockDim.x) hist_clear[(size_t)b * kFuseHistBins + i] = 0u;
-  if (done_clear && row == 0 && d == 0) done_clear[b] = 0;  // every attention CTA has passed its spin
+  if (done_clear && row == 0 && d == 0) {  // every attention CTA has passed its spin
+    done_clear[b] = 0;                      // scan CTAs
+    done_clear[gridDim.y + b] = 0;          // prep CTAs
+  }
   const size_t base = (size_t)b * S * HG + row;
   float m = -INFINITY, acc = 0.f, L = 0.f;
 #ifndef KVB_MERGE_CH
@@ -1095,6 +1101,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
   p.scan_done = nullptr;
 #endif
   p.scan_ctas = s->scan_ctas;
+  p.prep_ctas = p.scan_done ? s->prep_ctas : 0;
   if (!fn) return cudaErrorNotSupported;
   ensure_smem(fn, g.smem);
   void* args[] = {&p};

@@ -42,6 +42,36 @@ __device__ __forceinline__ void fuse_threshold(const uint32_t* hb, int K, int* r
   const int tid = threadIdx.x;
   const int per = (kFuseHistBins + blockDim.x - 1) / blockDim.x;
   const int i0 = tid * per, i1 = min(kFuseHistBins, i0 + per);
+  constexpr int kRun = 8;  // bins per thread kept in registers (blocks of >= 256 threads)
+  if (per <= kRun) {
+    // one round of independent loads; the owner of the crossing searches its
+    // run in registers (a load per step would put up to 8 dependent L2 round
+    // trips on the selection's critical path)
+    uint32_t cv[kRun];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      const int i = i0 + q;
+      cv[q] = (q < per && i < i1) ? ld_hist(hb, kFuseHistBins - 1 - i, hb_shared) : 0u;
+      loc += (int)cv[q];
+    }
+    int tot;
+    int above = block_excl_scan(loc, red, &tot);
+    if (above < K && K <= above + loc) {
+      bool found = false;
+#pragma unroll
+      for (int q = 0; q < kRun; ++q) {
+        if (!found && above + (int)cv[q] >= K) {
+          *s_tb = kFuseHistBins - 1 - (i0 + q);
+          *s_kb = K - above;
+          found = true;
+        }
+        if (!found) above += (int)cv[q];
+      }
+    }
+    __syncthreads();
+    return;
+  }
   int loc = 0;
 #pragma unroll 8
   for (int i = i0; i < i1; ++i) loc += (int)ld_hist(hb, kFuseHistBins - 1 - i, hb_shared);

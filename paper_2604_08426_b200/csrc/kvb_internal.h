@@ -41,8 +41,10 @@ struct kvb_store {
   // by K2b after use (no memset nodes in the decode step). One decode step per
   // store at a time (the store's side stream and events are per store too).
   uint32_t* k2_hist = nullptr;     // [B][2048] top-11-bit key histogram
-  int32_t* scan_done = nullptr;    // [B] finished scan CTAs per sequence (decode step; reset by the merge)
+  int32_t* scan_done = nullptr;    // [2][B] finished scan CTAs, then finished prep CTAs, per
+                                   // sequence (decode step; reset by the merge)
   int scan_ctas = 0;               // scan CTAs per sequence of the last histogram scan launch
+  int prep_ctas = 0;               // prep CTAs per sequence publishing into scan_done[B + b] (0: none)
   int32_t* k2_meta = nullptr;      // [B][4] threshold bin / counts
   int32_t* k2_overflow = nullptr;  // [B]
   bool k2_dirty = false;           // a failed launch may have left scratch dirty
@@ -90,7 +92,9 @@ constexpr int64_t kTracePrep = 12288;  // decode prep: [CTA][4] entry / waited /
 constexpr int64_t kTraceAttExit = 16384;  // bulk attention: [CTA] exit
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size).
-cudaError_t ensure_smem(const void* func, size_t bytes);
+// carveout: preferred shared-memory carveout in percent (set once per kernel;
+// -1 = maximum shared, the default for every kernel of the decode chain)
+cudaError_t ensure_smem(const void* func, size_t bytes, int carveout = -1);
 // Number of SMs of the current device and resident CTAs/SM for a kernel.
 int sm_count();
 int resident_ctas(const void* func, int threads, size_t smem);
@@ -230,7 +234,10 @@ cudaError_t launch_attend_chunks(const kvb_store* s, const AttendLaunch& a, cons
                                  uint32_t* sel_hist = nullptr, int32_t* chunk_out = nullptr,
                                  const float* svd_logits = nullptr);
 // the two halves of launch_attend: per-step query prep, then the attention
-cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl = false);
+// pdone (decode step, may be null): per-sequence counter each prep CTA
+// increments once q~ / q2 / tickets are written; *ctas_per_seq receives the count
+cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaStream_t st, bool pdl = false,
+                               int32_t* pdone = nullptr, int* ctas_per_seq = nullptr);
 cudaError_t launch_attend_main(const kvb_store* s, const AttendLaunch& a, cudaStream_t st);
 cudaError_t launch_merge_attention(const float* out_p, const float* lse_p, int parts, int rows,
                                    int D, float* out, float* lse, cudaStream_t st,
