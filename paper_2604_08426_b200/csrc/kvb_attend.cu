@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
     return;
   }
   const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
-  float* rsm = fsm + G * D;         // [r][D+1] (rows r0..r1 used)
+  float* rsm = fsm + G * D;         // [r1 - r0][D+1]: this CTA's rows only
   const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
   const int Dg = hpg * D;
   const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
       const int rr = r0 + i / cpr, c = i % cpr;
       const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
       const __half2* hv = reinterpret_cast<const __half2*>(&u);
-      float* dst = rsm + rr * (D + 1) + c * 8;
+      float* dst = rsm + (rr - r0) * (D + 1) + c * 8;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __half22float2(hv[k]);
@@ -722,13 +722,13 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
   } else {
     for (int i = threadIdx.x; i < (r1 - r0) * D; i += blockDim.x) {
       const int rr = r0 + i / D, d = i % D;
-      rsm[rr * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+      rsm[(rr - r0) * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
     }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < (r1 - r0) * G; o += blockDim.x) {
     const int g = o / (r1 - r0), rr = r0 + o % (r1 - r0);
-    const float* rw = rsm + rr * (D + 1);
+    const float* rw = rsm + (rr - r0) * (D + 1);
     const float* qq = qs + g * D;
     float acc = 0.f;
 #pragma unroll 8
@@ -842,11 +842,13 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   AttWs w = carve_att_ws(s, a, geo);
   const bool svd = s->d.slow_kind == KVB_SLOW_SVD;
   const int r = svd ? s->d.svd_rank : 0;
-  const size_t fs = sizeof(float) * ((size_t)G * D + (svd ? (size_t)r * (D + 1) : 0));
-#ifndef KVB_PREP_CARVE
-#define KVB_PREP_CARVE -1
-#endif
-  ensure_smem((const void*)k5_prep, fs, KVB_PREP_CARVE);
+  // per CTA: q [G][D] + its share of the rank rows (r / 4 rounded to even, +2)
+  const int nrs = svd ? 4 : 1;
+  const size_t rows = svd ? (size_t)((r + nrs - 1) / nrs + 2) : 0;
+  const size_t fs = sizeof(float) * ((size_t)G * D + rows * (D + 1));
+  // the scan's 25% split: the prep's CTAs (<= 24 KB shared) run beside the
+  // decode step's scan CTAs instead of holding SMs in another split
+  ensure_smem((const void*)k5_prep, fs, 25);
   count_launch();
   const float* q = a.q;
   const uint16_t* right = svd ? s->svd_right : nullptr;
@@ -857,7 +859,7 @@ cudaError_t launch_attend_prep(const kvb_store* s, const AttendLaunch& a, cudaSt
   uint64_t* tr = trace_buffer();
   void* args[] = {(void*)&q, (void*)&right, (void*)&q2, (void*)&qt2, (void*)&Hh, (void*)&Gg,
                   (void*)&Dd, (void*)&rr, (void*)&sg, (void*)&ctr, (void*)&tr, (void*)&pdone};
-  const dim3 grid(H, B, svd ? 4 : 1);
+  const dim3 grid(H, B, nrs);
   if (ctas_per_seq) *ctas_per_seq = pdone ? (int)(grid.x * grid.z) : 0;
   if (pdl) return launch_pdl((const void*)k5_prep, grid, dim3(256), fs, st, args);
   return cudaLaunchKernel((const void*)k5_prep, grid, dim3(256), args, fs, st);
