@@ -368,12 +368,8 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
     // stage the sequence's scores in the ring's tail by bulk copies (overlaps
     // the threshold search) when they fit beside >= 4096 candidate slots
     const size_t sbytes = (size_t)p.C * 4;
-#ifdef KVB_NO_STAGE
-    const bool staged = false;
-#else
     const bool staged = (sbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(scs) & 15) == 0) &&
                         used + sbytes + 4096 * 8 <= ring_bytes;
-#endif
     __shared__ __align__(8) uint64_t stage_bar;
     float* stage = staged ? reinterpret_cast<float*>(pro + ring_bytes - sbytes) : nullptr;
     if (staged && tid == 0) {
@@ -1095,11 +1091,7 @@ cudaError_t launch_attend_bulk(const kvb_store* s, const BulkLaunch& a, cudaStre
 #undef KVB_BULK_VAR
   dim3 grid(g.splits, B);
   p.nB = B;
-#ifndef KVB_EXP_NOSPIN
   p.scan_done = (var == 2 && s->scan_ctas > 0) ? s->scan_done : nullptr;
-#else
-  p.scan_done = nullptr;
-#endif
   p.scan_ctas = s->scan_ctas;
   p.prep_ctas = p.scan_done ? s->prep_ctas : 0;
   if (!fn) return cudaErrorNotSupported;

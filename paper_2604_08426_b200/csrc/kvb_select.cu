@@ -1001,7 +1001,6 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
     fs = (fs + 15) & ~size_t(15);
     const size_t room = 220 * 1024 > fs ? 220 * 1024 - fs : 0;
     const int ccap = (int)std::min<size_t>(room / 8, 8192);
-#ifndef KVB_EXP_OLDSEL
     if (ccap >= 1024) {
       p.cand_cap = ccap;
       fs += (size_t)ccap * 8;
@@ -1010,7 +1009,6 @@ cudaError_t launch_select(const kvb_store* s, const SelectLaunch& a, cudaStream_
       void* args[] = {&p};
       return launch_pdl((const void*)k2_select_fuse, dim3(s->d.batch), dim3(kSelThreads), fs, st, args);
     }
-#endif
   }
   ensure_smem((const void*)k2_select, smem);
   count_launch();
