@@ -675,6 +675,38 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
     }
   };
   stamp(0);
+  const int rs = blockIdx.z, nrs = gridDim.z;  // this CTA folds rows [r0, r1)
+  const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
+  float* rsm = fsm + G * D;         // [r1 - r0][D+1]: this CTA's rows only
+  // the factor rows are store state, independent of the previous layer:
+  // stage them before the PDL wait, while the previous layer's merge leaves
+  // HBM idle (under the scan they would queue behind its stream)
+  if (right) {
+    const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
+    const int Dg = hpg * D;
+    const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
+    if ((D % 8) == 0 && (Dg % 8) == 0 && (col0 % 8) == 0) {
+      const int cpr = D / 8;  // 16-byte chunks per row
+#pragma unroll 4
+      for (int i = threadIdx.x; i < (r1 - r0) * cpr; i += blockDim.x) {
+        const int rr = r0 + i / cpr, c = i % cpr;
+        const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
+        const __half2* hv = reinterpret_cast<const __half2*>(&u);
+        float* dst = rsm + (rr - r0) * (D + 1) + c * 8;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(hv[k]);
+          dst[2 * k] = f.x;
+          dst[2 * k + 1] = f.y;
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < (r1 - r0) * D; i += blockDim.x) {
+        const int rr = r0 + i / D, d = i % D;
+        rsm[(rr - r0) * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
+      }
+    }
+  }
   // decode step: PDL-launched behind the previous layer -- wait for it before
   // touching q, then let the PDL-launched scan start beside this kernel
   pdl_wait();
@@ -683,7 +715,6 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
   // split tickets of the attention that follows (self-resetting; zeroed here
   // so a fresh caller workspace needs no memset)
   if (counters && h == 0 && blockIdx.z == 0 && threadIdx.x == 0) counters[b] = 0;
-  const int rs = blockIdx.z, nrs = gridDim.z;  // this CTA folds rows [r0, r1)
   const int HG = H * G;
   float* qs = fsm;                 // [G][D]
   const float* qb = q + ((size_t)b * H + h) * G * D;
@@ -698,32 +729,6 @@ __global__ void __launch_bounds__(256) k5_prep(const float* __restrict__ q,
   if (!right) {
     publish();
     return;
-  }
-  const int r0 = (r * rs / nrs) & ~1, r1 = rs == nrs - 1 ? r : (r * (rs + 1) / nrs) & ~1;
-  float* rsm = fsm + G * D;         // [r1 - r0][D+1]: this CTA's rows only
-  const int hpg = H / sgroups, grp = h / hpg, col0 = (h % hpg) * D;
-  const int Dg = hpg * D;
-  const uint16_t* rb = right + ((size_t)b * sgroups + grp) * r * Dg + col0;
-  if ((D % 8) == 0 && (Dg % 8) == 0 && (col0 % 8) == 0) {
-    const int cpr = D / 8;  // 16-byte chunks per row
-#pragma unroll 4
-    for (int i = threadIdx.x; i < (r1 - r0) * cpr; i += blockDim.x) {
-      const int rr = r0 + i / cpr, c = i % cpr;
-      const uint4 u = *reinterpret_cast<const uint4*>(rb + (size_t)rr * Dg + c * 8);
-      const __half2* hv = reinterpret_cast<const __half2*>(&u);
-      float* dst = rsm + (rr - r0) * (D + 1) + c * 8;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(hv[k]);
-        dst[2 * k] = f.x;
-        dst[2 * k + 1] = f.y;
-      }
-    }
-  } else {
-    for (int i = threadIdx.x; i < (r1 - r0) * D; i += blockDim.x) {
-      const int rr = r0 + i / D, d = i % D;
-      rsm[(rr - r0) * (D + 1) + d] = __half2float(__ushort_as_half(rb[(size_t)rr * Dg + d]));
-    }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < (r1 - r0) * G; o += blockDim.x) {

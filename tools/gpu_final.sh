@@ -13,7 +13,7 @@ timeout 1200 python bench.py --steps 30 --warmup 3 > $O/bench.json 2> $O/bench.e
 timeout 600 python bench.py --variant proposed_b --steps 10 --warmup 3 --also "" --no-cpu-baseline > $O/bench_pb.json 2>&1
 timeout 600 python bench.py --variant higgs4c2 --steps 10 --warmup 3 --also "" --no-cpu-baseline > $O/bench_h4.json 2>&1
 timeout 300 python tools/trace_chain.py > $O/trace_chain.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k1|k2|k3|k5|prep|merge" -c 60 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k1_|k2a|k2b|k3_|k5_" -c 60 --csv \
   --log-file $O/launches.csv python bench.py --profile-steps 2 --layers 4 --also "" > $O/launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_dense_sum|k5_attend_bulk|k5_merge|k5_prep" -s 8 -c 4 \
   -o $O/prof python bench.py --profile-steps 3 --layers 2 --also "" > $O/ncu.log 2>&1
