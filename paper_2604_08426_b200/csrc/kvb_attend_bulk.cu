@@ -291,7 +291,9 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   // Same slot / owner mapping as produce() for k < pre_done (it skips them).
   int pre_done = 0;
   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
+#ifndef KVB_NO_PRESTAGE
     pre_done = min(min(2, n_rloc / ett), nst - 1);
+#endif
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
       if (warp != H + k % kBProducers) continue;  // tile k's producer warp
