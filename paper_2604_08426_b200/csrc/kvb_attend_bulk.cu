@@ -291,9 +291,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
   // Same slot / owner mapping as produce() for k < pre_done (it skips them).
   int pre_done = 0;
   if (VAR == 2 && p.mode == 1 && p.sel_scores) {
-#ifndef KVB_NO_PRESTAGE
     pre_done = min(min(2, n_rloc / ett), nst - 1);
-#endif
     const int vbytes0 = H * kBD * 2;
     for (int k = 0; k < pre_done; ++k) {
       if (warp != H + k % kBProducers) continue;  // tile k's producer warp
@@ -374,7 +372,10 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
                         used + sbytes + 4096 * 8 <= ring_bytes;
     __shared__ __align__(8) uint64_t stage_bar;
     float* stage = staged ? reinterpret_cast<float*>(pro + ring_bytes - sbytes) : nullptr;
-    if (staged && tid == 0) {
+    // issued by the first producer lane: consumer lane 0 has the q~ loads in
+    // flight, which its mbarrier-init fence would wait for
+    const int stid = H * 32;
+    if (staged && tid == stid) {
       mbar_init(&stage_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
       mbar_arrive_tx(&stage_bar, (uint32_t)sbytes);
@@ -390,7 +391,7 @@ __device__ __forceinline__ void attend_item(const BulkParams& p, const int b, co
                        p.trace ? p.trace + (size_t)p.nB * S * 8 + 64 + ((size_t)b * S + split) * 8
                                : nullptr,
                        stage, staged ? &stage_bar : nullptr);
-    if (staged && tid == 0)  // all threads waited on it inside (and synced after)
+    if (staged && tid == stid)  // all threads waited on it inside (and synced after)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(saddr(&stage_bar)) : "memory");
     const int per = (p.Wc + nthr - 1) / nthr;
     const int w0 = min(p.Wc, tid * per), w1 = min(p.Wc, w0 + per);

@@ -195,16 +195,7 @@ k1_dense_sum(const T* __restrict__ lm, const float* __restrict__ q, float* __res
       if (c + r >= C) break;
       const float x = warp_sum_butterfly(a[r]);
       if (lane == 0) {
-#ifdef KVB_SCORE_EVL
-        {
-          uint64_t pol;
-          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-          asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(out + c + r), "f"(x), "l"(pol)
-                       : "memory");
-        }
-#else
         out[c + r] = x;
-#endif
         if (hist) atomicAdd(&shist[score_key(x) >> 21], 1u);
       }
     }
