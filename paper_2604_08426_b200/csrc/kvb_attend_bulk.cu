@@ -50,11 +50,12 @@ constexpr int kBMaxKs = 10;   // SVD rank <= 160
 constexpr int kBMaxStages = 8;
 constexpr float kLazy = 8.f;  // rescale threshold (natural-log units)
 #ifndef KVB_BULK_PRODUCERS
-#define KVB_BULK_PRODUCERS 2
+#define KVB_BULK_PRODUCERS 3
 #endif
 // producer warps: each bulk copy is issued through a uniform-register
 // waterfall (~40 instructions), so one warp issues ~1 tile per us -- the
-// consumers' pace; two or more keep the ring ahead of them. Warps per CTA:
+// consumers' pace; three keep the ring ahead of them (C2: 1 / 2 / 3 / 4
+// producer warps 3011 / 3215 / 3240 / 3234 tok/s, interleaved on one box). Warps per CTA:
 // H consumers + producers <= 12 (3 per SM sub-partition at <= 168 registers).
 constexpr int kBProducers = KVB_BULK_PRODUCERS;
 
