@@ -1,3 +1,5 @@
+# Final-build evidence: smoke, GPU suite, C2 bench line (+ variants), Proposed-B / HIGGS4@2 lines, chain trace.
+# Usage: bash tools/gpu_final_bench.sh  (writes gpurun_out/r02f)
 set -u
 O=gpurun_out/r02f; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
